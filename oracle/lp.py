@@ -1,0 +1,109 @@
+"""Independent ground truths used to PIN the oracle (TEST INFRASTRUCTURE ONLY).
+
+None of these calls Algorithm 1: they are closed forms and brute-force linear
+programs for cases where eq:Unbal_OT_beckman has an exact
+solution by other means.  Citations: P:nnn = PAPER.md line, S:nnn = SPEC.md line.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+
+
+def w1_1d(p, q):
+    """Balanced 1-D Beckmann (eq:OT_beckman) on a 1 x n grid:
+    div M = M_i - M_{i-1} = q_i - p_i fixes M uniquely as a prefix sum, so
+    W = sum_i |sum_{j<=i} (q_j - p_j)|."""
+    p, q = np.asarray(p, float), np.asarray(q, float)
+    if abs(p.sum() - q.sum()) > 1e-9 * max(1.0, abs(p.sum())):
+        raise ValueError("unbalanced input")
+    return float(np.abs(np.cumsum(q - p)[:-1]).sum())
+
+
+def two_delta(m_p, m_q, d, alpha):
+    """Two axis-aligned deltas at grid distance d: transport the
+    common mass min(m_p, m_q) at cost min(d, 2 alpha) per unit (moving costs d,
+    destroy+create costs 2 alpha) and pay alpha per unit of surplus."""
+    return min(m_p, m_q) * min(d, 2.0 * alpha) + alpha * abs(m_p - m_q)
+
+
+def uot_1d_enum(p, q, alpha):
+    """Exact optimum of eq:Unbal_OT_beckman on a 1 x n grid (p = 1, L6 unit
+    spacing) by exhaustive vertex enumeration, n <= 7.
+
+    Eliminating r = div M - f (f = q - p) leaves the convex piecewise-linear
+        F(M) = sum_{i<n-1} |M_i| + alpha sum_i |M_i - M_{i-1} - f_i|
+    in M in R^{n-1} (M_{-1} = M_{n-1} = 0).  A minimiser exists at a point where
+    n-1 linearly independent pieces vanish; enumerate all such choices."""
+    p, q = np.asarray(p, float), np.asarray(q, float)
+    n = p.size
+    f = q - p
+    m = n - 1
+    if m == 0:
+        return alpha * abs(f[0])
+    rows, rhs = [], []
+    for i in range(m):                       # |M_i| = 0
+        e = np.zeros(m); e[i] = 1.0
+        rows.append(e); rhs.append(0.0)
+    for i in range(n):                       # M_i - M_{i-1} - f_i = 0
+        e = np.zeros(m)
+        if i < m:
+            e[i] += 1.0
+        if i - 1 >= 0:
+            e[i - 1] -= 1.0
+        rows.append(e); rhs.append(f[i])
+    rows, rhs = np.array(rows), np.array(rhs)
+
+    def F(M):
+        Mf = np.concatenate([M, [0.0]])
+        Mp = np.concatenate([[0.0], M])
+        return np.abs(M).sum() + alpha * np.abs(Mf - Mp - f).sum()
+
+    best = np.inf
+    for S in itertools.combinations(range(len(rows)), m):
+        A = rows[list(S)]
+        if abs(np.linalg.det(A)) < 1e-12:
+            continue
+        M = np.linalg.solve(A, rhs[list(S)])
+        best = min(best, F(M))
+    return float(best)
+
+
+def uot_1d_linprog(p, q, alpha):
+    """Same LP as uot_1d_enum solved by scipy HiGHS (any n): variables
+    M = M+ - M-, r = r+ - r- >= 0;  min sum(M+ + M-) + alpha sum(r+ + r-)
+    s.t. M_i - M_{i-1} - r_i = q_i - p_i (eq:Unbal_OT_beckman with L1)."""
+    from scipy.optimize import linprog
+    p, q = np.asarray(p, float), np.asarray(q, float)
+    n = p.size
+    m = n - 1
+    nv = 2 * m + 2 * n
+    c = np.concatenate([np.ones(2 * m), alpha * np.ones(2 * n)])
+    A = np.zeros((n, nv))
+    for i in range(n):
+        if i < m:
+            A[i, i] += 1.0; A[i, m + i] -= 1.0
+        if i - 1 >= 0:
+            A[i, i - 1] -= 1.0; A[i, m + i - 1] += 1.0
+        A[i, 2 * m + i] -= 1.0; A[i, 2 * m + n + i] += 1.0
+    res = linprog(c, A_eq=A, b_eq=q - p, bounds=(0, None), method="highs")
+    assert res.status == 0, res.message
+    return float(res.fun)
+
+
+def laplacian_matrix(nx, ny):
+    """Explicit matrix of div o div^* built column by column from the
+    DEFINITION of div and its adjoint as the matrix transpose --
+    independent of the oracle's stencil code (used by pin P5)."""
+    N = nx * ny
+    nmx = [(j, i) for j in range(ny) for i in range(nx - 1)]   # existing Mx (L3)
+    nmy = [(j, i) for j in range(ny - 1) for i in range(nx)]   # existing My
+    D = np.zeros((N, len(nmx) + len(nmy)))
+    for c, (j, i) in enumerate(nmx):       # unit Mx[j,i]: +1 at (j,i), -1 at (j,i+1)
+        D[j * nx + i, c] += 1.0
+        D[j * nx + i + 1, c] -= 1.0
+    for c, (j, i) in enumerate(nmy):       # unit My[j,i]: +1 at (j,i), -1 at (j+1,i)
+        D[j * nx + i, len(nmx) + c] += 1.0
+        D[(j + 1) * nx + i, len(nmx) + c] -= 1.0
+    return D @ D.T, D
