@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark of the fused UOT iteration (Algorithm 1, arXiv 1909.00149) on B200.
+
+Metric (BASELINE.json): pixel-iterations/sec of the UOT prox step, with the
+achieved HBM GB/s of the fused iteration kernel vs the measured peak.
+
+A STEP is one full solve of the configured workload on this rank's pairs:
+cold start (uot_reset: zero state + f = x_{t+1} - x_t, row a0) followed by the
+config's iteration count of the fused kernel (rows a1-a6), residual/objective
+reductions every 10 iterations evaluated on the device with the stopping test
+(tol 1e-12, never met at these counts), and the report read back.
+px-it per step = pairs x N x iterations actually executed.
+
+Default workload: BASELINE configs[3] (C4: T=256 video, 1024^2, 255 pairs,
+500 iterations), the HBM-bound configuration that is sharded over 1/2/4/8
+GPUs; --config selects another.  Inputs (9.7 GB of state at N=1) exceed the
+126 MB L2, so no L2 flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+N>1: launched by torchrun, one process per GPU; contiguous pair ranges per
+rank ("strong" scaling: the config's total work is fixed); the shared
+boundary frame of each shard comes from the next rank over NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALG_BYTES_PER_PXIT = {"fixed": 36}   # read Mx,My,r,a,f; write Mx,My,r,a (fp32)
+METRIC = "pixel-iterations/sec of the UOT prox step; achieved HBM GB/s vs peak"
+UNIT = "px-it/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--iters", type=int, default=0, help="override the config's iteration count (testing only)")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--check-every", type=int, default=10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------ helpers
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def pair_range(n_pairs, world, rank):
+    from paper_1909_00149_b200.dist import shard_range
+    return shard_range(n_pairs, world, rank)
+
+
+def make_frames(cfg, f0, f1, rank_chain=None):
+    """Frames of chain 0 (or of the batched pairs), indices [f0, f1)."""
+    from paper_1909_00149_b200 import inputs
+    if cfg.name == "C4":
+        return inputs.gen_c4_frames(f0, f1)
+    if cfg.name == "C5":
+        return inputs.gen_c5(pairs=range(f0, f1))
+    full = inputs.generate(cfg.name)
+    if cfg.n_chains == 1:
+        return full[:, f0:f1]
+    return full[f0:f1]
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index):
+        self.dev = dev_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------ CPU oracle
+def cpu_oracle_rate(cfg, seconds_target=12.0):
+    """Oracle (oracle/, fp64 C, OpenMP over pairs) on a bounded sample of the workload.
+    Returns (px-it/s, cores used, sample description)."""
+    import numpy as np
+    import oracle
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    n_pairs = min(cfg.n_pairs, max(2, cores))
+    if cfg.n_chains == 1:
+        fr = np.ascontiguousarray(make_frames(cfg, 0, n_pairs + 1))
+    else:
+        fr = np.ascontiguousarray(make_frames(cfg, 0, n_pairs))
+    pairs = fr.shape[0] * (fr.shape[1] - 1)
+    N = cfg.nx * cfg.ny
+    t1 = oracle.default_steps(cfg.nx, cfg.ny, prox=False)[0]
+    # calibrate: 2 iterations, then size the sample to ~seconds_target
+    t0 = time.perf_counter()
+    oracle.iterate(fr, cfg.alpha, math.inf, t1, t1, 2)
+    dt = max(time.perf_counter() - t0, 1e-3)
+    its = int(max(2, min(cfg.iters, 2 * seconds_target / dt)))
+    t0 = time.perf_counter()
+    oracle.iterate(fr, cfg.alpha, math.inf, t1, t1, its)
+    dt = time.perf_counter() - t0
+    threads = min(int(os.environ.get("OMP_NUM_THREADS", cores)), pairs)
+    sample = f"{cfg.name}: {pairs} of {cfg.n_pairs} pairs x {N} px x {its} of {cfg.iters} iterations, fp64"
+    return pairs * N * its / dt, threads, sample, dt
+
+
+# ------------------------------------------------------------------------------------------ reference arm
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    rates = []
+    for k in range(args.warmup + args.steps):
+        rate, threads, sample, dt = cpu_oracle_rate(cfg, seconds_target=min(args.cpu_seconds, 8.0))
+        if k >= args.warmup:
+            rates.append((rate, dt))
+    value = sum(r for r, _ in rates) / len(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(d for _, d in rates) / len(rates),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators, paper_1909_00149_b200/inputs.py)",
+        "config": config_dict(cfg, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(cfg, gpus):
+    return {"workload": f"{cfg.name}: {cfg.note}", "B": cfg.n_chains, "T": cfg.n_frames, "pairs": cfg.n_pairs,
+            "ny": cfg.ny, "nx": cfg.nx, "iterations": cfg.iters, "alpha": cfg.alpha, "mode": "fixed marginals (rho=inf)",
+            "parallelism": f"frame-range shards x{gpus}" if gpus > 1 else "single GPU",
+            "l2": "inputs larger than L2 (no flush needed)" if cfg.n_pairs * cfg.nx * cfg.ny * 36 > 126e6 * 4
+            else "L2-resident workload (effective GB/s may exceed HBM peak)"}
+
+
+# ------------------------------------------------------------------------------------------ main arm
+def main():
+    args = parse()
+    from paper_1909_00149_b200 import inputs
+    cfg = inputs.CONFIGS[args.config]
+    if args.iters:
+        cfg = inputs.Config(**{**cfg.__dict__, "iters": args.iters})
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1909_00149_b200.uot import Problem
+    from paper_1909_00149_b200 import dist as udist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- this rank's shard: pairs [p0, p1) -> frames [p0, p1] (last = shared boundary frame)
+    p0, p1 = udist.shard_range(cfg.n_pairs, world, rank)
+    if cfg.n_chains == 1:
+        own = make_frames(cfg, p0, p1 if rank < world - 1 else p1 + 1)      # owned frames
+        host = torch.from_numpy(np.ascontiguousarray(own))
+        shape = (1, p1 - p0 + 1, cfg.ny, cfg.nx)
+    else:
+        own = make_frames(cfg, p0, p1)                                       # batched independent pairs
+        host = torch.from_numpy(np.ascontiguousarray(own))
+        shape = tuple(own.shape)
+    host_pinned = host.pin_memory()
+    frames = torch.empty(shape, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def upload(src_pinned):
+        """H2D of the owned frames + boundary frame from the next rank (NCCL)."""
+        n_own = src_pinned.shape[1] if cfg.n_chains == 1 else src_pinned.shape[0]
+        if cfg.n_chains == 1:
+            frames[:, :n_own].copy_(src_pinned, non_blocking=True)
+            if world > 1:
+                udist.exchange_boundary_frame(frames, rank, world)
+        else:
+            frames.copy_(src_pinned, non_blocking=True)
+
+    upload(host_pinned)
+    torch.cuda.synchronize(dev)
+    prob = Problem(frames, cfg.alpha, stream=stream)
+    G = prob.G
+    N = cfg.nx * cfg.ny
+
+    def step():
+        prob.reset()
+        rep = prob.solve(cfg.iters, tol=1e-12, check_every=args.check_every)
+        return rep
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # ---- timed region (device-resident inputs)
+    launches0 = prob.launches
+    prob.set_timing(True)
+    prob.get_timing()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters_done = 0
+    reps = []
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rep = step()
+            reps.append(rep)
+            iters_done += rep["iterations"]
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    kern_ms, kern_n = prob.get_timing()
+    prob.set_timing(False)
+    launches = prob.launches - launches0
+    ms_max = max_over_ranks(ms)
+    pxit_total = sum_over_ranks(float(G) * N * iters_done)
+    value = pxit_total / (ms_max / 1e3)
+
+    # ---- roofline of the dominant kernel (fused iteration), per launch
+    peak, peak_src = load_peaks()
+    alg_bytes_launch = ALG_BYTES_PER_PXIT["fixed"] * G * N
+    avg_launch_s = (kern_ms / max(kern_n, 1)) / 1e3
+    achieved = alg_bytes_launch / avg_launch_s / 1e9
+    traffic = None
+    prof_sum = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof_sum):
+        try:
+            d = json.load(open(prof_sum)).get(cfg.name)
+            if d:
+                traffic = d.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the public API with HOST buffers
+    e2e = None
+    if not args.no_e2e:
+        h2d = sum_over_ranks(float(host_pinned.numel() * 4))   # owned frames, all ranks
+        d2h = sum_over_ranks(32.0 * 8)                         # report readback (uot_solve), all ranks
+
+        def e2e_step():
+            upload(host_pinned)
+            prob.reset()
+            return prob.solve(cfg.iters, tol=1e-12, check_every=args.check_every)
+
+        for _ in range(max(1, args.warmup // 2)):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        it2 = 0
+        for _ in range(args.steps):
+            it2 += e2e_step()["iterations"]
+        e1.record(stream)
+        barrier()
+        ms2 = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": sum_over_ranks(float(G) * N * it2) / (ms2 / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "wall_s": time.perf_counter() - t0}
+
+    # ---- CPU oracle beside it (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            rate, threads, sample, _ = cpu_oracle_rate(cfg, args.cpu_seconds)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
+        except Exception as ex:   # the oracle is a reported baseline, not the product
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        last = reps[-1]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generators, paper_1909_00149_b200/inputs.py; no dataset in the paper's bench)",
+            "config": config_dict(cfg, world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_iter_fixed (fused Alg.1 iteration)",
+                         "alg_bytes_per_launch": alg_bytes_launch, "avg_launch_ms": avg_launch_s * 1e3,
+                         "launches_timed": kern_n, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "hbm_gbs_step": ALG_BYTES_PER_PXIT["fixed"] * value / 1e9,
+            "objective": last["objective"], "iterations_per_step": iters_done // args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,172 @@
+/*
+ * uot.h -- C-ABI of the B200 (sm_100a) hot path of arXiv 1909.00149:
+ * the per-iteration Chambolle-Pock update of Algorithm 1
+ * that evaluates / proxes the unbalanced Beckmann OT regulariser
+ * eq:Unbal_OT_beckman on pixel grids.
+ *
+ * Library: paper_1909_00149_b200/libuot_b200.so (extern "C", no C++ types,
+ * no exceptions across the ABI).  All compute runs in the library's CUDA
+ * kernels; there is no CPU fallback: without a CUDA device every compute
+ * entry point returns UOT_E_CUDA.
+ *
+ * Readings of the paper (sign of the constraint, rho convention, boundary,
+ * stopping rule, ...) are DESIGN.md L1..L21 and are cited as "Lnn".
+ *
+ * ---------------------------------------------------------------------------
+ * Problem.  A context holds B independent chains of T frames x_t (fp32,
+ * [B][T][ny][nx], C-contiguous, i = contiguous axis = paper index i, P:152,
+ * L5).  Each adjacent pair (t, t+1) carries one UOT term (eq:RPCA_UOTDF
+ * P:746-756, "T-1 OT problems"), pair g = b*(T-1) + t, with the
+ * constraint (L1)
+ *        div(M_g) - r_g = x_{t+1} - x_t          (north star: psi = -r)
+ * and the objective ||M_g||_{2,1} + alpha ||r_g||_1 (p = 1).
+ * Per pair the state is the flux M = (Mx, My) (Mx[:, nx-1] and
+ * My[ny-1, :] are pinned to 0, L3), the transport residual r and the
+ * dual a.  In prox mode (rho finite) the frames become variables x
+ * with centres p = frames (eq:Prox_UOT P:218-226, Alg.1 line 4 P:314, L2, L19).
+ *
+ * One iteration (Alg.1 lines 3-7), every right-hand side at
+ * iteration k (Jacobi, L10):
+ *   m_i <- shrink^{l2}_{tau1}(m_i - tau1 div^*(a)_i)
+ *   x   <- Pi_+((rho tau1 p + x - tau1 A^T a)/(1 + rho tau1))  (prox only)
+ *   r   <- shrink^{l1}_{alpha tau1}(r + tau1 a)
+ *   a   <- a + tau2 (2 K(M',r',x') - K(M,r,x)),  K = div M - r - x_{t+1} + x_t
+ *
+ * ---------------------------------------------------------------------------
+ */
+#ifndef UOT_B200_H
+#define UOT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes.  0/2/3 mirror the exit codes of SPEC.md S:477. */
+#define UOT_OK              0
+#define UOT_E_INVALID       2  /* bad argument; nothing was enqueued            */
+#define UOT_E_NOT_CONVERGED 3  /* uot_solve hit max_iters with tol > 0; state and report valid */
+#define UOT_E_NONFINITE     4  /* NaN/Inf seen in the reductions         */
+#define UOT_E_CUDA          5  /* CUDA error (incl. no device); see uot_last_error */
+
+/* uot_params.flags */
+#define UOT_FORCE_STEPS     1u /* accept tau1*tau2 >= 1/||K||^2 (Theorem 1 not satisfied) */
+/* uot_reset flags */
+#define UOT_RESET_X_FROM_P  1u /* prox mode: x^0 = max(p, 0) instead of 0 (L8)   */
+
+typedef struct uot_ctx uot_ctx;   /* opaque, host-side */
+
+typedef struct {
+    int32_t  nx, ny;       /* grid, >= 1 each; nx = contiguous axis            */
+    int32_t  n_chains;     /* B >= 1 independent chains (batched pairs: T = 2)                 */
+    int32_t  n_frames;     /* T >= 2 frames per chain held by this context (a shard's frames
+                              include the shared boundary frame)        */
+    double   alpha;        /* paper mu > 0; p = 1                               */
+    double   rho;          /* weight of (rho/2)||x - p||^2 as printed in Alg.1 line 4 (L2);
+                              +INFINITY = fixed marginals (x == frames, evaluation of eq:Unbal_OT_beckman) */
+    double   tau1, tau2;   /* primal / dual steps > 0; 0 = Theorem-1 default (uot_default_steps,
+                              safety 0.99)                                                      */
+    uint32_t flags;        /* UOT_FORCE_STEPS                                                   */
+} uot_params;
+
+/* Device buffers.  ALL are CALLER-OWNED device pointers (e.g. torch tensors),
+ * fp32 unless noted, C-contiguous; the library stores the pointers (they must
+ * outlive the context) and allocates nothing on the device.  P = T-1.
+ * 16-byte alignment and nx % 4 == 0 select the float4 kernels; otherwise a
+ * scalar-lane variant runs (same results up to fp32 rounding order).       */
+typedef struct {
+    const float* frames;   /* [B][T][ny][nx] x_t (fixed) or prox centres p_t                   */
+    float*  f;             /* [B][P][ny][nx] scratch: x_{t+1} - x_t (fixed mode)               */
+    float*  mx[2];         /* [B][P][ny][nx] ping-pong flux x-component                         */
+    float*  my[2];         /* [B][P][ny][nx] ping-pong flux y-component                         */
+    float*  r;             /* [B][P][ny][nx] transport residual (updated in place)              */
+    float*  a[2];          /* [B][P][ny][nx] ping-pong dual                                      */
+    float*  x[2];          /* [B][T][ny][nx] ping-pong frames (prox mode), NULL when rho = inf  */
+    const float* a_prev_halo; /* [B][ny][nx] dual of the pair preceding frame 0 (chain prox shard), or NULL = 0 */
+    const float* a_next_halo; /* [B][ny][nx] dual of the pair following frame T-1, or NULL = 0          */
+    double* scratch;       /* uot_scratch_doubles(&params) doubles (reduction partials, flags)  */
+} uot_buffers;
+
+/* Reductions (fp64) summed over this context's pairs, DESIGN.md "Reductions". */
+typedef struct {
+    double objective;      /* sum ||M||_{2,1} + alpha ||r||_1 (+ (rho/2)||x - p||^2 in prox mode) */
+    double transport;      /* sum ||M||_{2,1}                                      */
+    double growth;         /* sum alpha ||r||_1                                                  */
+    double prox_term;      /* (rho/2) sum ||x - p||^2 (0 in fixed mode)                         */
+    double primal_res;     /* ||K^{k+1}||_2, constraint violation (L13)                         */
+    double dual_res;       /* ||z^{k+1} - z^k||_2 / tau1, z = (M, r[, x]) (L13)                 */
+    double upper_bound;    /* sum ||M||_{2,1} + alpha ||div M - f||_1 >= V (feasible repair)   */
+    double lower_bound;    /* weak-duality bound <= V (uot_objective only, else NaN)           */
+    double f_norm;         /* ||x_{t+1} - x_t||_2 over all pairs (stopping scale)               */
+    int64_t iterations;    /* executions of Alg.1 lines 3-7 since the last uot_reset (L9)      */
+    int32_t converged;     /* uot_solve: 1 if the tol test passed                               */
+    int32_t nonfinite;     /* 1 if a NaN/Inf was seen                                           */
+} uot_report;
+
+/* Number of doubles the caller must provide in buffers.scratch. */
+size_t uot_scratch_doubles(const uot_params* params);
+
+/* Theorem-1 steps (L11/L12): tau1 = tau2 = sqrt(safety / ||K||^2),
+ * ||K||^2 = lambda_max(div div^*) + 1 (fixed), + 3 (pair prox, the paper's
+ * bound), + 3 + 2cos(pi/T) (chain prox of T frames); lambda_max =
+ * g(nx) + g(ny), g(n) = 2 + 2cos(pi/n) (n >= 2), g(1) = 0.  0 < safety < 1.
+ * Host-only, no device needed.  Returns UOT_OK or UOT_E_INVALID. */
+int uot_default_steps(const uot_params* params, double safety, double* tau1, double* tau2);
+
+/* Validate params/buffers, bind the stream (a cudaStream_t, NULL = legacy
+ * default stream) and create a context.  Enqueues nothing; call uot_reset.
+ * On error *out = NULL and a message is available from uot_last_error(NULL). */
+int uot_create(const uot_params* params, const uot_buffers* buffers, void* cuda_stream, uot_ctx** out);
+
+/* Cold start ("initialized to 0"): M = r = a = 0, x = 0 (or max(p,0)
+ * with UOT_RESET_X_FROM_P), f = x_{t+1} - x_t; iteration count 0.  Async. */
+int uot_reset(uot_ctx* ctx, uint32_t flags);
+
+/* Copy frames from HOST memory (pinned for async) into buffers.frames's
+ * device storage on the context stream and recompute f; the state is kept
+ * (warm start across outer iterations).  host_frames holds
+ * B*T*ny*nx floats in the same layout.  Async w.r.t. the host if pinned. */
+int uot_load_frames(uot_ctx* ctx, const float* host_frames);
+
+/* Run n_iters >= 0 iterations (Alg.1 lines 3-7).  out == NULL: fully async
+ * (graph-capturable, no host sync); out != NULL: the last iteration also
+ * computes the reductions and the call synchronises the stream to fill *out. */
+int uot_prox_step(uot_ctx* ctx, int32_t n_iters, uot_report* out);
+
+/* Iterate until primal_res <= tol*max(f_norm, 1e-30) and dual_res <= the same
+ * (L13), checking every check_every iterations ON THE DEVICE (no host sync in
+ * the loop: later launches exit immediately once converged), or until
+ * max_iters.  tol <= 0: run exactly max_iters.  Fills *out (may be NULL).
+ * Returns UOT_OK, UOT_E_NOT_CONVERGED (tol > 0 and not met), UOT_E_NONFINITE. */
+int uot_solve(uot_ctx* ctx, int32_t max_iters, double tol, int32_t check_every, uot_report* out);
+
+/* Objective and weak-duality certificate of the CURRENT state, per pair
+ * (DESIGN.md "Certificate"):  per_pair[g*8 + .] = {transport, sum|r|, U,
+ * <a,f>, max ||div^* a||, max |a|, L, objective}, L <= V_alpha <= U.
+ * per_pair may be NULL; out may be NULL.  Synchronises the stream. */
+int uot_objective(uot_ctx* ctx, double* per_pair, uot_report* out);
+
+/* Kernel timing for the roofline report (bench.py): enable != 0 brackets every
+ * fused-iteration kernel launch with a CUDA event pair on the context stream.
+ * uot_get_timing synchronises, returns the summed device time (ms) and the
+ * number of timed launches since the last call, and clears the record. */
+int uot_set_timing(uot_ctx* ctx, int enable);
+int uot_get_timing(uot_ctx* ctx, double* ms_total, int64_t* n_launches);
+
+/* Which ping-pong slot (0/1) of mx/my/a/x holds the current iterate. */
+int uot_state_slot(const uot_ctx* ctx);
+
+/* CUDA kernels launched by this context since creation (for accounting). */
+int64_t uot_launch_count(const uot_ctx* ctx);
+
+void uot_destroy(uot_ctx* ctx);
+
+/* Last error message of ctx (or of the last failed uot_create if ctx == NULL). */
+const char* uot_last_error(const uot_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UOT_B200_H */

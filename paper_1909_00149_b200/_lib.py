@@ -1,0 +1,100 @@
+"""ctypes binding of the C-ABI in include/uot.h (argument marshalling only).
+
+Loads the IN-TREE library ``paper_1909_00149_b200/libuot_b200.so``.  There is
+no fallback of any kind: if the library is missing or cannot be loaded, every
+entry point raises.  Every step of the hot path runs in the library's kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libuot_b200.so")
+
+UOT_OK = 0
+UOT_E_INVALID = 2
+UOT_E_NOT_CONVERGED = 3
+UOT_E_NONFINITE = 4
+UOT_E_CUDA = 5
+UOT_FORCE_STEPS = 1
+UOT_RESET_X_FROM_P = 1
+
+EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset", "uot_load_frames",
+            "uot_prox_step", "uot_solve", "uot_objective", "uot_set_timing", "uot_get_timing",
+            "uot_state_slot", "uot_launch_count",
+            "uot_destroy", "uot_last_error")
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("n_chains", ctypes.c_int32),
+                ("n_frames", ctypes.c_int32), ("alpha", ctypes.c_double), ("rho", ctypes.c_double),
+                ("tau1", ctypes.c_double), ("tau2", ctypes.c_double), ("flags", ctypes.c_uint32)]
+
+
+_fp = ctypes.c_void_p
+
+
+class Buffers(ctypes.Structure):
+    _fields_ = [("frames", _fp), ("f", _fp), ("mx", _fp * 2), ("my", _fp * 2), ("r", _fp),
+                ("a", _fp * 2), ("x", _fp * 2), ("a_prev_halo", _fp), ("a_next_halo", _fp),
+                ("scratch", _fp)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("objective", ctypes.c_double), ("transport", ctypes.c_double), ("growth", ctypes.c_double),
+                ("prox_term", ctypes.c_double), ("primal_res", ctypes.c_double), ("dual_res", ctypes.c_double),
+                ("upper_bound", ctypes.c_double), ("lower_bound", ctypes.c_double), ("f_norm", ctypes.c_double),
+                ("iterations", ctypes.c_int64), ("converged", ctypes.c_int32), ("nonfinite", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class UotError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"uot error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libuot_b200.so (raises if it is not built: no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_1909_00149_b200.build` "
+                           "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    P, B, R = ctypes.POINTER(Params), ctypes.POINTER(Buffers), ctypes.POINTER(Report)
+    ctx_pp = ctypes.POINTER(ctypes.c_void_p)
+    L.uot_scratch_doubles.argtypes = [P]; L.uot_scratch_doubles.restype = ctypes.c_size_t
+    L.uot_default_steps.argtypes = [P, ctypes.c_double, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    L.uot_default_steps.restype = ctypes.c_int
+    L.uot_create.argtypes = [P, B, ctypes.c_void_p, ctx_pp]; L.uot_create.restype = ctypes.c_int
+    L.uot_reset.argtypes = [ctypes.c_void_p, ctypes.c_uint32]; L.uot_reset.restype = ctypes.c_int
+    L.uot_load_frames.argtypes = [ctypes.c_void_p, ctypes.c_void_p]; L.uot_load_frames.restype = ctypes.c_int
+    L.uot_prox_step.argtypes = [ctypes.c_void_p, ctypes.c_int32, R]; L.uot_prox_step.restype = ctypes.c_int
+    L.uot_solve.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, R]
+    L.uot_solve.restype = ctypes.c_int
+    L.uot_objective.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), R]
+    L.uot_objective.restype = ctypes.c_int
+    L.uot_set_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]; L.uot_set_timing.restype = ctypes.c_int
+    L.uot_get_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+    L.uot_get_timing.restype = ctypes.c_int
+    L.uot_state_slot.argtypes = [ctypes.c_void_p]; L.uot_state_slot.restype = ctypes.c_int
+    L.uot_launch_count.argtypes = [ctypes.c_void_p]; L.uot_launch_count.restype = ctypes.c_int64
+    L.uot_destroy.argtypes = [ctypes.c_void_p]; L.uot_destroy.restype = None
+    L.uot_last_error.argtypes = [ctypes.c_void_p]; L.uot_last_error.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def check(rc, ctx=None, allow=()):
+    if rc == UOT_OK or rc in allow:
+        return rc
+    msg = lib().uot_last_error(ctx)
+    raise UotError(rc, msg.decode() if msg else "")

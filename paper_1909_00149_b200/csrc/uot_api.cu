@@ -1,0 +1,674 @@
+// uot_api.cu -- C-ABI (include/uot.h) over the sm_100a kernels of the fused
+// Algorithm-1 iteration (arXiv 1909.00149).
+//
+// The library owns no device memory: every buffer, including the fp64
+// reduction scratch, is caller-owned (PyTorch tensors in the Python binding).
+// Everything is enqueued on the stream bound at uot_create; host synchronisation
+// happens only when a host report is requested.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <new>
+#include <vector>
+
+#include "uot.h"
+#include "uot_kernels.cuh"
+
+using namespace uotk;
+
+// ============================================================================ kernels
+namespace uotk {
+
+// Fixed-order block reduction of one double (256 threads): warp butterfly, then
+// warp 0 over the 8 warp sums.  Same inputs -> same bits.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = (l < (int)(blockDim.x >> 5)) ? sh[l] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
+    }
+    return r;   // valid in thread 0
+}
+
+__device__ __forceinline__ double block_max(double v, double* sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = (l < (int)(blockDim.x >> 5)) ? sh[l] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(kFull, r, o));
+    }
+    return r;
+}
+
+__global__ void __launch_bounds__(256) k_setup_f(const SetupArgs S) {
+    __shared__ double sh[32];
+    const int g = blockIdx.y;
+    const int b = g / S.P, t = g % S.P;
+    const float* x0 = S.frames + ((size_t)b * S.T + t) * (size_t)S.N;
+    const float* x1 = x0 + S.N;
+    float* f = S.f + (size_t)g * S.N;
+    double s2 = 0.0, s1 = 0.0;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < S.N;
+         k += (long long)S.bpp * blockDim.x) {
+        const float v = x1[k] - x0[k];                    // f = x_{t+1} - x_t (L1)
+        f[k] = v;
+        s2 += (double)v * v;
+        s1 += fabs((double)v);
+    }
+    s2 = block_sum(s2, sh);
+    s1 = block_sum(s1, sh);
+    if (threadIdx.x == 0) {
+        double* P = S.partials + ((size_t)g * S.bpp + blockIdx.x) * kRec;
+        P[0] = s2; P[1] = s1;
+        for (int q = 2; q < kRec; ++q) P[q] = 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_objective(const ObjArgs O) {
+    __shared__ double sh[32];
+    const int g = blockIdx.y;
+    const int b = g / O.P, t = g % O.P;
+    const int nx = O.nx, ny = O.ny;
+    const size_t po = (size_t)g * O.N;
+    const float* x0 = O.x + ((size_t)b * O.T + t) * (size_t)O.N;
+    const float* x1 = x0 + O.N;
+    const float* mx = O.mx + po;
+    const float* my = O.my + po;
+    const float* r = O.r + po;
+    const float* a = O.a + po;
+    double tr = 0, gr = 0, ub = 0, af = 0, mg = 0, ma = 0, px = 0;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < O.N;
+         k += (long long)O.bpp * blockDim.x) {
+        const int i = (int)(k % nx), j = (int)(k / nx);
+        const double mxk = (i < nx - 1) ? mx[k] : 0.0;
+        const double myk = (j < ny - 1) ? my[k] : 0.0;
+        const double mxl = (i >= 1) ? mx[k - 1] : 0.0;          // i-1 < nx-1 always
+        const double myu = (j >= 1) ? my[k - nx] : 0.0;
+        const double dv = (mxk - mxl) + (myk - myu);             // div M
+        const double f = (double)(x1[k] - x0[k]);
+        tr += sqrt(mxk * mxk + myk * myk);
+        gr += fabs((double)r[k]);
+        ub += fabs(dv - f);
+        af += (double)a[k] * f;
+        const double gx = (i < nx - 1) ? (double)a[k] - (double)a[k + 1] : 0.0;   // div^* a (L4)
+        const double gy = (j < ny - 1) ? (double)a[k] - (double)a[k + nx] : 0.0;
+        mg = fmax(mg, sqrt(gx * gx + gy * gy));
+        ma = fmax(ma, fabs((double)a[k]));
+        if (O.p != nullptr) {
+            const int s_hi = (t == O.P - 1) ? t + 1 : t;         // frames attributed to pair t
+            for (int s = t; s <= s_hi; ++s) {
+                const size_t fo = ((size_t)b * O.T + s) * (size_t)O.N + k;
+                const double d = (double)O.x[fo] - (double)O.p[fo];
+                px += d * d;
+            }
+        }
+    }
+    tr = block_sum(tr, sh); gr = block_sum(gr, sh); ub = block_sum(ub, sh); af = block_sum(af, sh);
+    mg = block_max(mg, sh); ma = block_max(ma, sh); px = block_sum(px, sh);
+    if (threadIdx.x == 0) {
+        double* P = O.partials + ((size_t)g * O.bpp + blockIdx.x) * kRec;
+        P[0] = tr; P[1] = gr; P[2] = ub; P[3] = af; P[4] = mg; P[5] = ma; P[6] = px; P[7] = 0.0;
+    }
+}
+
+// glob slots
+enum {
+    GL_TR = 0, GL_GR = 1, GL_K2 = 2, GL_DZ = 3, GL_UB = 4, GL_PX = 5,
+    GL_FSQ = 8, GL_FL1 = 9, GL_CONV = 10, GL_NONF = 11, GL_LASTRED = 12,
+    GL_N = 32
+};
+
+__global__ void __launch_bounds__(256) k_pair_reduce(const ReduceArgs R) {
+    __shared__ double sh[32];
+    __shared__ int am_last;
+    if (R.is_iteration && R.stop != nullptr && *reinterpret_cast<const volatile int*>(R.stop)) return;
+    const int g = blockIdx.x;
+    const double* base = R.partials + (size_t)g * R.recs_per_pair * kRec;
+    double out[kRec];
+#pragma unroll
+    for (int q = 0; q < kRec; ++q) {
+        const bool mx = (R.max_mask >> q) & 1u;
+        double v = 0.0;
+        for (int k = threadIdx.x; k < R.recs_per_pair; k += blockDim.x) {
+            const double e = base[(size_t)k * kRec + q];
+            v = mx ? fmax(v, e) : v + e;
+        }
+        out[q] = mx ? block_max(v, sh) : block_sum(v, sh);
+    }
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < kRec; ++q) R.pair_out[(size_t)g * kRec + q] = out[q];
+        __threadfence();
+        am_last = (atomicAdd(R.counter, 1) == R.G - 1);
+    }
+    __syncthreads();
+    if (!am_last || threadIdx.x != 0) return;
+    __threadfence();
+    // last block: pairs in fixed order
+    const volatile double* po = R.pair_out;
+    *R.counter = 0;
+    if (R.is_setup) {
+        double s2 = 0, s1 = 0;
+        for (int q = 0; q < R.G; ++q) { s2 += po[(size_t)q * kRec + 0]; s1 += po[(size_t)q * kRec + 1]; }
+        R.glob[GL_FSQ] = s2;
+        R.glob[GL_FL1] = s1;
+        return;
+    }
+    if (!R.is_iteration) return;
+    double tot[6] = {0, 0, 0, 0, 0, 0};
+    for (int q = 0; q < R.G; ++q)
+        for (int c = 0; c < 6; ++c) tot[c] += po[(size_t)q * kRec + c];
+    bool nonfinite = false;
+    for (int c = 0; c < 6; ++c) { R.glob[c] = tot[c]; nonfinite |= !isfinite(tot[c]); }
+    R.glob[GL_LASTRED] = (double)R.iteration;
+    if (nonfinite) {
+        R.glob[GL_NONF] = 1.0;
+        if (R.stop) *R.stop = 1;
+        return;
+    }
+    if (R.tol > 0.0 && R.stop != nullptr) {
+        // L13: primal ||K|| and dual ||dz||/tau1 relative to ||f||
+        const double scale = R.tol * fmax(sqrt(R.glob[GL_FSQ]), 1e-30);
+        const double primal = sqrt(tot[2]);
+        const double dual = sqrt(tot[3]) / R.tau1;
+        if (primal <= scale && dual <= scale) {
+            R.glob[GL_CONV] = (double)R.iteration;
+            __threadfence();
+            *R.stop = 1;
+        }
+    }
+}
+
+__global__ void k_init_glob(double* glob, int* stop, int* counter, int reset_all) {
+    if (threadIdx.x == 0) {
+        if (reset_all) {
+            for (int q = 0; q < GL_N; ++q) glob[q] = 0.0;
+        }
+        glob[GL_CONV] = -1.0;
+        glob[GL_NONF] = 0.0;
+        *stop = 0;
+        *counter = 0;
+    }
+}
+
+}  // namespace uotk
+
+// ============================================================================ host side
+struct Geometry {
+    int vec, strips, segs, H, items;
+};
+
+struct uot_ctx {
+    uot_params p;
+    uot_buffers b;
+    cudaStream_t s;
+    int B, T, P, G, nx, ny;
+    long long N;
+    bool prox;
+    Geometry geo;
+    int bpp;
+    float tau1f, tau2f;
+    double tau1, tau2;
+    int64_t iter;
+    int64_t launches;
+    double* part;
+    double* pair_it;
+    double* pair_obj;
+    double* glob;
+    int* stop;
+    int* counter;
+    bool timing;
+    std::vector<cudaEvent_t> ev;     // event pool, pairs (start, stop)
+    size_t ev_used;
+    char err[512];
+};
+
+static char g_err[512] = "";
+
+static int fail(uot_ctx* c, int code, const char* fmt, ...) {
+    char* dst = c ? c->err : g_err;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(dst, 512, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+static const int kSMs = 148;
+
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+// Work decomposition of k_iter: strips of
+// 32*vec pixels; segment height H chosen so that the warp count fills the
+// 148 SMs several times, H in [4, 64].
+static Geometry choose_geometry(int nx, int ny, int G, bool vec4_ok) {
+    const long long target = (long long)kSMs * 48;   // warps: ~3 waves at 16 resident warps/SM
+    Geometry g{};
+    g.vec = vec4_ok ? 4 : 1;
+    if (vec4_ok) {
+        const int strips4 = (nx + 127) / 128;
+        const long long max_w = (long long)G * strips4 * ((ny + 3) / 4);
+        if (max_w < target && (nx % 4 == 0)) {
+            // small grid: narrower strips give more warps
+            g.vec = 1;
+        }
+    }
+    const int forced_vec = env_int("UOT_VEC", 0);
+    if (forced_vec == 1 || (forced_vec == 4 && vec4_ok)) g.vec = forced_vec;
+    g.strips = (nx + 32 * g.vec - 1) / (32 * g.vec);
+    const long long cols = (long long)G * g.strips;
+    long long segs_needed = (target + cols - 1) / cols;
+    int H = (int)((ny + segs_needed - 1) / segs_needed);
+    if (H > 64) H = 64;
+    if (H < 4) H = 4;
+    const int forced_h = env_int("UOT_SEG_H", 0);
+    if (forced_h > 0) H = forced_h < 4 ? 4 : forced_h;
+    if (H > ny) H = ny;
+    g.H = H;
+    g.segs = (ny + H - 1) / H;
+    g.items = G * g.strips * g.segs;
+    return g;
+}
+
+static int blocks_per_pair(long long N) {
+    long long b = (N + 4095) / 4096;
+    if (b < 1) b = 1;
+    if (b > 256) b = 256;
+    return (int)b;
+}
+
+static size_t part_records(const Geometry& g, int G, int bpp) {
+    size_t a = (size_t)g.items, b = (size_t)G * bpp;
+    return a > b ? a : b;
+}
+
+static double chain_norm2(int nx, int ny, int T, bool prox) {
+    const double pi = 3.14159265358979323846;
+    const double lam = (nx >= 2 ? 2.0 + 2.0 * cos(pi / nx) : 0.0) + (ny >= 2 ? 2.0 + 2.0 * cos(pi / ny) : 0.0);
+    if (!prox) return lam + 1.0;                        // K = [D, -I]
+    return lam + 1.0 + 2.0 + 2.0 * cos(pi / T);         // K = [D, -I, A], A path incidence (L12)
+}
+
+extern "C" {
+
+size_t uot_scratch_doubles(const uot_params* p) {
+    if (!p || p->nx < 1 || p->ny < 1 || p->n_chains < 1 || p->n_frames < 2) return 0;
+    const int G = p->n_chains * (p->n_frames - 1);
+    const long long N = (long long)p->nx * p->ny;
+    const int bpp = blocks_per_pair(N);
+    size_t recs = 0;
+    for (int v4 = 0; v4 < 2; ++v4) {
+        Geometry g = choose_geometry(p->nx, p->ny, G, v4 && (p->nx % 4 == 0));
+        size_t r = part_records(g, G, bpp);
+        if (r > recs) recs = r;
+    }
+    // also cover the vec-1 geometry with H = 4 (env overrides)
+    Geometry g1{1, (p->nx + 31) / 32, (p->ny + 3) / 4, 4, 0};
+    size_t r1 = (size_t)G * g1.strips * g1.segs;
+    if (r1 > recs) recs = r1;
+    return recs * kRec + 2 * (size_t)G * kRec + GL_N + 4;
+}
+
+int uot_default_steps(const uot_params* p, double safety, double* tau1, double* tau2) {
+    if (!p || !tau1 || !tau2) return fail(nullptr, UOT_E_INVALID, "null argument");
+    if (!(safety > 0.0 && safety < 1.0)) return fail(nullptr, UOT_E_INVALID, "safety must be in (0,1)");
+    if (p->nx < 1 || p->ny < 1 || p->n_frames < 2) return fail(nullptr, UOT_E_INVALID, "bad grid");
+    const bool prox = isfinite(p->rho);
+    const double t = sqrt(safety / chain_norm2(p->nx, p->ny, p->n_frames, prox));
+    *tau1 = t;
+    *tau2 = t;
+    return UOT_OK;
+}
+
+static bool al16(const void* q) { return ((uintptr_t)q & 15u) == 0; }
+
+int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_ctx** out) {
+    if (!out) return fail(nullptr, UOT_E_INVALID, "out is NULL");
+    *out = nullptr;
+    if (!prm || !buf) return fail(nullptr, UOT_E_INVALID, "params/buffers NULL");
+    uot_params p = *prm;
+    if (p.nx < 1 || p.ny < 1) return fail(nullptr, UOT_E_INVALID, "nx, ny must be >= 1");
+    if (p.n_chains < 1 || p.n_frames < 2) return fail(nullptr, UOT_E_INVALID, "need n_chains >= 1, n_frames >= 2");
+    if (!(p.alpha > 0.0) || !isfinite(p.alpha)) return fail(nullptr, UOT_E_INVALID, "alpha must be finite and > 0");
+    if (!(p.rho > 0.0)) return fail(nullptr, UOT_E_INVALID, "rho must be > 0 (+inf = fixed marginals)");
+    if (!(p.tau1 >= 0.0) || !(p.tau2 >= 0.0) || !isfinite(p.tau1) || !isfinite(p.tau2))
+        return fail(nullptr, UOT_E_INVALID, "tau1, tau2 must be finite and >= 0");
+    const bool prox = isfinite(p.rho);
+    if (prox) return fail(nullptr, UOT_E_INVALID, "prox mode (finite rho) is not available in this build");
+    if (p.tau1 == 0.0 || p.tau2 == 0.0) {
+        double t1, t2;
+        uot_default_steps(&p, 0.99, &t1, &t2);
+        if (p.tau1 == 0.0) p.tau1 = t1;
+        if (p.tau2 == 0.0) p.tau2 = t2;
+    }
+    const double bound = 1.0 / chain_norm2(p.nx, p.ny, p.n_frames, prox);
+    if (!(p.flags & UOT_FORCE_STEPS) && !(p.tau1 * p.tau2 < bound))
+        return fail(nullptr, UOT_E_INVALID, "tau1*tau2 = %g violates Theorem 1 bound %g (set UOT_FORCE_STEPS)",
+                    p.tau1 * p.tau2, bound);
+    const uot_buffers& b = *buf;
+    if (!b.frames || !b.mx[0] || !b.mx[1] || !b.my[0] || !b.my[1] || !b.r || !b.a[0] || !b.a[1] || !b.scratch)
+        return fail(nullptr, UOT_E_INVALID, "a required buffer pointer is NULL");
+    if (!prox && !b.f) return fail(nullptr, UOT_E_INVALID, "fixed mode needs buffers.f");
+    if (((uintptr_t)b.scratch & 7u) != 0) return fail(nullptr, UOT_E_INVALID, "scratch must be 8-byte aligned");
+
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, UOT_E_CUDA, "no CUDA device (%s)", cudaGetErrorString(e));
+    }
+
+    uot_ctx* c = new (std::nothrow) uot_ctx();
+    if (!c) return fail(nullptr, UOT_E_CUDA, "host allocation failed");
+    c->p = p;
+    c->b = b;
+    c->s = reinterpret_cast<cudaStream_t>(stream);
+    c->B = p.n_chains; c->T = p.n_frames; c->P = p.n_frames - 1; c->G = c->B * c->P;
+    c->nx = p.nx; c->ny = p.ny; c->N = (long long)p.nx * p.ny;
+    c->prox = prox;
+    const bool vec4_ok = (p.nx % 4 == 0) && al16(b.frames) && al16(b.f) && al16(b.mx[0]) && al16(b.mx[1]) &&
+                         al16(b.my[0]) && al16(b.my[1]) && al16(b.r) && al16(b.a[0]) && al16(b.a[1]);
+    c->geo = choose_geometry(p.nx, p.ny, c->G, vec4_ok);
+    c->bpp = blocks_per_pair(c->N);
+    c->tau1 = p.tau1; c->tau2 = p.tau2;
+    c->tau1f = (float)p.tau1; c->tau2f = (float)p.tau2;
+    c->iter = 0;
+    c->launches = 0;
+    const size_t recs = part_records(c->geo, c->G, c->bpp);
+    c->part = b.scratch;
+    c->pair_it = c->part + recs * kRec;
+    c->pair_obj = c->pair_it + (size_t)c->G * kRec;
+    c->glob = c->pair_obj + (size_t)c->G * kRec;
+    int* ints = reinterpret_cast<int*>(c->glob + GL_N);
+    c->stop = ints;
+    c->counter = ints + 1;
+    c->err[0] = 0;
+    c->timing = false;
+    c->ev_used = 0;
+    *out = c;
+    return UOT_OK;
+}
+
+static int check_launch(uot_ctx* c, const char* what, bool kernel = true) {
+    if (kernel) c->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return UOT_OK;
+}
+
+static int launch_setup(uot_ctx* c) {
+    SetupArgs S{c->T, c->P, c->N, c->bpp, c->b.frames, c->b.f, c->part};
+    k_setup_f<<<dim3(c->bpp, c->G), 256, 0, c->s>>>(S);
+    int rc = check_launch(c, "k_setup_f");
+    if (rc) return rc;
+    ReduceArgs R{};
+    R.partials = c->part; R.recs_per_pair = c->bpp; R.G = c->G; R.pair_out = c->pair_obj;
+    R.glob = c->glob; R.counter = c->counter; R.stop = nullptr; R.max_mask = 0u;
+    R.is_iteration = 0; R.is_setup = 1; R.iteration = 0; R.tol = 0; R.tau1 = c->tau1;
+    k_pair_reduce<<<c->G, 256, 0, c->s>>>(R);
+    return check_launch(c, "k_pair_reduce(setup)");
+}
+
+int uot_reset(uot_ctx* c, uint32_t flags) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    (void)flags;
+    const size_t bytes = (size_t)c->G * c->N * sizeof(float);
+    cudaMemsetAsync(c->b.mx[0], 0, bytes, c->s);
+    cudaMemsetAsync(c->b.my[0], 0, bytes, c->s);
+    cudaMemsetAsync(c->b.r, 0, bytes, c->s);
+    cudaMemsetAsync(c->b.a[0], 0, bytes, c->s);
+    int rc = check_launch(c, "memset", false);
+    if (rc) return rc;
+    k_init_glob<<<1, 32, 0, c->s>>>(c->glob, c->stop, c->counter, 1);
+    rc = check_launch(c, "k_init_glob");
+    if (rc) return rc;
+    c->iter = 0;
+    return launch_setup(c);
+}
+
+int uot_load_frames(uot_ctx* c, const float* host_frames) {
+    if (!c || !host_frames) return fail(c, UOT_E_INVALID, "null argument");
+    const size_t bytes = (size_t)c->B * c->T * c->N * sizeof(float);
+    cudaError_t e = cudaMemcpyAsync(const_cast<float*>(c->b.frames), host_frames, bytes, cudaMemcpyHostToDevice, c->s);
+    if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "cudaMemcpyAsync: %s", cudaGetErrorString(e));
+    return launch_setup(c);
+}
+
+extern "C++" {
+template <int V, bool RED>
+static void launch_iter_t(uot_ctx* c, const IterArgs& A) {
+    const int blocks = (A.items + kWarps - 1) / kWarps;
+    k_iter_fixed<V, RED><<<blocks, kWarps * 32, 0, c->s>>>(A);
+}
+}
+
+static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
+    for (int k = 0; k < n; ++k) {
+        const int in = (int)(c->iter & 1), o = in ^ 1;
+        const bool red = (reduce_last && k == n - 1) || (reduce_every > 0 && ((k + 1) % reduce_every == 0));
+        IterArgs A{};
+        A.nx = c->nx; A.ny = c->ny;
+        A.strips = c->geo.strips; A.segs = c->geo.segs; A.H = c->geo.H; A.items = c->geo.items;
+        A.N = c->N;
+        A.f = c->b.f;
+        A.mx_in = c->b.mx[in]; A.my_in = c->b.my[in]; A.a_in = c->b.a[in];
+        A.mx_out = c->b.mx[o]; A.my_out = c->b.my[o]; A.a_out = c->b.a[o];
+        A.r = c->b.r;
+        A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
+        A.partials = c->part;
+        A.stop = stop;
+        cudaEvent_t e1 = nullptr;
+        if (c->timing) {
+            if (c->ev_used + 2 > c->ev.size()) {
+                for (int q = 0; q < 2; ++q) {
+                    cudaEvent_t e;
+                    if (cudaEventCreate(&e) != cudaSuccess) return fail(c, UOT_E_CUDA, "cudaEventCreate");
+                    c->ev.push_back(e);
+                }
+            }
+            cudaEventRecord(c->ev[c->ev_used], c->s);
+            e1 = c->ev[c->ev_used + 1];
+            c->ev_used += 2;
+        }
+        if (c->geo.vec == 4) {
+            if (red) launch_iter_t<4, true>(c, A); else launch_iter_t<4, false>(c, A);
+        } else {
+            if (red) launch_iter_t<1, true>(c, A); else launch_iter_t<1, false>(c, A);
+        }
+        if (e1) cudaEventRecord(e1, c->s);
+        int rc = check_launch(c, "k_iter_fixed");
+        if (rc) return rc;
+        c->iter++;
+        if (red) {
+            ReduceArgs R{};
+            R.partials = c->part; R.recs_per_pair = c->geo.strips * c->geo.segs; R.G = c->G;
+            R.pair_out = c->pair_it; R.glob = c->glob; R.counter = c->counter;
+            R.stop = const_cast<int*>(stop); R.max_mask = 0u; R.is_iteration = 1; R.is_setup = 0;
+            R.iteration = c->iter; R.tol = tol; R.tau1 = c->tau1;
+            k_pair_reduce<<<c->G, 256, 0, c->s>>>(R);
+            rc = check_launch(c, "k_pair_reduce(iter)");
+            if (rc) return rc;
+        }
+    }
+    return UOT_OK;
+}
+
+static int read_glob(uot_ctx* c, double* h) {
+    cudaError_t e = cudaMemcpyAsync(h, c->glob, GL_N * sizeof(double), cudaMemcpyDeviceToHost, c->s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->s);
+    if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "reading reductions: %s", cudaGetErrorString(e));
+    return UOT_OK;
+}
+
+static void fill_report(const uot_ctx* c, const double* h, uot_report* out) {
+    memset(out, 0, sizeof(*out));
+    const double a = c->p.alpha;
+    out->transport = h[GL_TR];
+    out->growth = a * h[GL_GR];
+    out->prox_term = c->prox ? 0.5 * c->p.rho * h[GL_PX] : 0.0;
+    out->objective = out->transport + out->growth + out->prox_term;
+    out->primal_res = sqrt(h[GL_K2]);
+    out->dual_res = sqrt(h[GL_DZ]) / c->tau1;
+    out->upper_bound = out->transport + a * h[GL_UB];
+    out->lower_bound = NAN;
+    out->f_norm = sqrt(h[GL_FSQ]);
+    out->iterations = c->iter;
+    out->converged = h[GL_CONV] >= 0.0;
+    out->nonfinite = h[GL_NONF] != 0.0;
+}
+
+int uot_prox_step(uot_ctx* c, int32_t n, uot_report* out) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    if (n < 0) return fail(c, UOT_E_INVALID, "n_iters < 0");
+    int rc = launch_iters(c, n, 0, out != nullptr && n > 0, nullptr, 0.0);
+    if (rc) return rc;
+    if (out) {
+        double h[GL_N];
+        rc = read_glob(c, h);
+        if (rc) return rc;
+        fill_report(c, h, out);
+        if (out->nonfinite) return fail(c, UOT_E_NONFINITE, "non-finite value in the reductions");
+    }
+    return UOT_OK;
+}
+
+int uot_solve(uot_ctx* c, int32_t max_iters, double tol, int32_t check_every, uot_report* out) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    if (max_iters < 0 || check_every < 1) return fail(c, UOT_E_INVALID, "max_iters >= 0 and check_every >= 1 required");
+    k_init_glob<<<1, 32, 0, c->s>>>(c->glob, c->stop, c->counter, 0);
+    int rc = check_launch(c, "k_init_glob");
+    if (rc) return rc;
+    const int64_t start = c->iter;
+    rc = launch_iters(c, max_iters, check_every, max_iters > 0, c->stop, tol);
+    if (rc) return rc;
+    double h[GL_N];
+    rc = read_glob(c, h);
+    if (rc) return rc;
+    if (h[GL_CONV] >= 0.0) c->iter = (int64_t)h[GL_CONV];    // later launches exited early
+    else if (h[GL_NONF] != 0.0 && h[GL_LASTRED] > 0) c->iter = (int64_t)h[GL_LASTRED];
+    (void)start;
+    uot_report rep;
+    fill_report(c, h, &rep);
+    if (out) *out = rep;
+    if (rep.nonfinite) return fail(c, UOT_E_NONFINITE, "non-finite value in the reductions");
+    if (tol > 0.0 && !rep.converged) return fail(c, UOT_E_NOT_CONVERGED, "not converged after %d iterations", max_iters);
+    return UOT_OK;
+}
+
+int uot_objective(uot_ctx* c, double* per_pair, uot_report* out) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    const int slot = (int)(c->iter & 1);
+    ObjArgs O{};
+    O.nx = c->nx; O.ny = c->ny; O.T = c->T; O.P = c->P; O.N = c->N; O.bpp = c->bpp;
+    O.x = c->prox ? c->b.x[slot] : c->b.frames;
+    O.p = c->prox ? c->b.frames : nullptr;
+    O.mx = c->b.mx[slot]; O.my = c->b.my[slot]; O.r = c->b.r; O.a = c->b.a[slot];
+    O.partials = c->part;
+    k_objective<<<dim3(c->bpp, c->G), 256, 0, c->s>>>(O);
+    int rc = check_launch(c, "k_objective");
+    if (rc) return rc;
+    ReduceArgs R{};
+    R.partials = c->part; R.recs_per_pair = c->bpp; R.G = c->G; R.pair_out = c->pair_obj;
+    R.glob = c->glob; R.counter = c->counter; R.stop = nullptr; R.max_mask = (1u << 4) | (1u << 5);
+    R.is_iteration = 0; R.is_setup = 0; R.tau1 = c->tau1;
+    k_pair_reduce<<<c->G, 256, 0, c->s>>>(R);
+    rc = check_launch(c, "k_pair_reduce(objective)");
+    if (rc) return rc;
+    double* rows = (double*)malloc(sizeof(double) * c->G * kRec);
+    double h[GL_N];
+    cudaError_t e = cudaMemcpyAsync(rows, c->pair_obj, sizeof(double) * c->G * kRec, cudaMemcpyDeviceToHost, c->s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, c->glob, GL_N * sizeof(double), cudaMemcpyDeviceToHost, c->s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->s);
+    if (e != cudaSuccess) { free(rows); return fail(c, UOT_E_CUDA, "objective readback: %s", cudaGetErrorString(e)); }
+    const double a = c->p.alpha;
+    double tr = 0, gr = 0, ub = 0, lb = 0, px = 0;
+    bool nonfinite = false;
+    for (int g = 0; g < c->G; ++g) {
+        const double* q = rows + (size_t)g * kRec;
+        double cc = 1.0;
+        if (q[4] > cc) cc = q[4];
+        if (q[5] / a > cc) cc = q[5] / a;
+        const double U = q[0] + a * q[2];
+        const double L = -q[3] / cc;                  // weak duality
+        if (per_pair) {
+            double* P = per_pair + (size_t)g * 8;
+            P[0] = q[0]; P[1] = q[1]; P[2] = U; P[3] = q[3]; P[4] = q[4]; P[5] = q[5]; P[6] = L;
+            P[7] = q[0] + a * q[1];
+        }
+        tr += q[0]; gr += q[1]; ub += U; lb += L; px += q[6];
+        for (int k = 0; k < 7; ++k) nonfinite |= !isfinite(q[k]);
+    }
+    free(rows);
+    if (out) {
+        memset(out, 0, sizeof(*out));
+        out->transport = tr;
+        out->growth = a * gr;
+        out->prox_term = c->prox ? 0.5 * c->p.rho * px : 0.0;
+        out->objective = tr + a * gr + out->prox_term;
+        out->primal_res = NAN;
+        out->dual_res = NAN;
+        out->upper_bound = ub;
+        out->lower_bound = lb;
+        out->f_norm = sqrt(h[GL_FSQ]);
+        out->iterations = c->iter;
+        out->nonfinite = nonfinite;
+    }
+    if (nonfinite) return fail(c, UOT_E_NONFINITE, "non-finite state");
+    return UOT_OK;
+}
+
+int uot_set_timing(uot_ctx* c, int enable) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    c->timing = enable != 0;
+    return UOT_OK;
+}
+
+int uot_get_timing(uot_ctx* c, double* ms_total, int64_t* n) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    cudaError_t e = cudaStreamSynchronize(c->s);
+    if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "sync: %s", cudaGetErrorString(e));
+    double tot = 0.0;
+    for (size_t q = 0; q + 1 < c->ev_used; q += 2) {
+        float ms = 0.f;
+        e = cudaEventElapsedTime(&ms, c->ev[q], c->ev[q + 1]);
+        if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "cudaEventElapsedTime: %s", cudaGetErrorString(e));
+        tot += ms;
+    }
+    if (ms_total) *ms_total = tot;
+    if (n) *n = (int64_t)(c->ev_used / 2);
+    c->ev_used = 0;
+    return UOT_OK;
+}
+
+int uot_state_slot(const uot_ctx* c) { return c ? (int)(c->iter & 1) : -1; }
+
+int64_t uot_launch_count(const uot_ctx* c) { return c ? c->launches : -1; }
+
+void uot_destroy(uot_ctx* c) {
+    if (!c) return;
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    delete c;
+}
+
+const char* uot_last_error(const uot_ctx* c) { return c ? c->err : g_err; }
+
+}  // extern "C"

@@ -1,0 +1,335 @@
+// uot_kernels.cuh -- sm_100a kernels of the fused Algorithm-1 iteration
+// (arXiv 1909.00149).  Readings "Lnn" are DESIGN.md's.
+//
+// Design:
+//  * One WARP marches down a vertical strip of 32*V pixels (V = 4: one float4
+//    per lane) over a segment of H rows of one pair.  Per row it streams the
+//    row's Mx, My, r, f and the NEXT row of a (a of the current row is kept
+//    from the previous step), so every plane is read once from HBM:
+//    20 B read + 16 B written per pixel-iteration (fixed marginals).
+//  * div^*(a) (sync point #1 of P:326) needs a at (j, i+1) and (j+1, i):
+//    the +i neighbour comes from the next lane by shuffle (lane 31: one halo
+//    load), the +j neighbour is the prefetched next row.
+//  * div(M^{k+1}) (sync point #2) needs M'x at (j, i-1) and M'y at (j-1, i):
+//    M'x(j, i-1) comes from the previous lane by shuffle (lane 0 RECOMPUTES
+//    the shrink of its left halo pixel), M'y(j-1, i) is carried from the
+//    previous row (the segment's first row recomputes row j0-1: prologue).
+//    Halo recomputation replaces both grid-wide synchronisations; a, M are
+//    ping-ponged so the halo reads see iteration-k values.
+//  * K^k = div(M^k) - r^k - f is recomputed from the incoming state, never
+//    stored (L8).  r is updated in place (its update is pointwise).
+//  * Optional fused reductions (transport, growth, ||K||^2, ||dz||^2,
+//    ||div M - f||_1) -> fp32 per lane, fp64 warp butterfly -> one record per
+//    warp; k_pair_reduce sums records in fixed order (deterministic).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace uotk {
+
+constexpr int kWarps = 4;          // warps (work items) per CTA in k_iter
+constexpr int kRec = 8;            // doubles per partial record
+constexpr unsigned kFull = 0xffffffffu;
+
+struct IterArgs {
+    int nx, ny;
+    int strips, segs, H, items;
+    long long N;                      // nx*ny
+    const float* f;                   // [G][N]            (fixed mode)
+    const float* mx_in;               // [G][N] iteration k
+    const float* my_in;
+    const float* a_in;
+    float* mx_out;                    // [G][N] iteration k+1
+    float* my_out;
+    float* a_out;
+    float* r;                         // [G][N] in place
+    float tau1, tau2, atau1;          // atau1 = alpha * tau1
+    double* partials;                 // [items][kRec] when reducing
+    const int* stop;                  // device stop flag or nullptr
+};
+
+template <int V>
+__device__ __forceinline__ void ld_ro(float (&d)[V], const float* p) {
+    if constexpr (V == 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        d[0] = t.x; d[1] = t.y; d[2] = t.z; d[3] = t.w;
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) d[v] = __ldg(p + v);
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void ld_rw(float (&d)[V], const float* p) {
+    if constexpr (V == 4) {
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        d[0] = t.x; d[1] = t.y; d[2] = t.z; d[3] = t.w;
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) d[v] = p[v];
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void st(float* p, const float (&d)[V]) {
+    if constexpr (V == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(d[0], d[1], d[2], d[3]);
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) p[v] = d[v];
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void zero(float (&d)[V]) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) d[v] = 0.f;
+}
+
+// shrink^{l2}_{tau1} factor: max(||q|| - tau1, 0)/||q||, 0 at q = 0 (L7).
+// rsqrt(0) = +inf -> 1 - tau1*inf = -inf -> 0.
+__device__ __forceinline__ float shrink_factor(float n2, float inv, float t1) {
+    return fmaxf(fmaf(-t1, inv, 1.f), 0.f);
+}
+
+// shrink^{l1}_{s}(q) = sign(q) max(|q| - s, 0)
+__device__ __forceinline__ float soft(float q, float s) {
+    return copysignf(fmaxf(fabsf(q) - s, 0.f), q);
+}
+
+template <int V, bool RED>
+__global__ void __launch_bounds__(kWarps * 32)
+k_iter_fixed(const IterArgs A) {
+    if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
+    const int lane = threadIdx.x & 31;
+    const int item = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (item >= A.items) return;                        // warp-uniform
+    const int strip = item % A.strips;
+    const int rest = item / A.strips;
+    const int seg = rest % A.segs;
+    const int pair = rest / A.segs;
+
+    const int nx = A.nx, ny = A.ny;
+    const int i0 = strip * 32 * V;
+    const int ib = i0 + lane * V;
+    const bool act = ib < nx;                           // whole vector inside (nx % V == 0)
+    const int iL = i0 - 1, iR = i0 + 32 * V;
+    const bool hasL = iL >= 0, hasR = iR < nx;
+    const int j0 = seg * A.H;
+    const int j1 = min(j0 + A.H, ny);
+    const size_t po = (size_t)pair * (size_t)A.N;
+
+    const float* __restrict__ fp = A.f + po;
+    const float* __restrict__ mxi = A.mx_in + po;
+    const float* __restrict__ myi = A.my_in + po;
+    const float* __restrict__ ai = A.a_in + po;
+    float* __restrict__ mxo = A.mx_out + po;
+    float* __restrict__ myo = A.my_out + po;
+    float* __restrict__ ao = A.a_out + po;
+    float* __restrict__ rp = A.r + po;
+    const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1;
+
+    bool colx[V];                                       // Mx exists / gx != 0: i < nx-1 (L3, L4)
+#pragma unroll
+    for (int v = 0; v < V; ++v) colx[v] = (ib + v) < nx - 1;
+
+    // ---- prologue: a at row j0, and M'y / My at row j0-1 ------------------------------
+    float a_c[V], myp_n[V], myp_o[V];
+    float aL_c = 0.f, aR_c = 0.f;
+    const size_t r0 = (size_t)j0 * nx;
+    if (act) ld_ro<V>(a_c, ai + r0 + ib); else zero<V>(a_c);
+    if (lane == 0 && hasL) aL_c = __ldg(ai + r0 + iL);
+    if (lane == 31 && hasR) aR_c = __ldg(ai + r0 + iR);
+    if (j0 > 0) {
+        const size_t rp0 = (size_t)(j0 - 1) * nx;
+        float a_p[V], mxp[V], myp[V];
+        float aR_p = 0.f;
+        if (act) { ld_ro<V>(a_p, ai + rp0 + ib); ld_ro<V>(mxp, mxi + rp0 + ib); ld_ro<V>(myp, myi + rp0 + ib); }
+        else { zero<V>(a_p); zero<V>(mxp); zero<V>(myp); }
+        if (lane == 31 && hasR) aR_p = __ldg(ai + rp0 + iR);
+        const float nb = __shfl_down_sync(kFull, a_p[0], 1);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const float ar = (v < V - 1) ? a_p[(v + 1) % V] : (lane == 31 ? aR_p : nb);
+            const float gx = colx[v] ? a_p[v] - ar : 0.f;
+            const float gy = a_p[v] - a_c[v];            // row j0-1 < ny-1
+            const float qx = (colx[v] ? mxp[v] : 0.f) - t1 * gx;
+            const float qy = myp[v] - t1 * gy;
+            const float n2 = qx * qx + qy * qy;
+            const float s = shrink_factor(n2, rsqrtf(n2), t1);
+            myp_n[v] = s * qy;
+            myp_o[v] = myp[v];
+        }
+    } else {
+        zero<V>(myp_n); zero<V>(myp_o);
+    }
+
+    // ---- software-pipelined row loop ---------------------------------------------------
+    float n_a[V], n_mx[V], n_my[V], n_r[V], n_f[V];
+    float n_aL = 0.f, n_aR = 0.f, n_mxL = 0.f, n_myL = 0.f;
+    auto fetch = [&](int j) {
+        const size_t rj = (size_t)j * nx;
+        const bool has_next = (j + 1) < ny;
+        if (act) {
+            ld_ro<V>(n_mx, mxi + rj + ib);
+            ld_ro<V>(n_my, myi + rj + ib);
+            ld_rw<V>(n_r, rp + rj + ib);
+            ld_ro<V>(n_f, fp + rj + ib);
+            if (has_next) ld_ro<V>(n_a, ai + rj + nx + ib); else zero<V>(n_a);
+        } else {
+            zero<V>(n_mx); zero<V>(n_my); zero<V>(n_r); zero<V>(n_f); zero<V>(n_a);
+        }
+        if (lane == 0 && hasL) {
+            n_mxL = __ldg(mxi + rj + iL);
+            n_myL = __ldg(myi + rj + iL);
+            n_aL = has_next ? __ldg(ai + rj + nx + iL) : 0.f;
+        }
+        if (lane == 31 && hasR) n_aR = has_next ? __ldg(ai + rj + nx + iR) : 0.f;
+    };
+    fetch(j0);
+
+    float s_tr = 0.f, s_gr = 0.f, s_k2 = 0.f, s_dz = 0.f, s_ub = 0.f;
+
+    for (int j = j0; j < j1; ++j) {
+        float c_a[V], c_mx[V], c_my[V], c_r[V], c_f[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) { c_a[v] = n_a[v]; c_mx[v] = n_mx[v]; c_my[v] = n_my[v]; c_r[v] = n_r[v]; c_f[v] = n_f[v]; }
+        const float c_aL = n_aL, c_aR = n_aR, c_mxL = n_mxL, c_myL = n_myL;
+        if (j + 1 < j1) fetch(j + 1);
+        const bool lastrow = (j == ny - 1);
+
+        // Alg.1 line 3: m <- shrink_{tau1}(m - tau1 div^*(a))
+        const float nb = __shfl_down_sync(kFull, a_c[0], 1);
+        float mxn[V], myn[V], mxk[V], myk[V], rn[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const float ar = (v < V - 1) ? a_c[(v + 1) % V] : (lane == 31 ? aR_c : nb);
+            const float gx = colx[v] ? a_c[v] - ar : 0.f;
+            const float gy = lastrow ? 0.f : a_c[v] - c_a[v];
+            mxk[v] = colx[v] ? c_mx[v] : 0.f;           // pinned components read as 0 (L3)
+            myk[v] = lastrow ? 0.f : c_my[v];
+            const float qx = mxk[v] - t1 * gx;
+            const float qy = myk[v] - t1 * gy;
+            const float n2 = qx * qx + qy * qy;
+            const float inv = rsqrtf(n2);
+            const float s = shrink_factor(n2, inv, t1);
+            mxn[v] = s * qx;
+            myn[v] = s * qy;
+            // Alg.1 line 5: r <- shrink^{l1}_{alpha tau1}(r + tau1 a)
+            rn[v] = soft(fmaf(t1, a_c[v], c_r[v]), at1);
+            if constexpr (RED) s_tr += (n2 > 0.f) ? fmaxf(n2 * inv - t1, 0.f) : 0.f;
+        }
+        // M'x and Mx at (j, i-1): previous lane, or recomputed halo for lane 0
+        const float upn = __shfl_up_sync(kFull, mxn[V - 1], 1);
+        const float upk = __shfl_up_sync(kFull, mxk[V - 1], 1);
+        float lmn0 = upn, lmk0 = upk;
+        if (lane == 0) {
+            if (hasL) {
+                const float gxL = aL_c - a_c[0];
+                const float gyL = lastrow ? 0.f : aL_c - c_aL;
+                const float kyL = lastrow ? 0.f : c_myL;
+                const float qx = c_mxL - t1 * gxL;
+                const float qy = kyL - t1 * gyL;
+                const float n2 = qx * qx + qy * qy;
+                lmn0 = shrink_factor(n2, rsqrtf(n2), t1) * qx;
+                lmk0 = c_mxL;
+            } else {
+                lmn0 = 0.f; lmk0 = 0.f;
+            }
+        }
+        // Alg.1 lines 6-7: b = 2K^{k+1} - K^k, a <- a + tau2 b
+        float an[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const float lmn = v ? mxn[(v + V - 1) % V] : lmn0;
+            const float lmk = v ? mxk[(v + V - 1) % V] : lmk0;
+            const float divn = (mxn[v] - lmn) + (myn[v] - myp_n[v]);
+            const float divk = (mxk[v] - lmk) + (myk[v] - myp_o[v]);
+            const float Kn = divn - rn[v] - c_f[v];
+            const float Kk = divk - c_r[v] - c_f[v];
+            an[v] = fmaf(t2, 2.f * Kn - Kk, a_c[v]);
+            if constexpr (RED) {
+                const float dmx = mxn[v] - mxk[v], dmy = myn[v] - myk[v], dr = rn[v] - c_r[v];
+                s_gr += fabsf(rn[v]);
+                s_k2 += Kn * Kn;
+                s_dz += dmx * dmx + dmy * dmy + dr * dr;
+                s_ub += fabsf(divn - c_f[v]);
+            }
+        }
+        if (act) {
+            const size_t rj = (size_t)j * nx + ib;
+            st<V>(mxo + rj, mxn);
+            st<V>(myo + rj, myn);
+            st<V>(rp + rj, rn);
+            st<V>(ao + rj, an);
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) { myp_n[v] = myn[v]; myp_o[v] = myk[v]; a_c[v] = c_a[v]; }
+        aL_c = c_aL;
+        aR_c = c_aR;
+    }
+
+    if constexpr (RED) {
+        double d0 = s_tr, d1 = s_gr, d2 = s_k2, d3 = s_dz, d4 = s_ub;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            d0 += __shfl_xor_sync(kFull, d0, o);
+            d1 += __shfl_xor_sync(kFull, d1, o);
+            d2 += __shfl_xor_sync(kFull, d2, o);
+            d3 += __shfl_xor_sync(kFull, d3, o);
+            d4 += __shfl_xor_sync(kFull, d4, o);
+        }
+        if (lane == 0) {
+            double* P = A.partials + (size_t)item * kRec;
+            P[0] = d0; P[1] = d1; P[2] = d2; P[3] = d3; P[4] = d4; P[5] = 0.0; P[6] = 0.0; P[7] = 0.0;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Setup (row a0): f = x_{t+1} - x_t per pair, and per-block partial sums of f^2, |f|.
+struct SetupArgs {
+    int T, P;                 // frames / pairs per chain
+    long long N;
+    int bpp;                  // blocks per pair
+    const float* frames;      // [B][T][N]
+    float* f;                 // [G][N]
+    double* partials;         // [G*bpp][kRec]
+};
+
+__global__ void __launch_bounds__(256) k_setup_f(const SetupArgs S);
+
+// Objective / certificate of the current state: per block records
+// {sum||M||, sum|r|, sum|div M - f|, sum a f, max||div^* a||, max|a|, sum (x-p)^2, 0}.
+struct ObjArgs {
+    int nx, ny, T, P;
+    long long N;
+    int bpp;
+    const float* x;           // [B][T][N] frames (fixed) or x (prox)
+    const float* p;           // [B][T][N] prox centres (prox) or nullptr
+    const float* mx; const float* my; const float* r; const float* a;
+    double* partials;
+};
+__global__ void __launch_bounds__(256) k_objective(const ObjArgs O);
+
+// Deterministic per-pair reduction of records (sum; bit k of max_mask -> max),
+// then the last block reduces the pairs in order into glob[0..7] and, for
+// iteration records, evaluates the stopping test (L13).
+struct ReduceArgs {
+    const double* partials;
+    int recs_per_pair;
+    int G;
+    double* pair_out;         // [G][kRec]
+    double* glob;             // global accumulators (see uot_api.cu)
+    int* counter;
+    int* stop;                // nullable
+    unsigned max_mask;
+    int is_iteration;         // 1: glob[0..7] iteration sums + stop test
+    int is_setup;             // 1: write glob f-norm slots
+    long long iteration;      // iteration index just completed
+    double tol;               // <= 0: no stop test
+    double tau1;
+};
+__global__ void __launch_bounds__(256) k_pair_reduce(const ReduceArgs R);
+
+}  // namespace uotk

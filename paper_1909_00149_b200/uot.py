@@ -1,0 +1,200 @@
+"""Python surface of the B200 UOT hot path (thin layer over include/uot.h).
+
+PyTorch is used only for device memory and streams: every buffer the C
+library works on is a torch tensor allocated here and passed by pointer; every
+arithmetic step of Algorithm 1 runs in the library's
+CUDA kernels.  There is no CPU or PyTorch fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import Buffers, Params, Report, check, lib
+
+__all__ = ["Problem", "default_steps", "scratch_doubles", "Report"]
+
+
+def _params(nx, ny, B, T, alpha, rho, tau1, tau2, flags=0) -> Params:
+    return Params(int(nx), int(ny), int(B), int(T), float(alpha), float(rho),
+                  float(tau1 or 0.0), float(tau2 or 0.0), int(flags))
+
+
+def default_steps(nx, ny, n_frames=2, rho=math.inf, safety=0.99):
+    """Theorem-1 steps (L11/L12) from the library."""
+    t1, t2 = ctypes.c_double(), ctypes.c_double()
+    p = _params(nx, ny, 1, n_frames, 1.0, rho, 0, 0)
+    check(lib().uot_default_steps(ctypes.byref(p), float(safety), ctypes.byref(t1), ctypes.byref(t2)))
+    return t1.value, t2.value
+
+
+def scratch_doubles(nx, ny, B, T, rho=math.inf) -> int:
+    p = _params(nx, ny, B, T, 1.0, rho, 0, 0)
+    return int(lib().uot_scratch_doubles(ctypes.byref(p)))
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+@dataclass
+class PairCert:
+    """uot_objective per-pair rows: see include/uot.h."""
+    rows: "object"   # numpy [G][8]: transport, sum|r|, U, <a,f>, max||div*a||, max|a|, L, objective
+
+
+class Problem:
+    """B chains of T frames [B][T][ny][nx] (fp32, CUDA), one UOT term per adjacent pair.
+
+    rho = inf: fixed marginals (evaluation of eq:Unbal_OT_beckman);
+    finite rho: prox mode (eq:Prox_UOT, L2/L19).
+    """
+
+    def __init__(self, frames: torch.Tensor, alpha: float, rho: float = math.inf,
+                 tau1: float | None = None, tau2: float | None = None, *, stream: torch.cuda.Stream | None = None,
+                 force_steps: bool = False, reset: bool = True):
+        if frames.dim() != 4:
+            raise ValueError("frames must be [B][T][ny][nx]")
+        if not frames.is_cuda or frames.dtype != torch.float32:
+            raise ValueError("frames must be a float32 CUDA tensor")
+        self.frames = frames.contiguous()
+        B, T, ny, nx = self.frames.shape
+        self.B, self.T, self.ny, self.nx = B, T, ny, nx
+        self.P = T - 1
+        self.G = B * self.P
+        self.alpha, self.rho = float(alpha), float(rho)
+        self.prox = math.isfinite(self.rho)
+        dev = self.frames.device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        plane = (B, self.P, ny, nx)
+        e = lambda shape: torch.empty(shape, dtype=torch.float32, device=dev)
+        self.f = e(plane) if not self.prox else None
+        self.mx = [e(plane), e(plane)]
+        self.my = [e(plane), e(plane)]
+        self.r = e(plane)
+        self.a = [e(plane), e(plane)]
+        self.x = [e(self.frames.shape), e(self.frames.shape)] if self.prox else [None, None]
+        self.a_prev_halo = None
+        self.a_next_halo = None
+        self._params = _params(nx, ny, B, T, alpha, rho, tau1, tau2,
+                               _lib.UOT_FORCE_STEPS if force_steps else 0)
+        nsc = int(lib().uot_scratch_doubles(ctypes.byref(self._params)))
+        self.scratch = torch.zeros(nsc, dtype=torch.float64, device=dev)
+        self._bufs = self._make_buffers()
+        ctx = ctypes.c_void_p()
+        check(lib().uot_create(ctypes.byref(self._params), ctypes.byref(self._bufs),
+                               ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx)))
+        self._ctx = ctx
+        if tau1 is None or tau2 is None:
+            d1, d2 = default_steps(nx, ny, T, rho)
+            self.tau1 = float(tau1) if tau1 is not None else d1
+            self.tau2 = float(tau2) if tau2 is not None else d2
+        else:
+            self.tau1, self.tau2 = float(tau1), float(tau2)
+        if reset:
+            self.reset()
+
+    def _make_buffers(self) -> Buffers:
+        b = Buffers()
+        b.frames = self.frames.data_ptr()
+        b.f = self.f.data_ptr() if self.f is not None else None
+        for k in range(2):
+            b.mx[k] = self.mx[k].data_ptr()
+            b.my[k] = self.my[k].data_ptr()
+            b.a[k] = self.a[k].data_ptr()
+            b.x[k] = self.x[k].data_ptr() if self.x[k] is not None else None
+        b.r = self.r.data_ptr()
+        b.a_prev_halo = None
+        b.a_next_halo = None
+        b.scratch = self.scratch.data_ptr()
+        return b
+
+    # ------------------------------------------------------------------ calls
+    def reset(self, x_from_p: bool = False):
+        check(lib().uot_reset(self._ctx, _lib.UOT_RESET_X_FROM_P if x_from_p else 0), self._ctx)
+
+    def load_frames_host(self, host_frames: torch.Tensor):
+        """H2D copy of new frames (pinned host tensor, same shape) + recompute f (warm state kept)."""
+        if host_frames.is_cuda or host_frames.dtype != torch.float32 or host_frames.shape != self.frames.shape:
+            raise ValueError("host_frames must be a CPU float32 tensor of the frames' shape")
+        if not host_frames.is_contiguous():
+            raise ValueError("host_frames must be contiguous")
+        self._host_keepalive = host_frames
+        check(lib().uot_load_frames(self._ctx, ctypes.c_void_p(host_frames.data_ptr())), self._ctx)
+
+    def step(self, n: int = 1, report: bool = False) -> dict | None:
+        """n iterations of Alg.1 lines 3-7; report=True syncs and returns the reductions of the last."""
+        if report:
+            rep = Report()
+            check(lib().uot_prox_step(self._ctx, int(n), ctypes.byref(rep)), self._ctx)
+            return rep.as_dict()
+        check(lib().uot_prox_step(self._ctx, int(n), None), self._ctx)
+        return None
+
+    def solve(self, max_iters: int, tol: float = 0.0, check_every: int = 10, raise_not_converged=False) -> dict:
+        rep = Report()
+        allow = () if raise_not_converged else (_lib.UOT_E_NOT_CONVERGED,)
+        rc = check(lib().uot_solve(self._ctx, int(max_iters), float(tol), int(check_every), ctypes.byref(rep)),
+                   self._ctx, allow=allow)
+        d = rep.as_dict()
+        d["status"] = rc
+        return d
+
+    def objective(self, per_pair: bool = False):
+        """Objective + weak-duality certificate of the current state (see include/uot.h)."""
+        import numpy as np
+        rep = Report()
+        rows = np.zeros((self.G, 8), dtype=np.float64) if per_pair else None
+        ptr = rows.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if per_pair else None
+        check(lib().uot_objective(self._ctx, ptr, ctypes.byref(rep)), self._ctx)
+        return (rep.as_dict(), rows) if per_pair else rep.as_dict()
+
+    def set_timing(self, enable: bool = True):
+        check(lib().uot_set_timing(self._ctx, int(bool(enable))), self._ctx)
+
+    def get_timing(self):
+        """(summed device ms of the timed fused-iteration launches, their count); clears."""
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        check(lib().uot_get_timing(self._ctx, ctypes.byref(ms), ctypes.byref(n)), self._ctx)
+        return ms.value, n.value
+
+    @property
+    def slot(self) -> int:
+        return int(lib().uot_state_slot(self._ctx))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().uot_launch_count(self._ctx))
+
+    def state(self) -> dict:
+        """Current iterate (views of the ping-pong slot)."""
+        s = self.slot
+        d = {"mx": self.mx[s], "my": self.my[s], "r": self.r, "a": self.a[s]}
+        if self.prox:
+            d["x"] = self.x[s]
+        return d
+
+    def state_dict(self) -> dict:
+        """Checkpoint: copies of the current state (+ iteration count)."""
+        d = {k: v.detach().clone() for k, v in self.state().items()}
+        d["iterations"] = self.iterations
+        return d
+
+    @property
+    def iterations(self) -> int:
+        return int(self.step(0, report=True)["iterations"])
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().uot_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

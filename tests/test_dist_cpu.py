@@ -1,0 +1,70 @@
+"""Multi-process (gloo, world_size 2/3, CPU) tests of the frame-range sharding
+host logic used by bench.py and the multi-GPU path."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1909_00149_b200.dist import (all_reduce_report, exchange_boundary_duals,
+                                        exchange_boundary_frame, shard_range)
+
+
+@pytest.mark.parametrize("n,w", [(255, 1), (255, 2), (255, 4), (255, 8), (63, 8), (8, 8), (64, 8)])
+def test_shard_range_partitions(n, w):
+    seen = []
+    sizes = []
+    for r in range(w):
+        p0, p1 = shard_range(n, w, r)
+        seen.extend(range(p0, p1))
+        sizes.append(p1 - p0)
+    assert seen == list(range(n))
+    assert max(sizes) - min(sizes) <= 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, T, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    full = torch.arange(T * 3 * 4, dtype=torch.float32).reshape(1, T, 3, 4)
+    p0, p1 = shard_range(T - 1, world, rank)
+    own_hi = p1 if rank < world - 1 else p1 + 1
+    frames = torch.zeros(1, p1 - p0 + 1, 3, 4)
+    frames[:, : own_hi - p0] = full[:, p0:own_hi]
+    exchange_boundary_frame(frames, rank, world)
+    ok_frames = torch.equal(frames, full[:, p0:p1 + 1])
+    # dual halo exchange: a_first/a_last tagged by rank
+    a_first = torch.full((1, 3, 4), 10.0 * rank + 1)
+    a_last = torch.full((1, 3, 4), 10.0 * rank + 2)
+    prev = torch.zeros(1, 3, 4)
+    nxt = torch.zeros(1, 3, 4)
+    exchange_boundary_duals(a_first, a_last, prev, nxt, rank, world)
+    ok_prev = rank == 0 or bool(torch.all(prev == 10.0 * (rank - 1) + 2))
+    ok_next = rank == world - 1 or bool(torch.all(nxt == 10.0 * (rank + 1) + 1))
+    rep = {"objective": 1.0 + rank, "transport": 1.0, "growth": 0.5, "prox_term": 0.0, "upper_bound": 2.0,
+           "primal_res": 3.0, "dual_res": 4.0, "f_norm": 1.0}
+    tot = all_reduce_report(rep, "cpu")
+    ok_rep = abs(tot["objective"] - sum(1.0 + r for r in range(world))) < 1e-12 and \
+        abs(tot["primal_res"] - 3.0 * world ** 0.5) < 1e-12
+    out[rank] = (ok_frames, ok_prev, ok_next, ok_rep)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,T", [(2, 9), (3, 10)])
+def test_gloo_boundary_exchange(world, T):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), T, out), nprocs=world, join=True)
+    for r in range(world):
+        assert out[r] == (True, True, True, True), (r, out[r])

@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the float64 oracle.
+
+Bar (BASELINE.json north star): after a fixed iteration count the objective
+matches within 1e-4 relative and every iterate plane F in {Mx, My, r, a}
+within 1e-3 max-abs after normalisation (L17):
+    e_F = max|F_gpu - F_ref| / max(max|F_ref|, max|f|).
+Both sides get the same fp32 frames (the oracle reads them as fp64) and the
+same step sizes.  Expected values come only from oracle/.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1909_00149_b200 import inputs
+from paper_1909_00149_b200.uot import Problem
+
+pytestmark = pytest.mark.gpu
+
+OBJ_RTOL = 1e-4
+ITER_TOL = 1e-3
+
+
+def gpu_run(frames_np, alpha, n, tau, env=None, report=True):
+    old = {}
+    for k, v in (env or {}).items():
+        old[k] = os.environ.get(k)
+        os.environ[k] = str(v)
+    try:
+        fr = torch.from_numpy(frames_np).cuda()
+        prob = Problem(fr, alpha, tau1=tau, tau2=tau)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    rep = prob.step(n, report=report)
+    st = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
+    return prob, st, rep
+
+
+def compare(frames_np, st_gpu, st_ref, pairs=None, tol=ITER_TOL):
+    """Normalised max-abs error per plane (L17); pairs = indices into the GPU planes."""
+    B, T, ny, nx = frames_np.shape
+    fr = frames_np.astype(np.float64)
+    f = (fr[:, 1:] - fr[:, :-1]).reshape(-1, ny, nx)
+    errs = {}
+    for name in ("mx", "my", "r", "a"):
+        g = st_gpu[name].reshape(-1, ny, nx)
+        ref = getattr(st_ref, name).reshape(-1, ny, nx)
+        if pairs is not None:
+            g = g[pairs]
+            f_sel = f[pairs]
+        else:
+            f_sel = f
+        scale = max(np.abs(ref).max(), np.abs(f_sel).max())
+        errs[name] = np.abs(g - ref).max() / scale
+    bad = {k: v for k, v in errs.items() if not v <= tol}
+    assert not bad, errs
+    return errs
+
+
+def tau_for(ny, nx):
+    return oracle.default_steps(nx, ny, prox=False, safety=0.99)[0]
+
+
+# ------------------------------------------------------------------------- small / ragged / edge cases
+CASES = [
+    # B, T, ny, nx, alpha, iters, kind
+    (1, 2, 1, 8, 0.7, 40, "uniform"),
+    (1, 2, 8, 1, 0.7, 40, "uniform"),
+    (1, 2, 1, 1, 0.7, 10, "uniform"),
+    (1, 2, 7, 9, 1.3, 60, "sparse"),
+    (2, 3, 37, 130, 2.0, 80, "sparse"),
+    (1, 4, 65, 260, 0.5, 80, "uniform"),
+    (3, 2, 33, 132, 1.0, 50, "signed"),
+    (1, 2, 130, 516, 5.0, 60, "sparse"),
+]
+
+
+@pytest.mark.parametrize("vec", [1, 4])
+@pytest.mark.parametrize("H", [0, 4, 7])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c[:4])) + f"-a{c[4]}")
+def test_parity_small(case, vec, H):
+    B, T, ny, nx, alpha, n, kind = case
+    fr = inputs.gen_random(B, T, ny, nx, seed=100 + ny + nx, kind=kind)
+    tau = tau_for(ny, nx)
+    env = {"UOT_VEC": vec, "UOT_SEG_H": H}
+    prob, st, rep = gpu_run(fr, alpha, n, tau, env)
+    ref, rrep = oracle.iterate(fr, alpha, math.inf, tau, tau, n)
+    compare(fr, st, ref)
+    obj_ref = rrep[:, 0].sum() + alpha * rrep[:, 1].sum()
+    assert rep["objective"] == pytest.approx(obj_ref, rel=OBJ_RTOL, abs=1e-6)
+    assert rep["upper_bound"] == pytest.approx(rrep[:, 0].sum() + alpha * rrep[:, 4].sum(), rel=OBJ_RTOL, abs=1e-6)
+    assert rep["primal_res"] == pytest.approx(math.sqrt(rrep[:, 2].sum()), rel=1e-2, abs=1e-5)
+    # pinned flux components are exactly zero (L3)
+    assert np.all(st["mx"][..., -1] == 0) and np.all(st["my"][..., -1, :] == 0)
+    # per-pair certificate vs the oracle's
+    _, rows = prob.objective(per_pair=True)
+    cert = oracle.certificate(fr, ref, alpha)
+    for col in (0, 2, 7):
+        np.testing.assert_allclose(rows[:, col], cert[:, col], rtol=OBJ_RTOL, atol=1e-6)
+    np.testing.assert_allclose(rows[:, 6], cert[:, 6], rtol=1e-3, atol=1e-5)
+
+
+def test_two_delta_converges_to_closed_form():
+    """alpha=2, d=3 two-delta case: GPU iterate at 4000 its matches the oracle; its
+    certified bracket contains the closed form 3."""
+    fr = inputs.gen_two_delta(8, 8, (3, 1), (3, 4))
+    tau = tau_for(8, 8)
+    prob, st, rep = gpu_run(fr, 2.0, 4000, tau)
+    ref, _ = oracle.iterate(fr, 2.0, math.inf, tau, tau, 4000)
+    compare(fr, st, ref)
+    r, rows = prob.objective(per_pair=True)
+    assert rows[0, 6] - 1e-4 <= 3.0 <= rows[0, 2] + 1e-4
+
+
+# ------------------------------------------------------------------------- BASELINE configs
+def _config_parity(name, frames, pairs_ref, n_iters=None):
+    cfg = inputs.CONFIGS[name]
+    n = n_iters or cfg.iters
+    B, T, ny, nx = frames.shape
+    tau = tau_for(ny, nx)
+    prob, st, rep = gpu_run(frames, cfg.alpha, n, tau)
+    G = B * (T - 1)
+    errs = []
+    obj_g = prob.objective(per_pair=True)[1]
+    for g in pairs_ref:
+        b, t = divmod(g, T - 1)
+        sub = np.ascontiguousarray(frames[b:b + 1, t:t + 2])
+        ref, rrep = oracle.iterate(sub, cfg.alpha, math.inf, tau, tau, n)
+        sg = {k: v.reshape(G, ny, nx)[g:g + 1] for k, v in st.items()}
+        errs.append(compare(sub, sg, ref))
+        cert = oracle.certificate(sub, ref, cfg.alpha)
+        assert obj_g[g, 7] == pytest.approx(cert[0, 7], rel=OBJ_RTOL), (g, obj_g[g], cert[0])
+        assert obj_g[g, 2] == pytest.approx(cert[0, 2], rel=OBJ_RTOL)
+    return prob, errs
+
+
+def test_parity_C1():
+    fr = inputs.gen_c1()
+    prob, errs = _config_parity("C1", fr, [0])
+
+
+def test_parity_C2():
+    fr = inputs.gen_c2()
+    prob, errs = _config_parity("C2", fr, [0])
+
+
+def test_parity_C3_subset():
+    """Full C3 launch (63 pairs, 1000 its); pairs are independent in fixed mode,
+    so an oracle run on a subset of pairs is an exact check."""
+    fr = inputs.gen_c3()
+    prob, errs = _config_parity("C3", fr, [0, 31, 62])
+
+
+@pytest.mark.slow
+def test_parity_C4_subset():
+    """Full C4 launch (255 pairs of 1024^2, 500 its) on one GPU; 2 pairs vs oracle."""
+    fr = inputs.gen_c4()
+    prob, errs = _config_parity("C4", fr, [0, 200])
+
+
+def test_parity_C5_windows():
+    """C5 (4096^2 pairs, 300 its) at full size: each pixel after k iterations
+    depends only on inputs within Chebyshev distance k (one stencil ring per
+    iteration), so the oracle on a (2k+3)^2 window (clipped at the grid edge)
+    gives that pixel exactly.  Sampled pixels vs those windows."""
+    cfg = inputs.CONFIGS["C5"]
+    fr = inputs.gen_c5(pairs=range(2))                 # 2 pairs of the config (pairs are independent)
+    B, T, ny, nx = fr.shape
+    n = cfg.iters
+    tau = tau_for(ny, nx)
+    prob, st, rep = gpu_run(fr, cfg.alpha, n, tau)
+    R = n + 2
+    for (b, j, i) in [(0, 2048, 1000), (1, 5, 4090), (0, 4095, 0)]:
+        j0, j1 = max(0, j - R), min(ny, j + R + 1)
+        i0, i1 = max(0, i - R), min(nx, i + R + 1)
+        sub = np.ascontiguousarray(fr[b:b + 1, :, j0:j1, i0:i1])
+        ref, _ = oracle.iterate(sub, cfg.alpha, math.inf, tau, tau, n)
+        fwin = (sub[0, 1].astype(np.float64) - sub[0, 0])
+        for name in ("mx", "my", "r", "a"):
+            gv = st[name][b, 0, j, i]
+            rv = getattr(ref, name)[0, 0, j - j0, i - i0]
+            scale = max(np.abs(getattr(ref, name)).max(), np.abs(fwin).max())
+            assert abs(gv - rv) / scale <= ITER_TOL, (name, b, j, i, gv, rv)
+
+
+def test_parity_C5_objective_full_grid():
+    """Objective of one full 4096^2 C5 pair after 20 iterations (same launch config)."""
+    cfg = inputs.CONFIGS["C5"]
+    fr = inputs.gen_c5(pairs=[0])
+    tau = tau_for(4096, 4096)
+    prob, st, rep = gpu_run(fr, cfg.alpha, 20, tau)
+    ref, rrep = oracle.iterate(fr, cfg.alpha, math.inf, tau, tau, 20)
+    compare(fr, st, ref)
+    assert rep["objective"] == pytest.approx(rrep[0, 0] + cfg.alpha * rrep[0, 1], rel=OBJ_RTOL)
+
+
+# ------------------------------------------------------------------------- API semantics
+def test_warm_start_and_determinism():
+    fr = inputs.gen_random(2, 3, 40, 64, seed=5, kind="sparse")
+    t = torch.from_numpy(fr).cuda()
+    p1 = Problem(t, 1.5)
+    p1.step(30)
+    p1.step(45)
+    p2 = Problem(t, 1.5)
+    p2.step(75)
+    for k in ("mx", "my", "r", "a"):
+        assert torch.equal(p1.state()[k], p2.state()[k])
+    r1 = p1.step(0, report=True)
+    assert r1["iterations"] == 75
+
+
+def test_solve_device_side_stop_matches_oracle():
+    """uot_solve stops on the device (L13); the returned state is iterate k_c,
+    and the oracle run for k_c iterations satisfies the same stopping test."""
+    fr = inputs.gen_random(1, 2, 12, 16, seed=9, kind="uniform")
+    tau = tau_for(12, 16)
+    prob = Problem(torch.from_numpy(fr).cuda(), 0.8, tau1=tau, tau2=tau)
+    tol = 1e-4
+    rep = prob.solve(20000, tol=tol, check_every=10)
+    assert rep["converged"] == 1 and rep["status"] == 0
+    kc = rep["iterations"]
+    assert kc % 10 == 0 and 0 < kc < 20000
+    ref, rrep = oracle.iterate(fr, 0.8, math.inf, tau, tau, kc)
+    st = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
+    compare(fr, st, ref)
+    fn = math.sqrt(rrep[0, 6])
+    assert math.sqrt(rrep[0, 2]) <= 1.5 * tol * fn
+    # a solve that cannot converge reports NOT_CONVERGED with a valid state
+    prob.reset()
+    rep = prob.solve(20, tol=1e-12, check_every=5)
+    assert rep["status"] == 3 and rep["iterations"] == 20
+
+
+def test_nonfinite_is_reported():
+    fr = inputs.gen_random(1, 2, 8, 8, seed=1)
+    fr[0, 1, 3, 3] = np.nan
+    prob = Problem(torch.from_numpy(fr).cuda(), 1.0)
+    from paper_1909_00149_b200._lib import UotError
+    with pytest.raises(UotError) as ei:
+        prob.step(3, report=True)
+    assert ei.value.code == 4
+
+
+def test_load_frames_host_matches_device_frames():
+    fr = inputs.gen_random(1, 3, 16, 32, seed=3)
+    fr2 = inputs.gen_random(1, 3, 16, 32, seed=4)
+    a = Problem(torch.from_numpy(fr).cuda(), 1.0)
+    a.load_frames_host(torch.from_numpy(fr2).pin_memory())
+    a.reset()
+    a.step(25)
+    b = Problem(torch.from_numpy(fr2).cuda(), 1.0)
+    b.step(25)
+    assert torch.equal(a.state()["a"], b.state()["a"])
