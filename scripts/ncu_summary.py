@@ -1,0 +1,82 @@
+#!/usr/bin/env python
+"""Summarise ncu outputs into profiles/ (run here, on the CPU box).
+
+  python scripts/ncu_summary.py launches <launches.csv> <out.md>
+  python scripts/ncu_summary.py full <report.ncu-rep> <config> <alg_bytes_per_launch> <out.json>
+"""
+import collections
+import csv
+import io
+import json
+import subprocess
+import sys
+
+
+def launches(path, out):
+    lines = open(path).read().splitlines()
+    start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
+    rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+    tot = collections.defaultdict(float)
+    cnt = collections.Counter()
+    for r in rows:
+        if r["Metric Name"] != "gpu__time_duration.sum":
+            continue
+        name = r["Kernel Name"].split("(")[0].replace("void ", "")
+        v = float(r["Metric Value"].replace(",", ""))
+        u = r["Metric Unit"]
+        us = v * 1e-3 if u == "ns" else (v if u in ("us", "usecond") else v * 1e3)
+        tot[name] += us
+        cnt[name] += 1
+    T = sum(tot.values())
+    with open(out, "w") as fh:
+        fh.write(f"# ncu launch list summary: {path}\n\n")
+        fh.write("ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised; compare SHARES)\n\n")
+        fh.write("| kernel | launches | total ms | share | avg us |\n|---|---|---|---|---|\n")
+        for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+            fh.write(f"| `{k[:80]}` | {cnt[k]} | {v / 1e3:.2f} | {100 * v / T:.1f}% | {v / cnt[k]:.1f} |\n")
+    print(open(out).read())
+
+
+METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+           "dram__bytes.sum.per_second", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+           "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+           "launch__grid_size", "launch__block_size", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+           "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "launch__occupancy_limit_registers",
+           "sm__cycles_elapsed.avg.per_second"]
+
+
+def full(rep, config, alg_bytes, out):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    res = {}
+    for vals in rows[2:]:
+        kname = vals[hdr.index("Kernel Name")]
+        d = {}
+        for m in METRICS:
+            if m in hdr:
+                d[m] = {"value": vals[hdr.index(m)], "unit": units[hdr.index(m)]}
+        res[kname] = d
+    def gb(x):
+        v = float(x["value"].replace(",", ""))
+        return v * {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3}[x["unit"]]
+    k, d = next(iter(res.items()))
+    traffic = (gb(d["dram__bytes_read.sum"]) + gb(d["dram__bytes_write.sum"])) * 1e9
+    summ = {"kernel": k, "report": rep, "metrics": d, "dram_bytes_per_launch": traffic,
+            "alg_bytes_per_launch": float(alg_bytes), "traffic_over_alg": traffic / float(alg_bytes)}
+    allp = {}
+    try:
+        allp = json.load(open(out))
+    except Exception:
+        pass
+    allp[config] = summ
+    json.dump(allp, open(out, "w"), indent=1)
+    print(json.dumps(summ, indent=1))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        full(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5])
