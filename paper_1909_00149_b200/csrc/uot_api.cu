@@ -63,12 +63,12 @@ __global__ void __launch_bounds__(256) k_setup_f(const SetupArgs S) {
     const int b = g / S.P, t = g % S.P;
     const float* x0 = S.frames + ((size_t)b * S.T + t) * (size_t)S.N;
     const float* x1 = x0 + S.N;
-    float* f = S.f + (size_t)g * S.N;
+    float* f = S.f ? S.f + (size_t)g * S.N : nullptr;
     double s2 = 0.0, s1 = 0.0;
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < S.N;
          k += (long long)S.bpp * blockDim.x) {
         const float v = x1[k] - x0[k];                    // f = x_{t+1} - x_t (L1)
-        f[k] = v;
+        if (S.f) f[k] = v;
         s2 += (double)v * v;
         s1 += fabs((double)v);
     }
@@ -193,6 +193,12 @@ __global__ void __launch_bounds__(256) k_pair_reduce(const ReduceArgs R) {
             *R.stop = 1;
         }
     }
+}
+
+// prox cold start (L8): x^0 = 0, or max(p, 0) with UOT_RESET_X_FROM_P
+__global__ void __launch_bounds__(256) k_init_x(const float* p, float* x, long long n, int from_p) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        x[k] = from_p ? fmaxf(p[k], 0.f) : 0.f;
 }
 
 __global__ void k_init_glob(double* glob, int* stop, int* counter, int reset_all) {
@@ -353,7 +359,6 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     if (!(p.tau1 >= 0.0) || !(p.tau2 >= 0.0) || !isfinite(p.tau1) || !isfinite(p.tau2))
         return fail(nullptr, UOT_E_INVALID, "tau1, tau2 must be finite and >= 0");
     const bool prox = isfinite(p.rho);
-    if (prox) return fail(nullptr, UOT_E_INVALID, "prox mode (finite rho) is not available in this build");
     if (p.tau1 == 0.0 || p.tau2 == 0.0) {
         double t1, t2;
         uot_default_steps(&p, 0.99, &t1, &t2);
@@ -368,6 +373,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     if (!b.frames || !b.mx[0] || !b.mx[1] || !b.my[0] || !b.my[1] || !b.r || !b.a[0] || !b.a[1] || !b.scratch)
         return fail(nullptr, UOT_E_INVALID, "a required buffer pointer is NULL");
     if (!prox && !b.f) return fail(nullptr, UOT_E_INVALID, "fixed mode needs buffers.f");
+    if (prox && (!b.x[0] || !b.x[1])) return fail(nullptr, UOT_E_INVALID, "prox mode needs buffers.x[0], x[1]");
     if (((uintptr_t)b.scratch & 7u) != 0) return fail(nullptr, UOT_E_INVALID, "scratch must be 8-byte aligned");
 
     int ndev = 0;
@@ -385,8 +391,10 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->B = p.n_chains; c->T = p.n_frames; c->P = p.n_frames - 1; c->G = c->B * c->P;
     c->nx = p.nx; c->ny = p.ny; c->N = (long long)p.nx * p.ny;
     c->prox = prox;
-    const bool vec4_ok = (p.nx % 4 == 0) && al16(b.frames) && al16(b.f) && al16(b.mx[0]) && al16(b.mx[1]) &&
-                         al16(b.my[0]) && al16(b.my[1]) && al16(b.r) && al16(b.a[0]) && al16(b.a[1]);
+    bool vec4_ok = (p.nx % 4 == 0) && al16(b.frames) && al16(b.mx[0]) && al16(b.mx[1]) &&
+                   al16(b.my[0]) && al16(b.my[1]) && al16(b.r) && al16(b.a[0]) && al16(b.a[1]);
+    if (prox) vec4_ok = vec4_ok && al16(b.x[0]) && al16(b.x[1]) && al16(b.a_prev_halo) && al16(b.a_next_halo);
+    else vec4_ok = vec4_ok && al16(b.f);
     c->geo = choose_geometry(p.nx, p.ny, c->G, vec4_ok);
     c->bpp = blocks_per_pair(c->N);
     c->tau1 = p.tau1; c->tau2 = p.tau2;
@@ -416,7 +424,7 @@ static int check_launch(uot_ctx* c, const char* what, bool kernel = true) {
 }
 
 static int launch_setup(uot_ctx* c) {
-    SetupArgs S{c->T, c->P, c->N, c->bpp, c->b.frames, c->b.f, c->part};
+    SetupArgs S{c->T, c->P, c->N, c->bpp, c->b.frames, c->prox ? nullptr : c->b.f, c->part};
     k_setup_f<<<dim3(c->bpp, c->G), 256, 0, c->s>>>(S);
     int rc = check_launch(c, "k_setup_f");
     if (rc) return rc;
@@ -430,7 +438,6 @@ static int launch_setup(uot_ctx* c) {
 
 int uot_reset(uot_ctx* c, uint32_t flags) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
-    (void)flags;
     const size_t bytes = (size_t)c->G * c->N * sizeof(float);
     cudaMemsetAsync(c->b.mx[0], 0, bytes, c->s);
     cudaMemsetAsync(c->b.my[0], 0, bytes, c->s);
@@ -441,6 +448,12 @@ int uot_reset(uot_ctx* c, uint32_t flags) {
     k_init_glob<<<1, 32, 0, c->s>>>(c->glob, c->stop, c->counter, 1);
     rc = check_launch(c, "k_init_glob");
     if (rc) return rc;
+    if (c->prox) {
+        const long long n = (long long)c->B * c->T * c->N;
+        k_init_x<<<4 * kSMs, 256, 0, c->s>>>(c->b.frames, c->b.x[0], n, (flags & UOT_RESET_X_FROM_P) ? 1 : 0);
+        rc = check_launch(c, "k_init_x");
+        if (rc) return rc;
+    }
     c->iter = 0;
     return launch_setup(c);
 }
@@ -454,10 +467,18 @@ int uot_load_frames(uot_ctx* c, const float* host_frames) {
 }
 
 extern "C++" {
-template <int V, bool RED>
+template <int V, bool RED, bool PROX>
 static void launch_iter_t(uot_ctx* c, const IterArgs& A) {
     const int blocks = (A.items + kWarps - 1) / kWarps;
-    k_iter_fixed<V, RED><<<blocks, kWarps * 32, 0, c->s>>>(A);
+    k_iter<V, RED, PROX><<<blocks, kWarps * 32, 0, c->s>>>(A);
+}
+template <int V>
+static void launch_iter_v(uot_ctx* c, const IterArgs& A, bool red, bool prox) {
+    if (prox) {
+        if (red) launch_iter_t<V, true, true>(c, A); else launch_iter_t<V, false, true>(c, A);
+    } else {
+        if (red) launch_iter_t<V, true, false>(c, A); else launch_iter_t<V, false, false>(c, A);
+    }
 }
 }
 
@@ -474,6 +495,13 @@ static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, c
         A.mx_out = c->b.mx[o]; A.my_out = c->b.my[o]; A.a_out = c->b.a[o];
         A.r = c->b.r;
         A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
+        A.G = c->G; A.T = c->T; A.P = c->P;
+        if (c->prox) {
+            const double rt = c->p.rho * c->tau1;
+            A.x_in = c->b.x[in]; A.x_out = c->b.x[o]; A.p = c->b.frames;
+            A.a_prev_halo = c->b.a_prev_halo; A.a_next_halo = c->b.a_next_halo;
+            A.c1 = (float)(rt / (1.0 + rt)); A.c2 = (float)(1.0 / (1.0 + rt)); A.c3 = (float)(c->tau1 / (1.0 + rt));
+        }
         A.partials = c->part;
         A.stop = stop;
         cudaEvent_t e1 = nullptr;
@@ -489,13 +517,10 @@ static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, c
             e1 = c->ev[c->ev_used + 1];
             c->ev_used += 2;
         }
-        if (c->geo.vec == 4) {
-            if (red) launch_iter_t<4, true>(c, A); else launch_iter_t<4, false>(c, A);
-        } else {
-            if (red) launch_iter_t<1, true>(c, A); else launch_iter_t<1, false>(c, A);
-        }
+        if (c->geo.vec == 4) launch_iter_v<4>(c, A, red, c->prox);
+        else launch_iter_v<1>(c, A, red, c->prox);
         if (e1) cudaEventRecord(e1, c->s);
-        int rc = check_launch(c, "k_iter_fixed");
+        int rc = check_launch(c, "k_iter");
         if (rc) return rc;
         c->iter++;
         if (red) {

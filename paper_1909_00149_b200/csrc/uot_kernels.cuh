@@ -34,6 +34,7 @@ constexpr unsigned kFull = 0xffffffffu;
 struct IterArgs {
     int nx, ny;
     int strips, segs, H, items;
+    int G, T, P;                      // pairs in context, frames / pairs per chain
     long long N;                      // nx*ny
     const float* f;                   // [G][N]            (fixed mode)
     const float* mx_in;               // [G][N] iteration k
@@ -44,6 +45,13 @@ struct IterArgs {
     float* a_out;
     float* r;                         // [G][N] in place
     float tau1, tau2, atau1;          // atau1 = alpha * tau1
+    // prox mode
+    const float* x_in;                // [B][T][N] iteration k
+    float* x_out;                     // [B][T][N] iteration k+1
+    const float* p;                   // [B][T][N] prox centres (= frames)
+    const float* a_prev_halo;         // [B][N] or nullptr
+    const float* a_next_halo;         // [B][N] or nullptr
+    float c1, c2, c3;                 // rho tau1/(1+rho tau1), 1/(1+rho tau1), tau1/(1+rho tau1)
     double* partials;                 // [items][kRec] when reducing
     const int* stop;                  // device stop flag or nullptr
 };
@@ -97,17 +105,35 @@ __device__ __forceinline__ float soft(float q, float s) {
     return copysignf(fmaxf(fabsf(q) - s, 0.f), q);
 }
 
-template <int V, bool RED>
+// Fused iteration.  PROX = false: fixed marginals (rho = inf), K = div M - r - f.
+// PROX = true: Alg.1 line 4 as well: frames x are iterates with
+// centres p; the warp of pair t also updates x_t (and x_{T-1} for the last
+// pair of the chain) from a_{t-1}, a_t, a_{t+1} at the same pixel:
+//   x_s' = max(0, c1 p_s + c2 x_s - c3 (A^T a)_s),  (A^T a)_s = a_s - a_{s-1},
+//   c1 = rho tau1/(1+rho tau1), c2 = 1/(1+rho tau1), c3 = tau1/(1+rho tau1),
+// with a_{-1} / a_{T-1} taken from the shard halos (or 0 at a chain end).
+template <int V, bool RED, bool PROX>
 __global__ void __launch_bounds__(kWarps * 32)
-k_iter_fixed(const IterArgs A) {
+k_iter(const IterArgs A) {
     if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
     const int lane = threadIdx.x & 31;
     const int item = blockIdx.x * kWarps + (threadIdx.x >> 5);
     if (item >= A.items) return;                        // warp-uniform
-    const int strip = item % A.strips;
-    const int rest = item / A.strips;
-    const int seg = rest % A.segs;
-    const int pair = rest / A.segs;
+    int strip, seg, pair;
+    if constexpr (PROX) {
+        // pair-fastest order: the 4 warps of a CTA are consecutive pairs at the same
+        // (segment, strip), so the neighbour-pair planes they share hit in L1/L2
+        pair = item % A.G;
+        const int rest = item / A.G;
+        strip = rest % A.strips;
+        seg = rest / A.strips;
+    } else {
+        strip = item % A.strips;
+        const int rest = item / A.strips;
+        seg = rest % A.segs;
+        pair = rest / A.segs;
+    }
+    const int rec = (pair * A.segs + seg) * A.strips + strip;   // partial record (pair-contiguous)
 
     const int nx = A.nx, ny = A.ny;
     const int i0 = strip * 32 * V;
@@ -119,7 +145,6 @@ k_iter_fixed(const IterArgs A) {
     const int j1 = min(j0 + A.H, ny);
     const size_t po = (size_t)pair * (size_t)A.N;
 
-    const float* __restrict__ fp = A.f + po;
     const float* __restrict__ mxi = A.mx_in + po;
     const float* __restrict__ myi = A.my_in + po;
     const float* __restrict__ ai = A.a_in + po;
@@ -128,6 +153,28 @@ k_iter_fixed(const IterArgs A) {
     float* __restrict__ ao = A.a_out + po;
     float* __restrict__ rp = A.r + po;
     const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1;
+
+    // fixed: f plane; prox: x_t, x_{t+1}, p_t, p_{t+1}, a_{t-1}, a_{t+1} planes, x' outputs
+    const float* __restrict__ fp = nullptr;
+    const float* __restrict__ x0i = nullptr; const float* __restrict__ x1i = nullptr;
+    const float* __restrict__ p0i = nullptr; const float* __restrict__ p1i = nullptr;
+    const float* __restrict__ ami = nullptr; const float* __restrict__ api = nullptr;
+    float* __restrict__ x0o = nullptr; float* __restrict__ x1o = nullptr;
+    bool last_pair = false;
+    if constexpr (PROX) {
+        const int b = pair / A.P, t = pair % A.P;
+        const size_t f0 = ((size_t)b * A.T + t) * (size_t)A.N;
+        x0i = A.x_in + f0; x1i = x0i + A.N;
+        p0i = A.p + f0; p1i = p0i + A.N;
+        x0o = A.x_out + f0;
+        last_pair = (t == A.P - 1);
+        if (last_pair) x1o = x0o + A.N;
+        ami = (t > 0) ? A.a_in + po - A.N : (A.a_prev_halo ? A.a_prev_halo + (size_t)b * A.N : nullptr);
+        api = (t < A.P - 1) ? A.a_in + po + A.N : (A.a_next_halo ? A.a_next_halo + (size_t)b * A.N : nullptr);
+    } else {
+        fp = A.f + po;
+    }
+    const float c1 = A.c1, c2 = A.c2, c3 = A.c3;
 
     bool colx[V];                                       // Mx exists / gx != 0: i < nx-1 (L3, L4)
 #pragma unroll
@@ -166,6 +213,7 @@ k_iter_fixed(const IterArgs A) {
 
     // ---- software-pipelined row loop ---------------------------------------------------
     float n_a[V], n_mx[V], n_my[V], n_r[V], n_f[V];
+    float n_x0[V], n_x1[V], n_p0[V], n_p1[V], n_am[V], n_ap[V];
     float n_aL = 0.f, n_aR = 0.f, n_mxL = 0.f, n_myL = 0.f;
     auto fetch = [&](int j) {
         const size_t rj = (size_t)j * nx;
@@ -174,10 +222,21 @@ k_iter_fixed(const IterArgs A) {
             ld_ro<V>(n_mx, mxi + rj + ib);
             ld_ro<V>(n_my, myi + rj + ib);
             ld_rw<V>(n_r, rp + rj + ib);
-            ld_ro<V>(n_f, fp + rj + ib);
+            if constexpr (PROX) {
+                ld_ro<V>(n_x0, x0i + rj + ib);
+                ld_ro<V>(n_x1, x1i + rj + ib);
+                ld_ro<V>(n_p0, p0i + rj + ib);
+                ld_ro<V>(n_p1, p1i + rj + ib);
+                if (ami) ld_ro<V>(n_am, ami + rj + ib); else zero<V>(n_am);
+                if (api) ld_ro<V>(n_ap, api + rj + ib); else zero<V>(n_ap);
+            } else {
+                ld_ro<V>(n_f, fp + rj + ib);
+            }
             if (has_next) ld_ro<V>(n_a, ai + rj + nx + ib); else zero<V>(n_a);
         } else {
-            zero<V>(n_mx); zero<V>(n_my); zero<V>(n_r); zero<V>(n_f); zero<V>(n_a);
+            zero<V>(n_mx); zero<V>(n_my); zero<V>(n_r); zero<V>(n_a);
+            if constexpr (PROX) { zero<V>(n_x0); zero<V>(n_x1); zero<V>(n_p0); zero<V>(n_p1); zero<V>(n_am); zero<V>(n_ap); }
+            else zero<V>(n_f);
         }
         if (lane == 0 && hasL) {
             n_mxL = __ldg(mxi + rj + iL);
@@ -188,12 +247,21 @@ k_iter_fixed(const IterArgs A) {
     };
     fetch(j0);
 
-    float s_tr = 0.f, s_gr = 0.f, s_k2 = 0.f, s_dz = 0.f, s_ub = 0.f;
+    float s_tr = 0.f, s_gr = 0.f, s_k2 = 0.f, s_dz = 0.f, s_ub = 0.f, s_px = 0.f;
 
     for (int j = j0; j < j1; ++j) {
         float c_a[V], c_mx[V], c_my[V], c_r[V], c_f[V];
+        float c_x0[V], c_x1[V], c_p0[V], c_p1[V], c_am[V], c_ap[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) { c_a[v] = n_a[v]; c_mx[v] = n_mx[v]; c_my[v] = n_my[v]; c_r[v] = n_r[v]; c_f[v] = n_f[v]; }
+        for (int v = 0; v < V; ++v) {
+            c_a[v] = n_a[v]; c_mx[v] = n_mx[v]; c_my[v] = n_my[v]; c_r[v] = n_r[v];
+            if constexpr (PROX) {
+                c_x0[v] = n_x0[v]; c_x1[v] = n_x1[v]; c_p0[v] = n_p0[v]; c_p1[v] = n_p1[v];
+                c_am[v] = n_am[v]; c_ap[v] = n_ap[v];
+            } else {
+                c_f[v] = n_f[v];
+            }
+        }
         const float c_aL = n_aL, c_aR = n_aR, c_mxL = n_mxL, c_myL = n_myL;
         if (j + 1 < j1) fetch(j + 1);
         const bool lastrow = (j == ny - 1);
@@ -218,6 +286,20 @@ k_iter_fixed(const IterArgs A) {
             // Alg.1 line 5: r <- shrink^{l1}_{alpha tau1}(r + tau1 a)
             rn[v] = soft(fmaf(t1, a_c[v], c_r[v]), at1);
             if constexpr (RED) s_tr += (n2 > 0.f) ? fmaxf(n2 * inv - t1, 0.f) : 0.f;
+        }
+        // Alg.1 line 4 (prox): x_t and x_{t+1} from the iteration-k duals
+        float x0n[V], x1n[V], fk[V], fn[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if constexpr (PROX) {
+                x0n[v] = fmaxf(fmaf(c1, c_p0[v], fmaf(c2, c_x0[v], -c3 * (a_c[v] - c_am[v]))), 0.f);
+                x1n[v] = fmaxf(fmaf(c1, c_p1[v], fmaf(c2, c_x1[v], -c3 * (c_ap[v] - a_c[v]))), 0.f);
+                fk[v] = c_x1[v] - c_x0[v];
+                fn[v] = x1n[v] - x0n[v];
+            } else {
+                fk[v] = c_f[v];
+                fn[v] = c_f[v];
+            }
         }
         // M'x and Mx at (j, i-1): previous lane, or recomputed halo for lane 0
         const float upn = __shfl_up_sync(kFull, mxn[V - 1], 1);
@@ -245,15 +327,25 @@ k_iter_fixed(const IterArgs A) {
             const float lmk = v ? mxk[(v + V - 1) % V] : lmk0;
             const float divn = (mxn[v] - lmn) + (myn[v] - myp_n[v]);
             const float divk = (mxk[v] - lmk) + (myk[v] - myp_o[v]);
-            const float Kn = divn - rn[v] - c_f[v];
-            const float Kk = divk - c_r[v] - c_f[v];
+            const float Kn = divn - rn[v] - fn[v];
+            const float Kk = divk - c_r[v] - fk[v];
             an[v] = fmaf(t2, 2.f * Kn - Kk, a_c[v]);
             if constexpr (RED) {
                 const float dmx = mxn[v] - mxk[v], dmy = myn[v] - myk[v], dr = rn[v] - c_r[v];
                 s_gr += fabsf(rn[v]);
                 s_k2 += Kn * Kn;
                 s_dz += dmx * dmx + dmy * dmy + dr * dr;
-                s_ub += fabsf(divn - c_f[v]);
+                s_ub += fabsf(divn - fn[v]);
+                if constexpr (PROX) {
+                    const float d0 = x0n[v] - c_x0[v], e0 = x0n[v] - c_p0[v];
+                    s_dz += d0 * d0;
+                    s_px += e0 * e0;
+                    if (last_pair) {
+                        const float d1 = x1n[v] - c_x1[v], e1 = x1n[v] - c_p1[v];
+                        s_dz += d1 * d1;
+                        s_px += e1 * e1;
+                    }
+                }
             }
         }
         if (act) {
@@ -262,6 +354,10 @@ k_iter_fixed(const IterArgs A) {
             st<V>(myo + rj, myn);
             st<V>(rp + rj, rn);
             st<V>(ao + rj, an);
+            if constexpr (PROX) {
+                st<V>(x0o + rj, x0n);
+                if (last_pair) st<V>(x1o + rj, x1n);
+            }
         }
 #pragma unroll
         for (int v = 0; v < V; ++v) { myp_n[v] = myn[v]; myp_o[v] = myk[v]; a_c[v] = c_a[v]; }
@@ -270,7 +366,7 @@ k_iter_fixed(const IterArgs A) {
     }
 
     if constexpr (RED) {
-        double d0 = s_tr, d1 = s_gr, d2 = s_k2, d3 = s_dz, d4 = s_ub;
+        double d0 = s_tr, d1 = s_gr, d2 = s_k2, d3 = s_dz, d4 = s_ub, d5 = s_px;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             d0 += __shfl_xor_sync(kFull, d0, o);
@@ -278,10 +374,11 @@ k_iter_fixed(const IterArgs A) {
             d2 += __shfl_xor_sync(kFull, d2, o);
             d3 += __shfl_xor_sync(kFull, d3, o);
             d4 += __shfl_xor_sync(kFull, d4, o);
+            if constexpr (PROX) d5 += __shfl_xor_sync(kFull, d5, o);
         }
         if (lane == 0) {
-            double* P = A.partials + (size_t)item * kRec;
-            P[0] = d0; P[1] = d1; P[2] = d2; P[3] = d3; P[4] = d4; P[5] = 0.0; P[6] = 0.0; P[7] = 0.0;
+            double* P = A.partials + (size_t)rec * kRec;
+            P[0] = d0; P[1] = d1; P[2] = d2; P[3] = d3; P[4] = d4; P[5] = PROX ? d5 : 0.0; P[6] = 0.0; P[7] = 0.0;
         }
     }
 }

@@ -56,7 +56,7 @@ class Problem:
 
     def __init__(self, frames: torch.Tensor, alpha: float, rho: float = math.inf,
                  tau1: float | None = None, tau2: float | None = None, *, stream: torch.cuda.Stream | None = None,
-                 force_steps: bool = False, reset: bool = True):
+                 force_steps: bool = False, reset: bool = True, halos: bool = False):
         if frames.dim() != 4:
             raise ValueError("frames must be [B][T][ny][nx]")
         if not frames.is_cuda or frames.dtype != torch.float32:
@@ -78,8 +78,9 @@ class Problem:
         self.r = e(plane)
         self.a = [e(plane), e(plane)]
         self.x = [e(self.frames.shape), e(self.frames.shape)] if self.prox else [None, None]
-        self.a_prev_halo = None
-        self.a_next_halo = None
+        # chain-prox shard halos (L19): duals of the pairs just outside this shard, [B][ny][nx]
+        self.a_prev_halo = torch.zeros((B, ny, nx), dtype=torch.float32, device=dev) if halos else None
+        self.a_next_halo = torch.zeros((B, ny, nx), dtype=torch.float32, device=dev) if halos else None
         self._params = _params(nx, ny, B, T, alpha, rho, tau1, tau2,
                                _lib.UOT_FORCE_STEPS if force_steps else 0)
         nsc = int(lib().uot_scratch_doubles(ctypes.byref(self._params)))
@@ -108,8 +109,8 @@ class Problem:
             b.a[k] = self.a[k].data_ptr()
             b.x[k] = self.x[k].data_ptr() if self.x[k] is not None else None
         b.r = self.r.data_ptr()
-        b.a_prev_halo = None
-        b.a_next_halo = None
+        b.a_prev_halo = self.a_prev_halo.data_ptr() if self.a_prev_halo is not None else None
+        b.a_next_halo = self.a_next_halo.data_ptr() if self.a_next_halo is not None else None
         b.scratch = self.scratch.data_ptr()
         return b
 

@@ -1,0 +1,120 @@
+"""GPU parity of the prox / chain-prox mode (Alg.1 line 4; L2, L19) vs the oracle,
+and bitwise equality of a frame-range-sharded chain (emulated on one GPU with
+copy-based halo exchange) with the unsharded chain."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1909_00149_b200 import inputs
+from paper_1909_00149_b200.uot import Problem
+
+pytestmark = pytest.mark.gpu
+
+
+def _cmp(fr, prob, ref, tol=1e-3):
+    B, T, ny, nx = fr.shape
+    f = np.abs(fr[:, 1:].astype(np.float64) - fr[:, :-1]).max()
+    st = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
+    errs = {}
+    for name in ("mx", "my", "r", "a", "x"):
+        rv = getattr(ref, name)
+        scale = max(np.abs(rv).max(), f, np.abs(fr).max() if name == "x" else 0.0)
+        errs[name] = np.abs(st[name] - rv).max() / scale
+    assert all(v <= tol for v in errs.values()), errs
+    return errs
+
+
+CASES = [(1, 2, 9, 12, 0.9, 2.0), (2, 2, 33, 64, 1.5, 0.5), (1, 5, 20, 36, 1.2, 3.0), (2, 4, 17, 128, 0.6, 10.0),
+         (1, 3, 40, 7, 2.0, 1.0)]
+
+
+@pytest.mark.parametrize("vec", [1, 4])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c)))
+@pytest.mark.parametrize("x_from_p", [False, True])
+def test_prox_parity(case, vec, x_from_p, monkeypatch):
+    B, T, ny, nx, alpha, rho = case
+    monkeypatch.setenv("UOT_VEC", str(vec))
+    fr = inputs.gen_random(B, T, ny, nx, seed=T * 7 + nx, kind="sparse")
+    tau = oracle.default_steps(nx, ny, prox=True, n_frames=T, safety=0.95)[0]
+    n = 70
+    prob = Problem(torch.from_numpy(fr).cuda(), alpha, rho=rho, tau1=tau, tau2=tau, reset=False)
+    prob.reset(x_from_p=x_from_p)
+    rep = prob.step(n, report=True)
+    s0 = oracle.zero_state(fr, prox=True, x_from_p=x_from_p)
+    ref, rrep = oracle.iterate(fr, alpha, rho, tau, tau, n, s0)
+    _cmp(fr, prob, ref)
+    obj = rrep[:, 0].sum() + alpha * rrep[:, 1].sum() + 0.5 * rho * rrep[:, 5].sum()
+    assert rep["objective"] == pytest.approx(obj, rel=1e-4, abs=1e-6)
+    assert rep["prox_term"] == pytest.approx(0.5 * rho * rrep[:, 5].sum(), rel=1e-4, abs=1e-6)
+    assert rep["dual_res"] == pytest.approx(math.sqrt(rrep[:, 3].sum()) / tau, rel=2e-2, abs=1e-4)
+    _, rows = prob.objective(per_pair=True)
+    cert = oracle.certificate(fr, ref, alpha, rho)
+    np.testing.assert_allclose(rows[:, 7], cert[:, 7], rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(rows[:, 2], cert[:, 2], rtol=1e-4, atol=1e-6)
+
+
+def test_prox_converges_to_kkt_point():
+    """Long prox run on the GPU: the fp32 fixed point satisfies x = Pi_+(p - A^T a / rho) (P15a)."""
+    fr = inputs.gen_random(1, 3, 12, 16, seed=3, kind="uniform")
+    rho, alpha = 2.0, 0.8
+    tau = oracle.default_steps(16, 12, prox=True, n_frames=3, safety=0.95)[0]
+    prob = Problem(torch.from_numpy(fr).cuda(), alpha, rho=rho, tau1=tau, tau2=tau)
+    prob.step(20000)
+    st = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
+    a = st["a"][0]
+    ATa = np.zeros_like(fr[0], dtype=np.float64)
+    for s in range(3):
+        ATa[s] = (a[s] if s < 2 else 0) - (a[s - 1] if s >= 1 else 0)
+    assert np.abs(st["x"][0] - np.maximum(fr[0] - ATa / rho, 0)).max() < 2e-4
+
+
+def _emulated_shards(fr, alpha, rho, tau, n, cut):
+    """Chain frames [0..T-1] split into shards [0..cut] and [cut..T-1] (shared frame `cut`);
+    per iteration the boundary duals are exchanged by device copies (what NCCL does across GPUs)."""
+    t = torch.from_numpy(fr).cuda()
+    A = Problem(t[:, :cut + 1].contiguous(), alpha, rho=rho, tau1=tau, tau2=tau, halos=True)
+    Bp = Problem(t[:, cut:].contiguous(), alpha, rho=rho, tau1=tau, tau2=tau, halos=True)
+    for _ in range(n):
+        sa, sb = A.slot, Bp.slot
+        Bp.a_prev_halo.copy_(A.a[sa][:, -1])
+        A.a_next_halo.copy_(Bp.a[sb][:, 0])
+        A.step(1)
+        Bp.step(1)
+    return A, Bp
+
+
+@pytest.mark.parametrize("T,cut", [(4, 2), (6, 1), (6, 4)])
+def test_sharded_chain_bitwise(T, cut):
+    fr = inputs.gen_random(2, T, 24, 64, seed=11, kind="sparse")
+    alpha, rho = 1.1, 4.0
+    tau = oracle.default_steps(64, 24, prox=True, n_frames=T, safety=0.95)[0]
+    n = 40
+    full = Problem(torch.from_numpy(fr).cuda(), alpha, rho=rho, tau1=tau, tau2=tau)
+    full.step(n)
+    A, Bp = _emulated_shards(fr, alpha, rho, tau, n, cut)
+    fs, sa, sb = full.state(), A.state(), Bp.state()
+    for k in ("mx", "my", "r", "a"):
+        assert torch.equal(fs[k][:, :cut], sa[k]), k
+        assert torch.equal(fs[k][:, cut:], sb[k]), k
+    assert torch.equal(fs["x"][:, :cut + 1], sa["x"])
+    assert torch.equal(fs["x"][:, cut:], sb["x"])
+    ref, _ = oracle.iterate(fr, alpha, rho, tau, tau, n)
+    _cmp(fr, full, ref)
+
+
+def test_chain_prox_C3_full_size_reduced_iterations():
+    """C3 launch configuration (64 frames, 256^2) in chain-prox mode (rho = 10, L15),
+    50 iterations, all pairs vs the oracle."""
+    cfg = inputs.CONFIGS["C3"]
+    fr = inputs.gen_c3()
+    rho, n = 10.0, 50
+    tau = oracle.default_steps(256, 256, prox=True, n_frames=64, safety=0.99)[0]
+    prob = Problem(torch.from_numpy(fr).cuda(), cfg.alpha, rho=rho, tau1=tau, tau2=tau)
+    rep = prob.step(n, report=True)
+    ref, rrep = oracle.iterate(fr, cfg.alpha, rho, tau, tau, n)
+    _cmp(fr, prob, ref)
+    obj = rrep[:, 0].sum() + cfg.alpha * rrep[:, 1].sum() + 0.5 * rho * rrep[:, 5].sum()
+    assert rep["objective"] == pytest.approx(obj, rel=1e-4)
