@@ -36,7 +36,11 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-ALG_BYTES_PER_PXIT = {"fixed": 36}   # read Mx,My,r,a,f; write Mx,My,r,a (fp32)
+# DESIGN.md "Algorithmic bytes" (fp32): fixed marginals read Mx,My,r,a,f and write Mx,My,r,a = 36 B per
+# pair-pixel-iteration; chain prox adds per frame x,p read + x write = 12 B (and has no f): 32 B/pair + 12 B/frame.
+def alg_bytes_per_iter(mode, G, B, T, N):
+    return 36 * G * N if mode == "fixed" else (32 * G + 12 * B * T) * N
+PROX_RHO = 10.0   # L15: chain-prox runs use rho = 10
 METRIC = "pixel-iterations/sec of the UOT prox step; achieved HBM GB/s vs peak"
 UNIT = "px-it/s"
 
@@ -49,6 +53,8 @@ def parse():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--iters", type=int, default=0, help="override the config's iteration count (testing only)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--mode", default="fixed", choices=["fixed", "prox"],
+                    help="fixed marginals (rho=inf) or chain prox (rho=10, per-iteration boundary-dual exchange)")
     ap.add_argument("--check-every", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -139,7 +145,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ CPU oracle
-def cpu_oracle_rate(cfg, seconds_target=12.0):
+def cpu_oracle_rate(cfg, seconds_target=12.0, rho=math.inf):
     """Oracle (oracle/, fp64 C, OpenMP over pairs) on a bounded sample of the workload.
     Returns (px-it/s, cores used, sample description)."""
     import numpy as np
@@ -153,17 +159,18 @@ def cpu_oracle_rate(cfg, seconds_target=12.0):
         fr = np.ascontiguousarray(make_frames(cfg, 0, n_pairs))
     pairs = fr.shape[0] * (fr.shape[1] - 1)
     N = cfg.nx * cfg.ny
-    t1 = oracle.default_steps(cfg.nx, cfg.ny, prox=False)[0]
+    t1 = oracle.default_steps(cfg.nx, cfg.ny, prox=math.isfinite(rho), n_frames=cfg.n_frames)[0]
     # calibrate: 2 iterations, then size the sample to ~seconds_target
     t0 = time.perf_counter()
-    oracle.iterate(fr, cfg.alpha, math.inf, t1, t1, 2)
+    oracle.iterate(fr, cfg.alpha, rho, t1, t1, 2)
     dt = max(time.perf_counter() - t0, 1e-3)
     its = int(max(2, min(cfg.iters, 2 * seconds_target / dt)))
     t0 = time.perf_counter()
-    oracle.iterate(fr, cfg.alpha, math.inf, t1, t1, its)
+    oracle.iterate(fr, cfg.alpha, rho, t1, t1, its)
     dt = time.perf_counter() - t0
     threads = min(int(os.environ.get("OMP_NUM_THREADS", cores)), pairs)
-    sample = f"{cfg.name}: {pairs} of {cfg.n_pairs} pairs x {N} px x {its} of {cfg.iters} iterations, fp64"
+    mode = "fixed marginals" if not math.isfinite(rho) else f"chain prox rho={rho}"
+    sample = f"{cfg.name} ({mode}): {pairs} of {cfg.n_pairs} pairs x {N} px x {its} of {cfg.iters} iterations, fp64"
     return pairs * N * its / dt, threads, sample, dt
 
 
@@ -174,7 +181,8 @@ def run_reference(args, cfg):
         return 0
     rates = []
     for k in range(args.warmup + args.steps):
-        rate, threads, sample, dt = cpu_oracle_rate(cfg, seconds_target=min(args.cpu_seconds, 8.0))
+        rate, threads, sample, dt = cpu_oracle_rate(cfg, seconds_target=min(args.cpu_seconds, 8.0),
+                                                    rho=PROX_RHO if args.mode == "prox" else math.inf)
         if k >= args.warmup:
             rates.append((rate, dt))
     value = sum(r for r, _ in rates) / len(rates)
@@ -183,7 +191,7 @@ def run_reference(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(d for _, d in rates) / len(rates),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generators, paper_1909_00149_b200/inputs.py)",
-        "config": config_dict(cfg, args.gpus),
+        "config": config_dict(cfg, args.gpus, args.mode),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -191,9 +199,10 @@ def run_reference(args, cfg):
     return 0
 
 
-def config_dict(cfg, gpus):
+def config_dict(cfg, gpus, mode="fixed"):
     return {"workload": f"{cfg.name}: {cfg.note}", "B": cfg.n_chains, "T": cfg.n_frames, "pairs": cfg.n_pairs,
-            "ny": cfg.ny, "nx": cfg.nx, "iterations": cfg.iters, "alpha": cfg.alpha, "mode": "fixed marginals (rho=inf)",
+            "ny": cfg.ny, "nx": cfg.nx, "iterations": cfg.iters, "alpha": cfg.alpha,
+            "mode": "fixed marginals (rho=inf)" if mode == "fixed" else f"chain prox (rho={PROX_RHO}, L15/L19)",
             "parallelism": f"frame-range shards x{gpus}" if gpus > 1 else "single GPU",
             "l2": "inputs larger than L2 (no flush needed)" if cfg.n_pairs * cfg.nx * cfg.ny * 36 > 126e6 * 4
             else "L2-resident workload (effective GB/s may exceed HBM peak)"}
@@ -251,14 +260,20 @@ def main():
 
     upload(host_pinned)
     torch.cuda.synchronize(dev)
-    prob = Problem(frames, cfg.alpha, stream=stream)
+    prox = args.mode == "prox"
+    rho = PROX_RHO if prox else math.inf
+    from paper_1909_00149_b200.uot import default_steps
+    tau, _ = default_steps(cfg.nx, cfg.ny, n_frames=cfg.n_frames, rho=rho)   # global chain length (L12)
+    prob = Problem(frames, cfg.alpha, rho=rho, tau1=tau, tau2=tau, stream=stream,
+                   halos=(prox and world > 1 and cfg.n_chains == 1))
+    driver = udist.ShardedChain(prob, rank, world)
     G = prob.G
     N = cfg.nx * cfg.ny
+    bytes_iter = alg_bytes_per_iter(args.mode, G, prob.B, prob.T, N)
 
     def step():
         prob.reset()
-        rep = prob.solve(cfg.iters, tol=1e-12, check_every=args.check_every)
-        return rep
+        return driver.run(cfg.iters, check_every=args.check_every, tol=1e-12)
 
     def barrier():
         if world > 1:
@@ -305,19 +320,21 @@ def main():
     prob.set_timing(False)
     launches = prob.launches - launches0
     ms_max = max_over_ranks(ms)
+    alg_gbs_job = sum_over_ranks(float(bytes_iter) * iters_done) / (ms_max / 1e3) / 1e9
     pxit_total = sum_over_ranks(float(G) * N * iters_done)
     value = pxit_total / (ms_max / 1e3)
 
-    # ---- roofline of the dominant kernel (fused iteration), per launch
+    # ---- roofline of the dominant kernel (fused iteration), per iteration (1 launch, or
+    #      interior + boundary launches in overlapped chain-prox shards)
     peak, peak_src = load_peaks()
-    alg_bytes_launch = ALG_BYTES_PER_PXIT["fixed"] * G * N
-    avg_launch_s = (kern_ms / max(kern_n, 1)) / 1e3
+    alg_bytes_launch = bytes_iter
+    avg_launch_s = (kern_ms / max(iters_done, 1)) / 1e3
     achieved = alg_bytes_launch / avg_launch_s / 1e9
     traffic = None
     prof_sum = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof_sum):
         try:
-            d = json.load(open(prof_sum)).get(cfg.name)
+            d = json.load(open(prof_sum)).get(cfg.name if not prox else cfg.name + "-prox")
             if d:
                 traffic = d.get("dram_bytes_per_launch")
         except Exception:
@@ -332,7 +349,7 @@ def main():
         def e2e_step():
             upload(host_pinned)
             prob.reset()
-            return prob.solve(cfg.iters, tol=1e-12, check_every=args.check_every)
+            return driver.run(cfg.iters, check_every=args.check_every, tol=1e-12)
 
         for _ in range(max(1, args.warmup // 2)):
             e2e_step()
@@ -354,7 +371,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            rate, threads, sample, _ = cpu_oracle_rate(cfg, args.cpu_seconds)
+            rate, threads, sample, _ = cpu_oracle_rate(cfg, args.cpu_seconds, rho=rho)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
         except Exception as ex:   # the oracle is a reported baseline, not the product
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {ex}"}
@@ -366,17 +383,17 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded generators, paper_1909_00149_b200/inputs.py; no dataset in the paper's bench)",
-            "config": config_dict(cfg, world),
+            "config": config_dict(cfg, world, args.mode),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_iter_fixed (fused Alg.1 iteration)",
+                         "kernel": f"k_iter<{'prox' if prox else 'fixed'}> (fused Alg.1 iteration)",
                          "alg_bytes_per_launch": alg_bytes_launch, "avg_launch_ms": avg_launch_s * 1e3,
                          "launches_timed": kern_n, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "hbm_gbs_step": ALG_BYTES_PER_PXIT["fixed"] * value / 1e9,
+            "hbm_gbs_step": alg_gbs_job,
             "objective": last["objective"], "iterations_per_step": iters_done // args.steps,
         }
         print(json.dumps(line), flush=True)

@@ -130,6 +130,29 @@ int uot_reset(uot_ctx* ctx, uint32_t flags);
  * B*T*ny*nx floats in the same layout.  Async w.r.t. the host if pinned. */
 int uot_load_frames(uot_ctx* ctx, const float* host_frames);
 
+/* Asynchronous iterations: enqueue n_iters >= 0 iterations with the residual
+ * reductions every check_every-th iteration (0 = none) and on the last one;
+ * tol > 0 arms the device-side stopping test (L13) -- later launches exit
+ * immediately once it passes.  No host synchronisation; read the result with
+ * uot_get_report. */
+int uot_iterate(uot_ctx* ctx, int32_t n_iters, int32_t check_every, double tol);
+
+/* One iteration restricted to a part of the pairs, for overlapping the shard
+ * halo exchange: UOT_PART_INTERIOR runs the pairs that
+ * do not read a_prev_halo / a_next_halo (first / last pair of each chain) and
+ * does NOT complete the iteration; UOT_PART_BOUNDARY runs the others and
+ * completes it (slot flip, reductions if reduce != 0).  UOT_PART_ALL = both.
+ * Async. */
+#define UOT_PART_ALL       0
+#define UOT_PART_INTERIOR  1
+#define UOT_PART_BOUNDARY  2
+int uot_iterate_part(uot_ctx* ctx, int32_t part, int32_t reduce);
+
+/* Synchronise the context stream and return the reductions of the last
+ * reducing iteration (and the iteration count, corrected if the device
+ * stopped early). */
+int uot_get_report(uot_ctx* ctx, uot_report* out);
+
 /* Run n_iters >= 0 iterations (Alg.1 lines 3-7).  out == NULL: fully async
  * (graph-capturable, no host sync); out != NULL: the last iteration also
  * computes the reductions and the call synchronises the stream to fill *out. */

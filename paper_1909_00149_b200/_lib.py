@@ -19,9 +19,10 @@ UOT_E_NONFINITE = 4
 UOT_E_CUDA = 5
 UOT_FORCE_STEPS = 1
 UOT_RESET_X_FROM_P = 1
+UOT_PART_ALL, UOT_PART_INTERIOR, UOT_PART_BOUNDARY = 0, 1, 2
 
 EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset", "uot_load_frames",
-            "uot_prox_step", "uot_solve", "uot_objective", "uot_set_timing", "uot_get_timing",
+            "uot_iterate", "uot_iterate_part", "uot_get_report", "uot_prox_step", "uot_solve", "uot_objective", "uot_set_timing", "uot_get_timing",
             "uot_state_slot", "uot_launch_count",
             "uot_destroy", "uot_last_error")
 
@@ -77,6 +78,11 @@ def lib():
     L.uot_create.argtypes = [P, B, ctypes.c_void_p, ctx_pp]; L.uot_create.restype = ctypes.c_int
     L.uot_reset.argtypes = [ctypes.c_void_p, ctypes.c_uint32]; L.uot_reset.restype = ctypes.c_int
     L.uot_load_frames.argtypes = [ctypes.c_void_p, ctypes.c_void_p]; L.uot_load_frames.restype = ctypes.c_int
+    L.uot_iterate.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_double]
+    L.uot_iterate.restype = ctypes.c_int
+    L.uot_iterate_part.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
+    L.uot_iterate_part.restype = ctypes.c_int
+    L.uot_get_report.argtypes = [ctypes.c_void_p, R]; L.uot_get_report.restype = ctypes.c_int
     L.uot_prox_step.argtypes = [ctypes.c_void_p, ctypes.c_int32, R]; L.uot_prox_step.restype = ctypes.c_int
     L.uot_solve.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, R]
     L.uot_solve.restype = ctypes.c_int

@@ -240,6 +240,7 @@ struct uot_ctx {
     int* stop;
     int* counter;
     bool timing;
+    bool stop_armed;
     std::vector<cudaEvent_t> ev;     // event pool, pairs (start, stop)
     size_t ev_used;
     char err[512];
@@ -411,6 +412,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->counter = ints + 1;
     c->err[0] = 0;
     c->timing = false;
+    c->stop_armed = false;
     c->ev_used = 0;
     *out = c;
     return UOT_OK;
@@ -482,13 +484,25 @@ static void launch_iter_v(uot_ctx* c, const IterArgs& A, bool red, bool prox) {
 }
 }
 
-static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
-    for (int k = 0; k < n; ++k) {
-        const int in = (int)(c->iter & 1), o = in ^ 1;
-        const bool red = (reduce_last && k == n - 1) || (reduce_every > 0 && ((k + 1) % reduce_every == 0));
+// Pairs selected by a launch: all, interior (not adjacent to a shard halo), boundary.
+static int pairs_in_part(const uot_ctx* c, int part) {
+    if (part == UOT_PART_ALL) return c->G;
+    const int nb = c->P >= 2 ? 2 : 1;
+    if (part == UOT_PART_BOUNDARY) return c->B * nb;
+    return c->B * (c->P - nb);
+}
+
+// One kernel launch of iteration c->iter for `part`; part ALL / BOUNDARY completes
+// the iteration (slot flip, reductions when `red`).
+static int launch_one(uot_ctx* c, int part, bool red, const int* stop, double tol) {
+    const int in = (int)(c->iter & 1), o = in ^ 1;
+    const int gsel = pairs_in_part(c, part);
+    if (gsel > 0) {
         IterArgs A{};
         A.nx = c->nx; A.ny = c->ny;
-        A.strips = c->geo.strips; A.segs = c->geo.segs; A.H = c->geo.H; A.items = c->geo.items;
+        A.strips = c->geo.strips; A.segs = c->geo.segs; A.H = c->geo.H;
+        A.items = gsel * c->geo.strips * c->geo.segs;
+        A.sel = part; A.Gsel = gsel;
         A.N = c->N;
         A.f = c->b.f;
         A.mx_in = c->b.mx[in]; A.my_in = c->b.my[in]; A.a_in = c->b.a[in];
@@ -522,17 +536,27 @@ static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, c
         if (e1) cudaEventRecord(e1, c->s);
         int rc = check_launch(c, "k_iter");
         if (rc) return rc;
-        c->iter++;
-        if (red) {
-            ReduceArgs R{};
-            R.partials = c->part; R.recs_per_pair = c->geo.strips * c->geo.segs; R.G = c->G;
-            R.pair_out = c->pair_it; R.glob = c->glob; R.counter = c->counter;
-            R.stop = const_cast<int*>(stop); R.max_mask = 0u; R.is_iteration = 1; R.is_setup = 0;
-            R.iteration = c->iter; R.tol = tol; R.tau1 = c->tau1;
-            k_pair_reduce<<<c->G, 256, 0, c->s>>>(R);
-            rc = check_launch(c, "k_pair_reduce(iter)");
-            if (rc) return rc;
-        }
+    }
+    if (part == UOT_PART_INTERIOR) return UOT_OK;
+    c->iter++;
+    if (red) {
+        ReduceArgs R{};
+        R.partials = c->part; R.recs_per_pair = c->geo.strips * c->geo.segs; R.G = c->G;
+        R.pair_out = c->pair_it; R.glob = c->glob; R.counter = c->counter;
+        R.stop = const_cast<int*>(stop); R.max_mask = 0u; R.is_iteration = 1; R.is_setup = 0;
+        R.iteration = c->iter; R.tol = tol; R.tau1 = c->tau1;
+        k_pair_reduce<<<c->G, 256, 0, c->s>>>(R);
+        int rc = check_launch(c, "k_pair_reduce(iter)");
+        if (rc) return rc;
+    }
+    return UOT_OK;
+}
+
+static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
+    for (int k = 0; k < n; ++k) {
+        const bool red = (reduce_last && k == n - 1) || (reduce_every > 0 && ((k + 1) % reduce_every == 0));
+        int rc = launch_one(c, UOT_PART_ALL, red, stop, tol);
+        if (rc) return rc;
     }
     return UOT_OK;
 }
@@ -561,40 +585,66 @@ static void fill_report(const uot_ctx* c, const double* h, uot_report* out) {
     out->nonfinite = h[GL_NONF] != 0.0;
 }
 
+int uot_iterate(uot_ctx* c, int32_t n, int32_t check_every, double tol) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    if (n < 0 || check_every < 0) return fail(c, UOT_E_INVALID, "n_iters and check_every must be >= 0");
+    const int* stop = nullptr;
+    if (tol > 0.0) {
+        k_init_glob<<<1, 32, 0, c->s>>>(c->glob, c->stop, c->counter, 0);
+        int rc = check_launch(c, "k_init_glob");
+        if (rc) return rc;
+        stop = c->stop;
+        c->stop_armed = true;
+    }
+    return launch_iters(c, n, check_every, n > 0, stop, tol);
+}
+
+int uot_iterate_part(uot_ctx* c, int32_t part, int32_t reduce) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    if (part != UOT_PART_ALL && part != UOT_PART_INTERIOR && part != UOT_PART_BOUNDARY)
+        return fail(c, UOT_E_INVALID, "bad part %d", part);
+    return launch_one(c, part, reduce != 0, nullptr, 0.0);
+}
+
+int uot_get_report(uot_ctx* c, uot_report* out) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    double h[GL_N];
+    int rc = read_glob(c, h);
+    if (rc) return rc;
+    if (c->stop_armed) {
+        if (h[GL_CONV] >= 0.0) c->iter = (int64_t)h[GL_CONV];             // later launches exited early
+        else if (h[GL_NONF] != 0.0 && h[GL_LASTRED] > 0) c->iter = (int64_t)h[GL_LASTRED];
+        c->stop_armed = false;
+    }
+    uot_report rep;
+    fill_report(c, h, &rep);
+    if (out) *out = rep;
+    if (rep.nonfinite) return fail(c, UOT_E_NONFINITE, "non-finite value in the reductions");
+    return UOT_OK;
+}
+
 int uot_prox_step(uot_ctx* c, int32_t n, uot_report* out) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     if (n < 0) return fail(c, UOT_E_INVALID, "n_iters < 0");
     int rc = launch_iters(c, n, 0, out != nullptr && n > 0, nullptr, 0.0);
     if (rc) return rc;
-    if (out) {
-        double h[GL_N];
-        rc = read_glob(c, h);
-        if (rc) return rc;
-        fill_report(c, h, out);
-        if (out->nonfinite) return fail(c, UOT_E_NONFINITE, "non-finite value in the reductions");
-    }
-    return UOT_OK;
+    return out ? uot_get_report(c, out) : UOT_OK;
 }
 
 int uot_solve(uot_ctx* c, int32_t max_iters, double tol, int32_t check_every, uot_report* out) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     if (max_iters < 0 || check_every < 1) return fail(c, UOT_E_INVALID, "max_iters >= 0 and check_every >= 1 required");
+    // always arm the device-side stop (tol <= 0 never triggers it, but non-finite values do)
     k_init_glob<<<1, 32, 0, c->s>>>(c->glob, c->stop, c->counter, 0);
     int rc = check_launch(c, "k_init_glob");
     if (rc) return rc;
-    const int64_t start = c->iter;
+    c->stop_armed = true;
     rc = launch_iters(c, max_iters, check_every, max_iters > 0, c->stop, tol);
     if (rc) return rc;
-    double h[GL_N];
-    rc = read_glob(c, h);
-    if (rc) return rc;
-    if (h[GL_CONV] >= 0.0) c->iter = (int64_t)h[GL_CONV];    // later launches exited early
-    else if (h[GL_NONF] != 0.0 && h[GL_LASTRED] > 0) c->iter = (int64_t)h[GL_LASTRED];
-    (void)start;
     uot_report rep;
-    fill_report(c, h, &rep);
+    rc = uot_get_report(c, &rep);
     if (out) *out = rep;
-    if (rep.nonfinite) return fail(c, UOT_E_NONFINITE, "non-finite value in the reductions");
+    if (rc) return rc;
     if (tol > 0.0 && !rep.converged) return fail(c, UOT_E_NOT_CONVERGED, "not converged after %d iterations", max_iters);
     return UOT_OK;
 }

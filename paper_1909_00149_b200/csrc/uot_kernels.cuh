@@ -35,6 +35,7 @@ struct IterArgs {
     int nx, ny;
     int strips, segs, H, items;
     int G, T, P;                      // pairs in context, frames / pairs per chain
+    int sel, Gsel;                    // pair selection (UOT_PART_*) and number of selected pairs
     long long N;                      // nx*ny
     const float* f;                   // [G][N]            (fixed mode)
     const float* mx_in;               // [G][N] iteration k
@@ -123,8 +124,20 @@ k_iter(const IterArgs A) {
     if constexpr (PROX) {
         // pair-fastest order: the 4 warps of a CTA are consecutive pairs at the same
         // (segment, strip), so the neighbour-pair planes they share hit in L1/L2
-        pair = item % A.G;
-        const int rest = item / A.G;
+        const int q = item % A.Gsel;
+        const int rest = item / A.Gsel;
+        if (A.sel == 0) {
+            pair = q;
+        } else {
+            const int nb = A.P >= 2 ? 2 : 1;              // boundary pairs per chain
+            if (A.sel == 2) {
+                const int b = q / nb, k = q % nb;
+                pair = b * A.P + (k == 0 ? 0 : A.P - 1);
+            } else {
+                const int Pi = A.P - nb, b = q / Pi;
+                pair = b * A.P + 1 + q % Pi;
+            }
+        }
         strip = rest % A.strips;
         seg = rest / A.strips;
     } else {

@@ -46,11 +46,12 @@ def exchange_boundary_frame(frames: torch.Tensor, rank: int, world: int, group=N
 
 
 def exchange_boundary_duals(a_first: torch.Tensor, a_last: torch.Tensor, prev_halo: torch.Tensor | None,
-                            next_halo: torch.Tensor | None, rank: int, world: int, group=None):
+                            next_halo: torch.Tensor | None, rank: int, world: int, group=None, wait: bool = True):
     """Chain-prox exchange (L19): the dual of this shard's first pair goes to
-    rank-1 (its next_halo), the dual of the last pair to rank+1 (its prev_halo)."""
+    rank-1 (its next_halo), the dual of the last pair to rank+1 (its prev_halo).
+    wait=False returns the works (the caller waits before the boundary pairs)."""
     if world == 1:
-        return
+        return []
     ops = []
     if rank > 0:
         ops.append(dist.P2POp(dist.isend, a_first.contiguous(), rank - 1, group))
@@ -58,8 +59,12 @@ def exchange_boundary_duals(a_first: torch.Tensor, a_last: torch.Tensor, prev_ha
     if rank < world - 1:
         ops.append(dist.P2POp(dist.isend, a_last.contiguous(), rank + 1, group))
         ops.append(dist.P2POp(dist.irecv, next_halo, rank + 1, group))
-    for w in dist.batch_isend_irecv(ops):
-        w.wait()
+    works = dist.batch_isend_irecv(ops)
+    if wait:
+        for w in works:
+            w.wait()
+        return []
+    return works
 
 
 def all_reduce_report(rep: dict, device, keys=("objective", "transport", "growth", "prox_term", "upper_bound")):
@@ -76,3 +81,41 @@ def all_reduce_report(rep: dict, device, keys=("objective", "transport", "growth
     out["dual_res"] = float(t[len(keys) + 1].sqrt())
     out["f_norm"] = float(t[len(keys) + 2].sqrt())
     return out
+
+
+class ShardedChain:
+    """Drive one rank's shard of a chain (or batch) problem (a `uot.Problem`).
+
+    Fixed marginals: iterations have no data-path exchange -- one async
+    `uot_iterate` call.  Chain prox with world > 1: every iteration k sends the
+    shard's first/last pair duals a^k to the neighbours (NCCL P2P over NVLink)
+    while the INTERIOR pairs of iteration k run; the two boundary pairs run
+    after the receive completes (`uot_iterate_part`), so the exchange overlaps
+    compute (DESIGN.md "Multi-GPU").
+    """
+
+    def __init__(self, prob, rank: int = 0, world: int = 1, group=None, overlap: bool = True):
+        self.prob, self.rank, self.world, self.group, self.overlap = prob, rank, world, group, overlap
+        self.exchanging = prob.prox and world > 1
+        if self.exchanging and (prob.a_prev_halo is None or prob.a_next_halo is None):
+            raise ValueError("chain-prox shards need Problem(..., halos=True)")
+
+    def run(self, n_iters: int, check_every: int = 10, tol: float = 0.0) -> dict:
+        from ._lib import UOT_PART_ALL, UOT_PART_BOUNDARY, UOT_PART_INTERIOR
+        p = self.prob
+        if not self.exchanging:
+            p.iterate(n_iters, check_every=check_every, tol=tol)
+            return p.report()
+        for k in range(n_iters):
+            red = (check_every > 0 and (k + 1) % check_every == 0) or k == n_iters - 1
+            s = p.slot
+            works = exchange_boundary_duals(p.a[s][:, 0], p.a[s][:, -1], p.a_prev_halo, p.a_next_halo,
+                                            self.rank, self.world, self.group, wait=not self.overlap)
+            if self.overlap:
+                p.iterate_part(UOT_PART_INTERIOR, red)
+                for w in works:
+                    w.wait()
+                p.iterate_part(UOT_PART_BOUNDARY, red)
+            else:
+                p.iterate_part(UOT_PART_ALL, red)
+        return p.report()

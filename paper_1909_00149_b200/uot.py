@@ -136,6 +136,20 @@ class Problem:
         check(lib().uot_prox_step(self._ctx, int(n), None), self._ctx)
         return None
 
+    def iterate(self, n: int, check_every: int = 0, tol: float = 0.0):
+        """Enqueue n iterations asynchronously (reductions every check_every and on the last)."""
+        check(lib().uot_iterate(self._ctx, int(n), int(check_every), float(tol)), self._ctx)
+
+    def iterate_part(self, part: int, reduce: bool = False):
+        """One iteration on a part of the pairs (_lib.UOT_PART_INTERIOR / _BOUNDARY / _ALL)."""
+        check(lib().uot_iterate_part(self._ctx, int(part), int(bool(reduce))), self._ctx)
+
+    def report(self) -> dict:
+        """Sync and return the reductions of the last reducing iteration."""
+        rep = Report()
+        check(lib().uot_get_report(self._ctx, ctypes.byref(rep)), self._ctx)
+        return rep.as_dict()
+
     def solve(self, max_iters: int, tol: float = 0.0, check_every: int = 10, raise_not_converged=False) -> dict:
         rep = Report()
         allow = () if raise_not_converged else (_lib.UOT_E_NOT_CONVERGED,)
@@ -187,7 +201,7 @@ class Problem:
 
     @property
     def iterations(self) -> int:
-        return int(self.step(0, report=True)["iterations"])
+        return int(self.report()["iterations"])
 
     def close(self):
         if getattr(self, "_ctx", None):

@@ -118,3 +118,48 @@ def test_chain_prox_C3_full_size_reduced_iterations():
     _cmp(fr, prob, ref)
     obj = rrep[:, 0].sum() + cfg.alpha * rrep[:, 1].sum() + 0.5 * rho * rrep[:, 5].sum()
     assert rep["objective"] == pytest.approx(obj, rel=1e-4)
+
+
+@pytest.mark.parametrize("T", [2, 3, 7])
+def test_interior_boundary_parts_equal_full_iteration(T):
+    """uot_iterate_part(INTERIOR) + (BOUNDARY) == one full iteration, bitwise, with reductions."""
+    from paper_1909_00149_b200 import _lib
+    fr = inputs.gen_random(2, T, 20, 32, seed=21, kind="sparse")
+    tau = oracle.default_steps(32, 20, prox=True, n_frames=T, safety=0.95)[0]
+    t = torch.from_numpy(fr).cuda()
+    a = Problem(t, 0.9, rho=3.0, tau1=tau, tau2=tau)
+    b = Problem(t, 0.9, rho=3.0, tau1=tau, tau2=tau)
+    for k in range(12):
+        red = k % 4 == 3
+        a.iterate_part(_lib.UOT_PART_INTERIOR, red)
+        a.iterate_part(_lib.UOT_PART_BOUNDARY, red)
+        b.iterate(1, check_every=1 if red else 0)
+    ra, rb = a.report(), b.report()
+    for key in ("mx", "my", "r", "a", "x"):
+        assert torch.equal(a.state()[key], b.state()[key]), key
+    assert ra["objective"] == rb["objective"] and ra["iterations"] == rb["iterations"] == 12
+
+
+def test_sharded_chain_driver_overlap_emulated():
+    """ShardedChain-style overlapped schedule (interior pairs, halo copy, boundary pairs) on
+    two shards of one chain equals the unsharded chain bitwise."""
+    from paper_1909_00149_b200 import _lib
+    T, cut, n = 9, 4, 30
+    fr = inputs.gen_random(1, T, 16, 64, seed=5, kind="sparse")
+    tau = oracle.default_steps(64, 16, prox=True, n_frames=T, safety=0.95)[0]
+    t = torch.from_numpy(fr).cuda()
+    full = Problem(t, 1.3, rho=5.0, tau1=tau, tau2=tau)
+    full.iterate(n)
+    A = Problem(t[:, :cut + 1].contiguous(), 1.3, rho=5.0, tau1=tau, tau2=tau, halos=True)
+    B = Problem(t[:, cut:].contiguous(), 1.3, rho=5.0, tau1=tau, tau2=tau, halos=True)
+    for _ in range(n):
+        sa, sb = A.slot, B.slot
+        A.iterate_part(_lib.UOT_PART_INTERIOR, False)
+        B.iterate_part(_lib.UOT_PART_INTERIOR, False)
+        B.a_prev_halo.copy_(A.a[sa][:, -1])
+        A.a_next_halo.copy_(B.a[sb][:, 0])
+        A.iterate_part(_lib.UOT_PART_BOUNDARY, False)
+        B.iterate_part(_lib.UOT_PART_BOUNDARY, False)
+    assert torch.equal(full.state()["a"][:, :cut], A.state()["a"])
+    assert torch.equal(full.state()["a"][:, cut:], B.state()["a"])
+    assert torch.equal(full.state()["x"][:, cut:], B.state()["x"])
