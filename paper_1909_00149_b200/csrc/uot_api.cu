@@ -17,6 +17,7 @@
 
 #include "uot.h"
 #include "uot_kernels.cuh"
+#include "uot_persist.cuh"
 
 using namespace uotk;
 
@@ -158,22 +159,24 @@ __global__ void __launch_bounds__(256) k_pair_reduce(const ReduceArgs R) {
         am_last = (atomicAdd(R.counter, 1) == R.G - 1);
     }
     __syncthreads();
-    if (!am_last || threadIdx.x != 0) return;
+    if (!am_last) return;
     __threadfence();
-    // last block: pairs in fixed order
-    const volatile double* po = R.pair_out;
+    // last block: sum the pairs' rows in fixed order (thread q < 8 owns field q)
+    __shared__ double tot[kRec];
+    if (threadIdx.x < kRec) {
+        double v = 0.0;
+        for (int g2 = 0; g2 < R.G; ++g2) v += __ldcg(R.pair_out + (size_t)g2 * kRec + threadIdx.x);
+        tot[threadIdx.x] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
     *R.counter = 0;
     if (R.is_setup) {
-        double s2 = 0, s1 = 0;
-        for (int q = 0; q < R.G; ++q) { s2 += po[(size_t)q * kRec + 0]; s1 += po[(size_t)q * kRec + 1]; }
-        R.glob[GL_FSQ] = s2;
-        R.glob[GL_FL1] = s1;
+        R.glob[GL_FSQ] = tot[0];
+        R.glob[GL_FL1] = tot[1];
         return;
     }
     if (!R.is_iteration) return;
-    double tot[6] = {0, 0, 0, 0, 0, 0};
-    for (int q = 0; q < R.G; ++q)
-        for (int c = 0; c < 6; ++c) tot[c] += po[(size_t)q * kRec + c];
     bool nonfinite = false;
     for (int c = 0; c < 6; ++c) { R.glob[c] = tot[c]; nonfinite |= !isfinite(tot[c]); }
     R.glob[GL_LASTRED] = (double)R.iteration;
@@ -239,6 +242,10 @@ struct uot_ctx {
     double* glob;
     int* stop;
     int* counter;
+    float* pxchg;       // persistent kernel exchange slots
+    int* pflags;        // [kMaxPersistCtas] + barrier[2]
+    struct { bool ok; int TW, TH, tx, ty, ctas, threads; size_t smem; } pg;
+    int64_t persist_launches;
     bool timing;
     bool stop_armed;
     std::vector<cudaEvent_t> ev;     // event pool, pairs (start, stop)
@@ -280,13 +287,13 @@ static Geometry choose_geometry(int nx, int ny, int G, bool vec4_ok) {
         }
     }
     const int forced_vec = env_int("UOT_VEC", 0);
-    if (forced_vec == 1 || (forced_vec == 4 && vec4_ok)) g.vec = forced_vec;
+    if (forced_vec == 1 || ((forced_vec == 4 || forced_vec == 2) && vec4_ok)) g.vec = forced_vec;
     g.strips = (nx + 32 * g.vec - 1) / (32 * g.vec);
     const long long cols = (long long)G * g.strips;
     long long segs_needed = (target + cols - 1) / cols;
     int H = (int)((ny + segs_needed - 1) / segs_needed);
     if (H > 64) H = 64;
-    if (H < 4) H = 4;
+    if (H < (g.vec == 4 ? 8 : 4)) H = (g.vec == 4 ? 8 : 4);   // r01 sweep (profiles/r01_sweep_vec_segH.txt)
     const int forced_h = env_int("UOT_SEG_H", 0);
     if (forced_h > 0) H = forced_h < 4 ? 4 : forced_h;
     if (H > ny) H = ny;
@@ -303,9 +310,16 @@ static int blocks_per_pair(long long N) {
     return (int)b;
 }
 
+static const int kMaxPersistCtas = 148;          // one tile-CTA per SM at most
+static const int kMaxTileEdge = 4 * 128 + 4 * 64; // 4*TW + 4*TH for the largest tile
 static size_t part_records(const Geometry& g, int G, int bpp) {
     size_t a = (size_t)g.items, b = (size_t)G * bpp;
-    return a > b ? a : b;
+    size_t m = a > b ? a : b;
+    return m > (size_t)kMaxPersistCtas ? m : (size_t)kMaxPersistCtas;
+}
+// persistent-kernel exchange slots (floats) + flags/barrier (ints), in doubles
+static size_t persist_scratch_doubles() {
+    return ((size_t)kMaxPersistCtas * 2 * kMaxTileEdge) / 2 + (kMaxPersistCtas + 8) / 2 + 8;
 }
 
 static double chain_norm2(int nx, int ny, int T, bool prox) {
@@ -313,6 +327,61 @@ static double chain_norm2(int nx, int ny, int T, bool prox) {
     const double lam = (nx >= 2 ? 2.0 + 2.0 * cos(pi / nx) : 0.0) + (ny >= 2 ? 2.0 + 2.0 * cos(pi / ny) : 0.0);
     if (!prox) return lam + 1.0;                        // K = [D, -I]
     return lam + 1.0 + 2.0 + 2.0 * cos(pi / T);         // K = [D, -I, A], A path incidence (L12)
+}
+
+// Persistent SMEM-resident path (uot_persist.cuh): small grids whose tiles fit
+// one CTA per SM; fixed marginals, or prox with T == 2 and no shard halos.
+static void plan_persist(uot_ctx* c) {
+    c->pg.ok = false;
+    const int mode = env_int("UOT_PERSIST", -1);      // -1 auto, 0 off, 1 force when possible
+    if (mode == 0) return;
+    if (c->prox && (c->T != 2 || c->b.a_prev_halo || c->b.a_next_halo)) return;
+    int dev = 0, nsm = kSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (!coop) return;
+    const int limit = nsm < kMaxPersistCtas ? nsm : kMaxPersistCtas;
+    struct Cand { int TW, TH; };
+    const Cand cands[] = {{32, 16}, {32, 32}, {64, 32}, {64, 64}, {128, 64}};
+    int TW = 0, TH = 0;
+    if ((long long)c->nx * c->ny <= 8192 && c->nx <= 128 && c->ny <= 128 && c->G <= limit) {
+        TW = c->nx; TH = c->ny;                           // one tile per pair: no inter-CTA sync
+    } else {
+        for (const Cand& q : cands) {
+            const long long tiles = (long long)((c->nx + q.TW - 1) / q.TW) * ((c->ny + q.TH - 1) / q.TH);
+            if (tiles * c->G <= limit) { TW = q.TW; TH = q.TH; break; }
+        }
+    }
+    const char* tenv = getenv("UOT_TILE");            // "WxH" override (tuning)
+    if (tenv && *tenv) {
+        int w = 0, h = 0;
+        if (sscanf(tenv, "%dx%d", &w, &h) == 2 && w > 0 && h > 0 && w <= 128 && h <= 64) { TW = w; TH = h; }
+    }
+    if (TW == 0) return;
+    const PLayout L(TW, TH);
+    const size_t smem = L.floats(c->prox) * sizeof(float);
+    if (smem > 200 * 1024) return;
+    int threads = ((TW * TH / 4 + 31) / 32) * 32;
+    if (threads < 128) threads = 128;
+    if (threads > 512) threads = 512;
+    const void* fn = c->prox ? (const void*)k_persist<true> : (const void*)k_persist<false>;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        return;
+    }
+    const int tx = (c->nx + TW - 1) / TW, ty = (c->ny + TH - 1) / TH;
+    const int ctas = tx * ty * c->G;
+    if (ctas > per_sm * nsm || ctas > kMaxPersistCtas) return;
+    c->pg.ok = true;
+    c->pg.TW = TW; c->pg.TH = TH; c->pg.tx = tx; c->pg.ty = ty; c->pg.ctas = ctas;
+    c->pg.threads = threads; c->pg.smem = smem;
 }
 
 extern "C" {
@@ -332,7 +401,7 @@ size_t uot_scratch_doubles(const uot_params* p) {
     Geometry g1{1, (p->nx + 31) / 32, (p->ny + 3) / 4, 4, 0};
     size_t r1 = (size_t)G * g1.strips * g1.segs;
     if (r1 > recs) recs = r1;
-    return recs * kRec + 2 * (size_t)G * kRec + GL_N + 4;
+    return recs * kRec + 2 * (size_t)G * kRec + GL_N + 4 + persist_scratch_doubles();
 }
 
 int uot_default_steps(const uot_params* p, double safety, double* tau1, double* tau2) {
@@ -410,9 +479,13 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     int* ints = reinterpret_cast<int*>(c->glob + GL_N);
     c->stop = ints;
     c->counter = ints + 1;
+    c->pxchg = reinterpret_cast<float*>(c->glob + GL_N + 4);
+    c->pflags = reinterpret_cast<int*>(c->pxchg + (size_t)kMaxPersistCtas * 2 * kMaxTileEdge);
+    plan_persist(c);
     c->err[0] = 0;
     c->timing = false;
     c->stop_armed = false;
+    c->persist_launches = 0;
     c->ev_used = 0;
     *out = c;
     return UOT_OK;
@@ -532,6 +605,7 @@ static int launch_one(uot_ctx* c, int part, bool red, const int* stop, double to
             c->ev_used += 2;
         }
         if (c->geo.vec == 4) launch_iter_v<4>(c, A, red, c->prox);
+        else if (c->geo.vec == 2) launch_iter_v<2>(c, A, red, c->prox);
         else launch_iter_v<1>(c, A, red, c->prox);
         if (e1) cudaEventRecord(e1, c->s);
         int rc = check_launch(c, "k_iter");
@@ -552,7 +626,52 @@ static int launch_one(uot_ctx* c, int part, bool red, const int* stop, double to
     return UOT_OK;
 }
 
+static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
+    cudaError_t e = cudaMemsetAsync(c->pflags, 0, sizeof(int) * (kMaxPersistCtas + 2), c->s);
+    if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "memset flags: %s", cudaGetErrorString(e));
+    PersistArgs A{};
+    A.nx = c->nx; A.ny = c->ny; A.G = c->G; A.T = c->T; A.P = c->P; A.N = c->N;
+    A.TW = c->pg.TW; A.TH = c->pg.TH; A.tiles_x = c->pg.tx; A.tiles_y = c->pg.ty;
+    A.n_iters = n; A.red_every = reduce_every; A.red_last = reduce_last ? 1 : 0;
+    A.iter0 = c->iter; A.prox = c->prox;
+    A.f = c->b.f;
+    for (int q = 0; q < 2; ++q) {
+        A.mxb[q] = c->b.mx[q]; A.myb[q] = c->b.my[q]; A.ab[q] = c->b.a[q]; A.xb[q] = c->b.x[q];
+    }
+    A.r = c->b.r; A.p = c->b.frames;
+    A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
+    if (c->prox) {
+        const double rt = c->p.rho * c->tau1;
+        A.c1 = (float)(rt / (1.0 + rt)); A.c2 = (float)(1.0 / (1.0 + rt)); A.c3 = (float)(c->tau1 / (1.0 + rt));
+    }
+    A.xchg = c->pxchg; A.flags = c->pflags; A.bar = c->pflags + kMaxPersistCtas;
+    A.partials = c->part; A.pair_out = c->pair_it; A.glob = c->glob;
+    A.stop = const_cast<int*>(stop); A.tol = tol; A.tau1d = c->tau1;
+    void* args[] = {&A};
+    cudaEvent_t e1 = nullptr;
+    if (c->timing) {
+        while (c->ev_used + 2 > c->ev.size()) {
+            cudaEvent_t ev;
+            if (cudaEventCreate(&ev) != cudaSuccess) return fail(c, UOT_E_CUDA, "cudaEventCreate");
+            c->ev.push_back(ev);
+        }
+        cudaEventRecord(c->ev[c->ev_used], c->s);
+        e1 = c->ev[c->ev_used + 1];
+        c->ev_used += 2;
+    }
+    const void* fn = c->prox ? (const void*)k_persist<true> : (const void*)k_persist<false>;
+    e = cudaLaunchCooperativeKernel(fn, dim3(c->pg.ctas), dim3(c->pg.threads), args, c->pg.smem, c->s);
+    if (e1) cudaEventRecord(e1, c->s);
+    if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "k_persist launch: %s", cudaGetErrorString(e));
+    int rc = check_launch(c, "k_persist");
+    if (rc) return rc;
+    c->iter += n;            // uot_get_report corrects it if the device stopped early
+    c->persist_launches++;
+    return UOT_OK;
+}
+
 static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
+    if (c->pg.ok && n >= 2) return launch_persist(c, n, reduce_every, reduce_last, stop, tol);
     for (int k = 0; k < n; ++k) {
         const bool red = (reduce_last && k == n - 1) || (reduce_every > 0 && ((k + 1) % reduce_every == 0));
         int rc = launch_one(c, UOT_PART_ALL, red, stop, tol);

@@ -62,6 +62,9 @@ __device__ __forceinline__ void ld_ro(float (&d)[V], const float* p) {
     if constexpr (V == 4) {
         const float4 t = __ldg(reinterpret_cast<const float4*>(p));
         d[0] = t.x; d[1] = t.y; d[2] = t.z; d[3] = t.w;
+    } else if constexpr (V == 2) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+        d[0] = t.x; d[1] = t.y;
     } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) d[v] = __ldg(p + v);
@@ -73,6 +76,9 @@ __device__ __forceinline__ void ld_rw(float (&d)[V], const float* p) {
     if constexpr (V == 4) {
         const float4 t = *reinterpret_cast<const float4*>(p);
         d[0] = t.x; d[1] = t.y; d[2] = t.z; d[3] = t.w;
+    } else if constexpr (V == 2) {
+        const float2 t = *reinterpret_cast<const float2*>(p);
+        d[0] = t.x; d[1] = t.y;
     } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) d[v] = p[v];
@@ -83,6 +89,8 @@ template <int V>
 __device__ __forceinline__ void st(float* p, const float (&d)[V]) {
     if constexpr (V == 4) {
         *reinterpret_cast<float4*>(p) = make_float4(d[0], d[1], d[2], d[3]);
+    } else if constexpr (V == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(d[0], d[1]);
     } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) p[v] = d[v];

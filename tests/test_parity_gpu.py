@@ -24,7 +24,7 @@ OBJ_RTOL = 1e-4
 ITER_TOL = 1e-3
 
 
-def gpu_run(frames_np, alpha, n, tau, env=None, report=True):
+def gpu_run(frames_np, alpha, n, tau, env=None, report=True, check_every=0):
     old = {}
     for k, v in (env or {}).items():
         old[k] = os.environ.get(k)
@@ -38,7 +38,11 @@ def gpu_run(frames_np, alpha, n, tau, env=None, report=True):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-    rep = prob.step(n, report=report)
+    if check_every:
+        prob.iterate(n, check_every=check_every)
+        rep = prob.report()
+    else:
+        rep = prob.step(n, report=report)
     st = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
     return prob, st, rep
 
@@ -82,14 +86,19 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("vec", [1, 4])
-@pytest.mark.parametrize("H", [0, 4, 7])
+# path variants: streaming kernel with lane width V and segment height H (UOT_PERSIST=0),
+# or the SMEM-resident persistent kernel (UOT_PERSIST=1, used when the grid fits)
+PATHS = [dict(UOT_VEC=1, UOT_SEG_H=0, UOT_PERSIST=0), dict(UOT_VEC=1, UOT_SEG_H=4, UOT_PERSIST=0),
+         dict(UOT_VEC=4, UOT_SEG_H=7, UOT_PERSIST=0), dict(UOT_VEC=4, UOT_SEG_H=0, UOT_PERSIST=0),
+         dict(UOT_VEC=2, UOT_SEG_H=5, UOT_PERSIST=0), dict(UOT_PERSIST=1)]
+
+
+@pytest.mark.parametrize("env", PATHS, ids=lambda e: "-".join(f"{k[4:]}{v}" for k, v in e.items()))
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c[:4])) + f"-a{c[4]}")
-def test_parity_small(case, vec, H):
+def test_parity_small(case, env):
     B, T, ny, nx, alpha, n, kind = case
     fr = inputs.gen_random(B, T, ny, nx, seed=100 + ny + nx, kind=kind)
     tau = tau_for(ny, nx)
-    env = {"UOT_VEC": vec, "UOT_SEG_H": H}
     prob, st, rep = gpu_run(fr, alpha, n, tau, env)
     ref, rrep = oracle.iterate(fr, alpha, math.inf, tau, tau, n)
     compare(fr, st, ref)
@@ -258,3 +267,38 @@ def test_load_frames_host_matches_device_frames():
     b = Problem(torch.from_numpy(fr2).cuda(), 1.0)
     b.step(25)
     assert torch.equal(a.state()["a"], b.state()["a"])
+
+
+@pytest.mark.parametrize("persist", [0, 1])
+def test_persistent_and_streaming_agree_with_checks(persist):
+    """Both execution paths with in-loop reductions every 7 iterations (grid barrier in
+    the persistent kernel) give the oracle's iterate and last-check reductions."""
+    fr = inputs.gen_random(1, 2, 96, 160, seed=77, kind="sparse")
+    tau = tau_for(96, 160)
+    n = 63
+    prob, st, rep = gpu_run(fr, 1.7, n, tau, env={"UOT_PERSIST": persist}, check_every=7)
+    ref, rrep = oracle.iterate(fr, 1.7, math.inf, tau, tau, n)
+    compare(fr, st, ref)
+    assert rep["iterations"] == n
+    assert rep["objective"] == pytest.approx(rrep[0, 0] + 1.7 * rrep[0, 1], rel=OBJ_RTOL)
+
+
+def test_persistent_solve_stops_on_device():
+    fr = inputs.gen_random(1, 2, 40, 48, seed=78, kind="uniform")
+    tau = tau_for(40, 48)
+    old = os.environ.get("UOT_PERSIST")
+    os.environ["UOT_PERSIST"] = "1"
+    try:
+        prob = Problem(torch.from_numpy(fr).cuda(), 0.9, tau1=tau, tau2=tau)
+    finally:
+        if old is None:
+            os.environ.pop("UOT_PERSIST")
+        else:
+            os.environ["UOT_PERSIST"] = old
+    rep = prob.solve(30000, tol=1e-4, check_every=10)
+    assert rep["converged"] == 1
+    kc = rep["iterations"]
+    assert kc % 10 == 0 and kc < 30000
+    ref, rrep = oracle.iterate(fr, 0.9, math.inf, tau, tau, kc)
+    st = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
+    compare(fr, st, ref)

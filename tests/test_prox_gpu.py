@@ -31,12 +31,16 @@ CASES = [(1, 2, 9, 12, 0.9, 2.0), (2, 2, 33, 64, 1.5, 0.5), (1, 5, 20, 36, 1.2, 
          (1, 3, 40, 7, 2.0, 1.0)]
 
 
-@pytest.mark.parametrize("vec", [1, 4])
+@pytest.mark.parametrize("vec", [1, 2, 4, "persist"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c)))
 @pytest.mark.parametrize("x_from_p", [False, True])
 def test_prox_parity(case, vec, x_from_p, monkeypatch):
     B, T, ny, nx, alpha, rho = case
-    monkeypatch.setenv("UOT_VEC", str(vec))
+    if vec == "persist":
+        monkeypatch.setenv("UOT_PERSIST", "1")
+    else:
+        monkeypatch.setenv("UOT_VEC", str(vec))
+        monkeypatch.setenv("UOT_PERSIST", "0")
     fr = inputs.gen_random(B, T, ny, nx, seed=T * 7 + nx, kind="sparse")
     tau = oracle.default_steps(nx, ny, prox=True, n_frames=T, safety=0.95)[0]
     n = 70
