@@ -41,7 +41,8 @@ def build(force: bool = False) -> str:
 class _Params(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("n_chains", ctypes.c_int32),
                 ("n_frames", ctypes.c_int32), ("alpha", ctypes.c_double), ("rho", ctypes.c_double),
-                ("tau1", ctypes.c_double), ("tau2", ctypes.c_double)]
+                ("tau1", ctypes.c_double), ("tau2", ctypes.c_double), ("p_norm", ctypes.c_int32),
+                ("fix_first", ctypes.c_int32)]
 
 
 def lib():
@@ -115,12 +116,15 @@ def lambda_max(nx: int, ny: int) -> float:
     return float(lib().uot_ref_lambda_max(int(nx), int(ny)))
 
 
-def default_steps(nx: int, ny: int, prox: bool, n_frames: int = 2, safety: float = 0.99):
+def default_steps(nx: int, ny: int, prox: bool, n_frames: int = 2, safety: float = 0.99, fix_first: bool = False):
     """tau1 = tau2 = sqrt(safety/||K||^2) with ||K||^2 from Theorem 1 (L11/L12):
-    lambda_max + 1 (fixed marginals), + 3 (pair prox), + 2 + 2cos(pi/T) (chain prox)."""
+    lambda_max + 1 (fixed marginals), + 3 (pair prox), + 3 + 2cos(pi/T) (chain prox),
+    + 2 (fixed-first-argument pair prox, K = [D, -I, -I])."""
     lam = lambda_max(nx, ny)
     if not prox:
         extra = 1.0
+    elif fix_first and n_frames == 2:
+        extra = 2.0
     else:
         extra = 1.0 + 2.0 + 2.0 * math.cos(math.pi / n_frames) if n_frames > 2 else 3.0
     t = math.sqrt(safety / (lam + extra))
@@ -137,34 +141,39 @@ class State:
     x: np.ndarray | None
 
 
-def zero_state(frames, prox: bool, x_from_p: bool = False) -> State:
-    """Cold start (P:532 'initialized to 0'); x0 = 0, or Pi_+(p) with x_from_p (L8)."""
+def zero_state(frames, prox: bool, x_from_p: bool = False, fix_first: bool = False) -> State:
+    """Cold start (P:532 'initialized to 0'); x0 = 0, or Pi_+(p) with x_from_p (L8);
+    with fix_first the first frame of each chain starts (and stays) at p_0."""
     frames = _f64(frames)
     B, T, ny, nx = frames.shape
     z = lambda: np.zeros((B, T - 1, ny, nx))
     x = None
     if prox:
         x = np.maximum(frames, 0.0).copy() if x_from_p else np.zeros_like(frames)
+        if fix_first:
+            x[:, 0] = frames[:, 0]
     return State(z(), z(), z(), z(), x)
 
 
-def iterate(frames, alpha, rho, tau1, tau2, n_iters, state: State | None = None):
+def iterate(frames, alpha, rho, tau1, tau2, n_iters, state: State | None = None, p_norm: int = 1,
+            fix_first: bool = False):
     """Run n_iters iterations of Algorithm 1 on frames [B][T][ny][nx].
 
     Returns (state, rep) where rep[B*(T-1), 8] are the reductions of the last
-    iteration (fields REP_FIELDS).  rho = inf -> fixed marginals.
+    iteration (fields REP_FIELDS).  rho = inf -> fixed marginals; alpha = inf ->
+    balanced Beckmann; p_norm 2 -> alpha ||r||_2^2; fix_first -> eq:Prox_UOT_specialcase.
     """
     frames = _f64(frames)
     if frames.ndim == 2:
         raise ValueError("frames must be [B][T][ny][nx]")
     B, T, ny, nx = frames.shape
     prox = math.isfinite(rho)
-    st = state if state is not None else zero_state(frames, prox)
+    st = state if state is not None else zero_state(frames, prox, fix_first=fix_first)
     st = State(_f64(st.mx).copy(), _f64(st.my).copy(), _f64(st.r).copy(), _f64(st.a).copy(),
                None if st.x is None else _f64(st.x).copy())
     if prox and st.x is None:
         st.x = np.zeros_like(frames)
-    prm = _Params(nx, ny, B, T, float(alpha), float(rho), float(tau1), float(tau2))
+    prm = _Params(nx, ny, B, T, float(alpha), float(rho), float(tau1), float(tau2), int(p_norm), int(fix_first))
     rep = np.zeros((B * (T - 1), 8))
     rc = lib().uot_ref_iterate(ctypes.byref(prm), _p(frames), _p(st.mx), _p(st.my), _p(st.r),
                                _p(st.a), _p(st.x) if prox else None, int(n_iters), _p(rep))
@@ -175,11 +184,11 @@ def iterate(frames, alpha, rho, tau1, tau2, n_iters, state: State | None = None)
     return st, rep
 
 
-def certificate(frames, state: State, alpha, rho=math.inf):
+def certificate(frames, state: State, alpha, rho=math.inf, p_norm: int = 1):
     """Objective and weak-duality bounds L <= V <= U per pair (fields CERT_FIELDS)."""
     frames = _f64(frames)
     B, T, ny, nx = frames.shape
-    prm = _Params(nx, ny, B, T, float(alpha), float(rho), 0.0, 0.0)
+    prm = _Params(nx, ny, B, T, float(alpha), float(rho), 0.0, 0.0, int(p_norm), 0)
     cert = np.zeros((B * (T - 1), 8))
     prox = math.isfinite(rho)
     lib().uot_ref_certificate(ctypes.byref(prm), _p(frames), _p(_f64(state.mx)), _p(_f64(state.my)),
@@ -188,10 +197,11 @@ def certificate(frames, state: State, alpha, rho=math.inf):
     return cert
 
 
-def evaluate(p, q, alpha, iters=20000, tol=1e-9, tau=None, chunk=2000):
+def evaluate(p, q, alpha, iters=20000, tol=1e-9, tau=None, chunk=2000, p_norm: int = 1):
     """V_alpha(p, q) of eq:Unbal_OT_beckman by Algorithm 1 without the
     x-block, run until the certified gap (U-L)/max(U,1e-12) <= tol or iters.
-    Returns (value_upper, value_lower, objective)."""
+    Returns (value_upper, value_lower, objective).  alpha = inf: balanced (U is
+    then the objective once div M = f holds to rounding, see certificate)."""
     p, q = _f64(p), _f64(q)
     if p.ndim == 1:
         p, q = p[None, :], q[None, :]
@@ -203,10 +213,12 @@ def evaluate(p, q, alpha, iters=20000, tol=1e-9, tau=None, chunk=2000):
     cert = None
     while done < iters:
         n = min(chunk, iters - done)
-        st, _ = iterate(frames, alpha, math.inf, t1, t2, n, st)
+        st, _ = iterate(frames, alpha, math.inf, t1, t2, n, st, p_norm=p_norm)
         done += n
-        cert = certificate(frames, st, alpha)
+        cert = certificate(frames, st, alpha, p_norm=p_norm)
         U, L = cert[0, 2], cert[0, 6]
+        if not math.isfinite(alpha):     # balanced: U needs exact feasibility; use the objective
+            U = cert[0, 7]
         if U - L <= tol * max(abs(U), 1e-12):
             break
     return cert[0, 2], cert[0, 6], cert[0, 7]

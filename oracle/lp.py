@@ -107,3 +107,47 @@ def laplacian_matrix(nx, ny):
         D[j * nx + i, len(nmx) + c] += 1.0
         D[(j + 1) * nx + i, len(nmx) + c] -= 1.0
     return D @ D.T, D
+
+
+def uot_1d_p2_enum(p, q, alpha):
+    """Exact optimum of the p = 2 variant (alpha ||r||_2^2) on a 1 x n grid,
+    n <= 7, by enumerating sign patterns of M: eliminating r = div M - f gives
+        F(M) = sum_i |M_i| + alpha sum_i (M_i - M_{i-1} - f_i)^2,
+    convex piecewise quadratic; on the piece with signs s (s_i = 0 -> M_i = 0)
+    F is a quadratic whose stationary point solves a linear system; the global
+    minimum is the best sign-consistent stationary point over all 3^(n-1) pieces."""
+    p, q = np.asarray(p, float), np.asarray(q, float)
+    n = p.size
+    f = q - p
+    m = n - 1
+    if m == 0:
+        return alpha * f[0] ** 2
+    D = np.zeros((n, m))                 # (D M)_i = M_i - M_{i-1}
+    for i in range(n):
+        if i < m:
+            D[i, i] += 1.0
+        if i - 1 >= 0:
+            D[i, i - 1] -= 1.0
+
+    def F(M):
+        return np.abs(M).sum() + alpha * ((D @ M - f) ** 2).sum()
+
+    best = F(np.zeros(m))
+    for signs in itertools.product((-1, 0, 1), repeat=m):
+        s = np.array(signs, float)
+        free = np.nonzero(s)[0]
+        if free.size == 0:
+            continue
+        Df = D[:, free]
+        # grad: s_free + 2 alpha Df^T (Df M - f) = 0
+        H = 2 * alpha * Df.T @ Df
+        g = 2 * alpha * Df.T @ f - s[free]
+        try:
+            Mf = np.linalg.solve(H, g)
+        except np.linalg.LinAlgError:
+            continue
+        if np.all(s[free] * Mf >= -1e-12):
+            M = np.zeros(m)
+            M[free] = Mf
+            best = min(best, F(M))
+    return float(best)

@@ -35,9 +35,13 @@ typedef struct {
     int32_t nx, ny;       /* grid */
     int32_t n_chains;     /* B independent sequences */
     int32_t n_frames;     /* T >= 2 frames per chain; pairs P = T-1 */
-    double alpha;         /* paper mu > 0 */
+    double alpha;         /* paper mu > 0; +INFINITY = balanced Beckmann (eq:OT_beckman,
+                             r dropped: footnote P:609) */
     double rho;           /* weight of (rho/2)||x-p||^2 as printed in Alg.1 line 4; INFINITY = fixed */
     double tau1, tau2;    /* primal / dual steps */
+    int32_t p_norm;       /* 1 or 2 (mu ||r||_2^2, the "averaging update" of P:297, L14) */
+    int32_t fix_first;    /* prox mode: frame 0 of each chain held at p_0 (eq:Prox_UOT_specialcase,
+                             P:337-349: "A := I, K := div(M) - s + x - r") */
 } uot_ref_params;
 
 #define REP_STRIDE 8
@@ -126,10 +130,10 @@ double uot_ref_lambda_max(int nx, int ny) {
  * rep[g*8 + .] (pair g = b*P + t) receives the reductions of the LAST executed
  * iteration:
  *   0: sum_k ||m_k^{k+1}||_2                (transport, ||M||_{2,1} P:146-151)
- *   1: sum_k |r_k^{k+1}|                    (growth, ||r||_1; objective adds alpha*)
+ *   1: sum_k |r_k^{k+1}|^p                  (growth, ||r||_p^p; objective adds alpha*)
  *   2: sum_k (K^{k+1}_k)^2                  (primal residual^2, L13)
  *   3: sum ||z^{k+1}-z^k||^2, z=(M,r[,x])   (dual residual^2 * tau1^2, L13)
- *   4: sum_k |div(M^{k+1}) - (x_{t+1}-x_t)| (repaired upper-bound growth term)
+ *   4: sum_k |div(M^{k+1}) - (x_{t+1}-x_t)|^p (repaired upper-bound growth term)
  *   5: sum_k (x^{k+1}-p)^2                  (prox term / (rho/2); 0 in fixed mode)
  *   6: sum_k f_k^2, f = x_{t+1}-x_t at k+1  (for relative stopping)
  *   7: number of pixels N
@@ -190,9 +194,16 @@ int uot_ref_iterate(const uot_ref_params* prm, const double* frames,
                 gy[o + k] = MYv(my + o, nx, ny, i, j) - tau1 * gy[o + k];  /* q_y */
             }
             uot_ref_shrink_l2((int64_t)N, gx + o, gy + o, tau1, mxn + o, myn + o);
-            /* Alg.1 line 5: r <- shrink^{l1}_{mu tau1}(r^k + tau1 a^k) */
+            /* Alg.1 line 5: r <- shrink^{l1}_{mu tau1}(r^k + tau1 a^k);
+             * p = 2: r <- argmin mu r^2 - a r + (r - r^k)^2/(2 tau1) = (r^k + tau1 a^k)/(1 + 2 mu tau1)
+             * ("averaging update"; derived); balanced (mu = inf): r = 0 */
             for (size_t k = 0; k < N; ++k) gx[o + k] = r[o + k] + tau1 * a[o + k];
-            uot_ref_shrink_l1((int64_t)N, gx + o, alpha * tau1, rn + o);
+            if (!isfinite(alpha))
+                for (size_t k = 0; k < N; ++k) rn[o + k] = 0.0;
+            else if (prm->p_norm == 2)
+                for (size_t k = 0; k < N; ++k) rn[o + k] = gx[o + k] / (1.0 + 2.0 * alpha * tau1);
+            else
+                uot_ref_shrink_l1((int64_t)N, gx + o, alpha * tau1, rn + o);
         }
         /* Alg.1 line 4 (prox mode): x <- Pi_+((rho tau1 p + x^k - tau1 A^T a^k)/(1+rho tau1)) */
         if (prox) {
@@ -204,6 +215,10 @@ int uot_ref_iterate(const uot_ref_params* prm, const double* frames,
                 double* xo = XV(xn, b, s);
                 const double* a_s = (s < P) ? a + ((size_t)b * P + s) * N : NULL;       /* a_s, s <= P-1 */
                 const double* a_sm = (s >= 1) ? a + ((size_t)b * P + s - 1) * N : NULL; /* a_{s-1} */
+                if (s == 0 && prm->fix_first) {          /* constant first argument s */
+                    for (size_t k = 0; k < N; ++k) xo[k] = p[k];
+                    continue;
+                }
                 for (size_t k = 0; k < N; ++k) {
                     double ATa = (a_s ? a_s[k] : 0.0) - (a_sm ? a_sm[k] : 0.0);
                     double v = (rho * tau1 * p[k] + xs[k] - tau1 * ATa) / (1.0 + rho * tau1);
@@ -233,11 +248,12 @@ int uot_ref_iterate(const uot_ref_params* prm, const double* frames,
                     double dmy = myn[o + k] - MYv(my + o, nx, ny, i, j);
                     double dr = rn[o + k] - r[o + k];
                     double f = x1[k] - x0[k];
+                    const double u = dv[o + k] - f;
                     s0 += sqrt(mxn[o + k] * mxn[o + k] + myn[o + k] * myn[o + k]);
-                    s1 += fabs(rn[o + k]);
+                    s1 += (prm->p_norm == 2) ? rn[o + k] * rn[o + k] : fabs(rn[o + k]);
                     s2 += Knew[o + k] * Knew[o + k];
                     s3 += dmx * dmx + dmy * dmy + dr * dr;
-                    s4 += fabs(dv[o + k] - f);
+                    s4 += (prm->p_norm == 2) ? u * u : fabs(u);
                     s6 += f * f;
                 }
                 if (prox) {
@@ -283,9 +299,13 @@ int uot_ref_iterate(const uot_ref_params* prm, const double* frames,
  *   max -<a, f>  s.t. ||(div^* a)_k||_2 <= 1, |a_k| <= alpha,
  * so for ANY a, with c = max(1, max_k ||(div^*a)_k||, max_k |a_k|/alpha),
  *   L = -<a, f>/c  <=  V_alpha(x_t, x_{t+1})  <=  U = ||M||_{2,1} + alpha ||div M - f||_1.
+ * p = 2 (alpha ||r||_2^2): dual max -<a,f> - ||a||^2/(4 alpha) s.t. ||div^*a|| <= 1:
+ *   c = max(1, max||div^*a||), L = -<a,f>/c - ||a||^2/(4 alpha c^2), U = ||M|| + alpha||div M - f||^2.
+ * balanced (alpha = inf, eq:OT_beckman): c = max(1, max||div^*a||), L = -<a,f>/c,
+ *   U = ||M|| if div M = f exactly, else +inf.
  * f = x_{t+1} - x_t uses x (prox mode) or the frames (fixed mode).
- * cert[g*8 + .]: 0 transport, 1 sum|r|, 2 U, 3 <a,f>, 4 max||div^*a||,
- * 5 max|a|, 6 L, 7 objective ||M||_{2,1} + alpha||r||_1. */
+ * cert[g*8 + .]: 0 transport, 1 sum|r|^p, 2 U, 3 <a,f>, 4 max||div^*a||,
+ * 5 max|a|, 6 L, 7 objective ||M||_{2,1} + alpha||r||_p^p. */
 int uot_ref_certificate(const uot_ref_params* prm, const double* frames,
                         const double* mx, const double* my, const double* r,
                         const double* a, const double* x, double* cert) {
@@ -305,25 +325,37 @@ int uot_ref_certificate(const uot_ref_params* prm, const double* frames,
         const double* x1 = base + ((size_t)b * T + t + 1) * N;
         uot_ref_div(nx, ny, mx + o, my + o, dv);
         uot_ref_div_adj(nx, ny, a + o, gx, gy);
-        double tr = 0, gr = 0, ub = 0, af = 0, mg = 0, ma = 0;
+        const int p2 = prm->p_norm == 2;
+        double tr = 0, gr = 0, ub = 0, af = 0, mg = 0, ma = 0, a2 = 0;
         for (size_t k = 0; k < N; ++k) {
             int i = (int)(k % nx), j = (int)(k / nx);
             double mxk = MXv(mx + o, nx, ny, i, j), myk = MYv(my + o, nx, ny, i, j);
             double f = x1[k] - x0[k];
+            double u = dv[k] - f;
             tr += sqrt(mxk * mxk + myk * myk);
-            gr += fabs(r[o + k]);
-            ub += fabs(dv[k] - f);
+            gr += p2 ? r[o + k] * r[o + k] : fabs(r[o + k]);
+            ub += p2 ? u * u : fabs(u);
             af += a[o + k] * f;
+            a2 += a[o + k] * a[o + k];
             double gn = sqrt(gx[k] * gx[k] + gy[k] * gy[k]);
             if (gn > mg) mg = gn;
             if (fabs(a[o + k]) > ma) ma = fabs(a[o + k]);
         }
         double c = 1.0;
         if (mg > c) c = mg;
-        if (ma / alpha > c) c = ma / alpha;
+        const int bal = !isfinite(alpha);
+        if (!bal && !p2 && ma / alpha > c) c = ma / alpha;
         double* C = cert + (size_t)g * REP_STRIDE;
-        C[0] = tr; C[1] = gr; C[2] = tr + alpha * ub; C[3] = af; C[4] = mg; C[5] = ma;
-        C[6] = -af / c; C[7] = tr + alpha * gr;
+        C[0] = tr; C[1] = gr; C[3] = af; C[4] = mg; C[5] = ma;
+        if (bal) {
+            C[2] = (ub == 0.0) ? tr : INFINITY;
+            C[6] = -af / c;
+            C[7] = tr;
+        } else {
+            C[2] = tr + alpha * ub;
+            C[6] = p2 ? -af / c - a2 / (4.0 * alpha * c * c) : -af / c;
+            C[7] = tr + alpha * gr;
+        }
     }
     free(dv); free(gx); free(gy);
     return 0;

@@ -11,6 +11,8 @@ muts=(
 's/(MYv(my, nx, ny, i, j) - MYv(my, nx, ny, i, j - 1));/(MYv(my, nx, ny, i, j) - MYv(my, nx, ny, i - 1, j));/'
 's/double s = (nrm > sigma) ? (nrm - sigma) \/ nrm : 0.0;/double s = (nrm > sigma) ? (nrm - sigma) : 0.0;/'
 's/uot_ref_shrink_l1((int64_t)N, gx + o, alpha \* tau1, rn + o);/uot_ref_shrink_l1((int64_t)N, gx + o, alpha, rn + o);/'
+'s/rn\[o + k\] = gx\[o + k\] \/ (1.0 + 2.0 \* alpha \* tau1);/rn[o + k] = gx[o + k] \/ (1.0 + alpha * tau1);/'
+'s/if (s == 0 \&\& prm->fix_first) {/if (s == 1 \&\& prm->fix_first) {/'
 )
 for m in "${muts[@]}"; do
   rm -rf w; mkdir w; cp -r /root/repo/oracle /root/repo/tests /root/repo/paper_1909_00149_b200 w/; rm -f w/oracle/liboracle.so

@@ -406,3 +406,80 @@ def test_oracle_deterministic_and_nonfinite():
     fr[0, 0, 2, 2] = np.nan
     with pytest.raises(FloatingPointError):
         oracle.iterate(fr, 0.9, math.inf, 0.3, 0.3, 3)
+
+
+# ----------------------------------------------------------------------------- P18-P20 NEXT(2) variants
+def test_P18_balanced_beckmann():
+    """P18: alpha = inf is balanced Beckmann eq:OT_beckman (r dropped, footnote P:609):
+    1-D value = sum |cumsum(q - p)|, two deltas cost d, and the
+    unbalanced value is <= balanced for every alpha."""
+    g = np.random.default_rng(30)
+    for trial in range(4):
+        p = g.random(12); q = g.random(12); q *= p.sum() / q.sum()
+        w = lp.w1_1d(p, q)
+        U, L, obj = oracle.evaluate(p, q, math.inf, iters=300000, tol=1e-9)
+        assert L - 1e-8 <= w and obj == pytest.approx(w, rel=1e-6)
+        assert oracle.evaluate(p, q, 0.7, iters=100000, tol=1e-8)[0] <= w + 1e-7
+    fr = np.zeros((1, 2, 8, 8)); fr[0, 0, 2, 1] = 1.0; fr[0, 1, 2, 5] = 1.0
+    U, L, obj = oracle.evaluate(fr[0, 0], fr[0, 1], math.inf, iters=300000, tol=1e-9)
+    assert obj == pytest.approx(4.0, rel=1e-3) and 4.0 * (1 - 1e-3) <= L <= 4.0 + 1e-9
+    st, _ = oracle.iterate(fr, math.inf, math.inf, 0.3, 0.3, 200)
+    assert np.all(st.r == 0)
+
+
+@pytest.mark.parametrize("alpha", [0.2, 1.0, 5.0])
+def test_P19_p2_residual_bruteforce_and_kkt(alpha):
+    """P19: p = 2 ("averaging update"; r = (r + tau1 a)/(1 + 2 alpha tau1))
+    vs exact sign-pattern enumeration of the 1-D problem; at the fixed point the
+    r-stationarity a = 2 alpha r holds (Lagrangian P:235-242)."""
+    g = np.random.default_rng(int(alpha * 10))
+    for trial in range(4):
+        p, q = g.random(5), g.random(5)
+        v = lp.uot_1d_p2_enum(p, q, alpha)
+        U, L, obj = oracle.evaluate(p, q, alpha, iters=300000, tol=1e-10, p_norm=2)
+        assert L - 1e-8 <= v <= U + 1e-8
+        assert U == pytest.approx(v, rel=1e-6, abs=1e-9)
+    fr = g.random((1, 2, 6, 7))
+    st, rep = oracle.iterate(fr, alpha, math.inf, 0.3, 0.3, 60000, p_norm=2)
+    np.testing.assert_allclose(st.a, 2 * alpha * st.r, atol=1e-8)
+    assert rep[0, 2] < 1e-18
+
+
+def test_P20_fixed_first_argument_prox():
+    """P20: eq:Prox_UOT_specialcase: frame 0 fixed at s, x = frame 1 with
+    A := I.  Fixed point satisfies x = Pi_+(p + a/rho), K = 0, |a| <= alpha,
+    ||div* a|| <= 1; s = p >= 0 gives x = p; a far-away delta prior barely
+    moves a strongly attached x."""
+    g = np.random.default_rng(31)
+    fr = g.random((2, 2, 7, 6)) * (g.random((2, 2, 7, 6)) < 0.5)
+    alpha, rho = 0.8, 1.5
+    t = oracle.default_steps(6, 7, prox=True, fix_first=True, safety=0.95)[0]
+    st, _ = oracle.iterate(fr, alpha, rho, t, t, 60000, fix_first=True)
+    np.testing.assert_array_equal(st.x[:, 0], fr[:, 0])
+    np.testing.assert_allclose(st.x[:, 1], np.maximum(fr[:, 1] + st.a[:, 0] / rho, 0), atol=1e-7)
+    for b in range(2):
+        K = oracle.div(st.mx[b, 0], st.my[b, 0]) - st.r[b, 0] - st.x[b, 1] + st.x[b, 0]
+        assert np.abs(K).max() < 1e-8
+        gx, gy = oracle.div_adj(st.a[b, 0])
+        assert np.hypot(gx, gy).max() <= 1 + 1e-8 and np.abs(st.a).max() <= alpha + 1e-8
+    p = g.random((6, 6))
+    st, _ = oracle.iterate(np.stack([p, p])[None], 1.0, 2.0, t, t, 5000, fix_first=True)
+    np.testing.assert_allclose(st.x[0, 1], p, atol=1e-9)
+    fr = np.zeros((1, 2, 8, 8)); fr[0, 0, 1, 1] = 1.0; fr[0, 1, 1, 4] = 1.0
+    t = oracle.default_steps(8, 8, prox=True, fix_first=True, safety=0.95)[0]
+    st, _ = oracle.iterate(fr, 10.0, 100.0, t, t, 60000, fix_first=True)
+    assert np.abs(st.x[0, 1] - fr[0, 1]).max() < 0.035          # |x - p| <= |a|/rho, |a| <= 3
+    c = oracle.certificate(np.stack([fr[0, 0], st.x[0, 1]])[None], st, 10.0)
+    assert c[0, 0] == pytest.approx(3.0, rel=3e-2)                    # transport ~ 3 (S:158)
+    # prox optimality vs the candidate x = p (value V(s, p) = 3 by P9): F(x*) <= F(p)
+    assert c[0, 7] + 0.5 * 100.0 * ((st.x[0, 1] - fr[0, 1]) ** 2).sum() <= 3.0 + 1e-7
+
+
+def test_P5d_fixed_first_step_norm():
+    """P5d: ||K||^2 = lambda_max + 2 for K = [D, -I, -I] (fixed-first pair prox)."""
+    nx, ny = 5, 3
+    _, D = lp.laplacian_matrix(nx, ny)
+    I = np.eye(nx * ny)
+    K = np.hstack([D, -I, -I])
+    t1, t2 = oracle.default_steps(nx, ny, prox=True, fix_first=True, safety=1.0)
+    assert 1.0 / (t1 * t2) == pytest.approx(np.linalg.norm(K, 2) ** 2, rel=1e-10)
