@@ -53,6 +53,10 @@ extern "C" {
 
 /* uot_params.flags */
 #define UOT_FORCE_STEPS     1u /* accept tau1*tau2 >= 1/||K||^2 (Theorem 1 not satisfied) */
+#define UOT_FIX_FIRST_FRAME 2u /* prox mode: frame 0 of each chain is a constant argument s
+                                  (eq:Prox_UOT_specialcase); x_0 stays = frames[b][0] */
+#define UOT_RESIDUAL_L2     4u /* p = 2: growth penalty alpha ||r||_2^2, r-update
+                                  r <- (r + tau1 a)/(1 + 2 alpha tau1) ("averaging update") */
 /* uot_reset flags */
 #define UOT_RESET_X_FROM_P  1u /* prox mode: x^0 = max(p, 0) instead of 0 (L8)   */
 
@@ -63,12 +67,13 @@ typedef struct {
     int32_t  n_chains;     /* B >= 1 independent chains (batched pairs: T = 2)                 */
     int32_t  n_frames;     /* T >= 2 frames per chain held by this context (a shard's frames
                               include the shared boundary frame)        */
-    double   alpha;        /* paper mu > 0; p = 1                               */
+    double   alpha;        /* paper mu > 0; p = 1 (or 2 with UOT_RESIDUAL_L2);
+                              +INFINITY = balanced Beckmann eq:OT_beckman (r dropped, footnote P:609) */
     double   rho;          /* weight of (rho/2)||x - p||^2 as printed in Alg.1 line 4 (L2);
                               +INFINITY = fixed marginals (x == frames, evaluation of eq:Unbal_OT_beckman) */
     double   tau1, tau2;   /* primal / dual steps > 0; 0 = Theorem-1 default (uot_default_steps,
                               safety 0.99)                                                      */
-    uint32_t flags;        /* UOT_FORCE_STEPS                                                   */
+    uint32_t flags;        /* UOT_FORCE_STEPS | UOT_FIX_FIRST_FRAME | UOT_RESIDUAL_L2          */
 } uot_params;
 
 /* Device buffers.  ALL are CALLER-OWNED device pointers (e.g. torch tensors),
@@ -93,11 +98,12 @@ typedef struct {
 typedef struct {
     double objective;      /* sum ||M||_{2,1} + alpha ||r||_1 (+ (rho/2)||x - p||^2 in prox mode) */
     double transport;      /* sum ||M||_{2,1}                                      */
-    double growth;         /* sum alpha ||r||_1                                                  */
+    double growth;         /* sum alpha ||r||_p^p (0 when balanced)                              */
     double prox_term;      /* (rho/2) sum ||x - p||^2 (0 in fixed mode)                         */
     double primal_res;     /* ||K^{k+1}||_2, constraint violation (L13)                         */
     double dual_res;       /* ||z^{k+1} - z^k||_2 / tau1, z = (M, r[, x]) (L13)                 */
-    double upper_bound;    /* sum ||M||_{2,1} + alpha ||div M - f||_1 >= V (feasible repair)   */
+    double upper_bound;    /* sum ||M||_{2,1} + alpha ||div M - f||_p^p >= V (feasible repair;
+                              balanced: ||M|| if div M = f exactly, else +inf)                 */
     double lower_bound;    /* weak-duality bound <= V (uot_objective only, else NaN)           */
     double f_norm;         /* ||x_{t+1} - x_t||_2 over all pairs (stopping scale)               */
     int64_t iterations;    /* executions of Alg.1 lines 3-7 since the last uot_reset (L9)      */
@@ -110,7 +116,8 @@ size_t uot_scratch_doubles(const uot_params* params);
 
 /* Theorem-1 steps (L11/L12): tau1 = tau2 = sqrt(safety / ||K||^2),
  * ||K||^2 = lambda_max(div div^*) + 1 (fixed), + 3 (pair prox, the paper's
- * bound), + 3 + 2cos(pi/T) (chain prox of T frames); lambda_max =
+ * bound), + 3 + 2cos(pi/T) (chain prox of T frames), + 2 (pair prox with
+ * UOT_FIX_FIRST_FRAME: K = [D, -I, -I]); lambda_max =
  * g(nx) + g(ny), g(n) = 2 + 2cos(pi/n) (n >= 2), g(1) = 0.  0 < safety < 1.
  * Host-only, no device needed.  Returns UOT_OK or UOT_E_INVALID. */
 int uot_default_steps(const uot_params* params, double safety, double* tau1, double* tau2);
@@ -166,8 +173,9 @@ int uot_prox_step(uot_ctx* ctx, int32_t n_iters, uot_report* out);
 int uot_solve(uot_ctx* ctx, int32_t max_iters, double tol, int32_t check_every, uot_report* out);
 
 /* Objective and weak-duality certificate of the CURRENT state, per pair
- * (DESIGN.md "Certificate"):  per_pair[g*8 + .] = {transport, sum|r|, U,
- * <a,f>, max ||div^* a||, max |a|, L, objective}, L <= V_alpha <= U.
+ * (DESIGN.md "Certificate"):  per_pair[g*8 + .] = {transport, sum|r|^p, U,
+ * <a,f>, max ||div^* a||, max |a|, L, objective}, L <= V_alpha <= U
+ * (p = 2: L = -<a,f>/c - ||a||^2/(4 alpha c^2), c = max(1, max||div^*a||)).
  * per_pair may be NULL; out may be NULL.  Synchronises the stream. */
 int uot_objective(uot_ctx* ctx, double* per_pair, uot_report* out);
 

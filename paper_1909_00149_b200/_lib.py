@@ -18,6 +18,8 @@ UOT_E_NOT_CONVERGED = 3
 UOT_E_NONFINITE = 4
 UOT_E_CUDA = 5
 UOT_FORCE_STEPS = 1
+UOT_FIX_FIRST_FRAME = 2
+UOT_RESIDUAL_L2 = 4
 UOT_RESET_X_FROM_P = 1
 UOT_PART_ALL, UOT_PART_INTERIOR, UOT_PART_BOUNDARY = 0, 1, 2
 

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_objective(const ObjArgs O) {
     const float* my = O.my + po;
     const float* r = O.r + po;
     const float* a = O.a + po;
-    double tr = 0, gr = 0, ub = 0, af = 0, mg = 0, ma = 0, px = 0;
+    double tr = 0, gr = 0, ub = 0, af = 0, mg = 0, ma = 0, px = 0, a2 = 0;
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < O.N;
          k += (long long)O.bpp * blockDim.x) {
         const int i = (int)(k % nx), j = (int)(k / nx);
@@ -104,10 +104,12 @@ __global__ void __launch_bounds__(256) k_objective(const ObjArgs O) {
         const double myu = (j >= 1) ? my[k - nx] : 0.0;
         const double dv = (mxk - mxl) + (myk - myu);             // div M
         const double f = (double)(x1[k] - x0[k]);
+        const double u = dv - f, rk = (double)r[k];
         tr += sqrt(mxk * mxk + myk * myk);
-        gr += fabs((double)r[k]);
-        ub += fabs(dv - f);
+        gr += O.p2 ? rk * rk : fabs(rk);
+        ub += O.p2 ? u * u : fabs(u);
         af += (double)a[k] * f;
+        a2 += (double)a[k] * (double)a[k];
         const double gx = (i < nx - 1) ? (double)a[k] - (double)a[k + 1] : 0.0;   // div^* a (L4)
         const double gy = (j < ny - 1) ? (double)a[k] - (double)a[k + nx] : 0.0;
         mg = fmax(mg, sqrt(gx * gx + gy * gy));
@@ -122,10 +124,10 @@ __global__ void __launch_bounds__(256) k_objective(const ObjArgs O) {
         }
     }
     tr = block_sum(tr, sh); gr = block_sum(gr, sh); ub = block_sum(ub, sh); af = block_sum(af, sh);
-    mg = block_max(mg, sh); ma = block_max(ma, sh); px = block_sum(px, sh);
+    mg = block_max(mg, sh); ma = block_max(ma, sh); px = block_sum(px, sh); a2 = block_sum(a2, sh);
     if (threadIdx.x == 0) {
         double* P = O.partials + ((size_t)g * O.bpp + blockIdx.x) * kRec;
-        P[0] = tr; P[1] = gr; P[2] = ub; P[3] = af; P[4] = mg; P[5] = ma; P[6] = px; P[7] = 0.0;
+        P[0] = tr; P[1] = gr; P[2] = ub; P[3] = af; P[4] = mg; P[5] = ma; P[6] = px; P[7] = a2;
     }
 }
 
@@ -199,9 +201,13 @@ __global__ void __launch_bounds__(256) k_pair_reduce(const ReduceArgs R) {
 }
 
 // prox cold start (L8): x^0 = 0, or max(p, 0) with UOT_RESET_X_FROM_P
-__global__ void __launch_bounds__(256) k_init_x(const float* p, float* x, long long n, int from_p) {
-    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
-        x[k] = from_p ? fmaxf(p[k], 0.f) : 0.f;
+// with UOT_FIX_FIRST_FRAME, frame 0 of each chain is the constant argument s = p_0
+__global__ void __launch_bounds__(256) k_init_x(const float* p, float* x, long long n, int from_p,
+                                                int fix_first, long long frame_len, int T) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const bool first = fix_first && ((k / frame_len) % T == 0);
+        x[k] = first ? p[k] : (from_p ? fmaxf(p[k], 0.f) : 0.f);
+    }
 }
 
 __global__ void k_init_glob(double* glob, int* stop, int* counter, int reset_all) {
@@ -246,6 +252,9 @@ struct uot_ctx {
     int* pflags;        // [kMaxPersistCtas] + barrier[2]
     struct { bool ok; int TW, TH, tx, ty, ctas, threads; size_t smem; } pg;
     int64_t persist_launches;
+    int r_mode;          // 0 l1, 1 l2 (p = 2), 2 balanced
+    float r_scale;
+    int fix_first;
     bool timing;
     bool stop_armed;
     std::vector<cudaEvent_t> ev;     // event pool, pairs (start, stop)
@@ -322,10 +331,11 @@ static size_t persist_scratch_doubles() {
     return ((size_t)kMaxPersistCtas * 2 * kMaxTileEdge) / 2 + (kMaxPersistCtas + 8) / 2 + 8;
 }
 
-static double chain_norm2(int nx, int ny, int T, bool prox) {
+static double chain_norm2(int nx, int ny, int T, bool prox, bool fix_first = false) {
     const double pi = 3.14159265358979323846;
     const double lam = (nx >= 2 ? 2.0 + 2.0 * cos(pi / nx) : 0.0) + (ny >= 2 ? 2.0 + 2.0 * cos(pi / ny) : 0.0);
     if (!prox) return lam + 1.0;                        // K = [D, -I]
+    if (fix_first && T == 2) return lam + 2.0;          // K = [D, -I, -I] (eq:Prox_UOT_specialcase)
     return lam + 1.0 + 2.0 + 2.0 * cos(pi / T);         // K = [D, -I, A], A path incidence (L12)
 }
 
@@ -409,7 +419,7 @@ int uot_default_steps(const uot_params* p, double safety, double* tau1, double* 
     if (!(safety > 0.0 && safety < 1.0)) return fail(nullptr, UOT_E_INVALID, "safety must be in (0,1)");
     if (p->nx < 1 || p->ny < 1 || p->n_frames < 2) return fail(nullptr, UOT_E_INVALID, "bad grid");
     const bool prox = isfinite(p->rho);
-    const double t = sqrt(safety / chain_norm2(p->nx, p->ny, p->n_frames, prox));
+    const double t = sqrt(safety / chain_norm2(p->nx, p->ny, p->n_frames, prox, (p->flags & UOT_FIX_FIRST_FRAME) != 0));
     *tau1 = t;
     *tau2 = t;
     return UOT_OK;
@@ -424,7 +434,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     uot_params p = *prm;
     if (p.nx < 1 || p.ny < 1) return fail(nullptr, UOT_E_INVALID, "nx, ny must be >= 1");
     if (p.n_chains < 1 || p.n_frames < 2) return fail(nullptr, UOT_E_INVALID, "need n_chains >= 1, n_frames >= 2");
-    if (!(p.alpha > 0.0) || !isfinite(p.alpha)) return fail(nullptr, UOT_E_INVALID, "alpha must be finite and > 0");
+    if (!(p.alpha > 0.0)) return fail(nullptr, UOT_E_INVALID, "alpha must be > 0 (+inf = balanced)");
     if (!(p.rho > 0.0)) return fail(nullptr, UOT_E_INVALID, "rho must be > 0 (+inf = fixed marginals)");
     if (!(p.tau1 >= 0.0) || !(p.tau2 >= 0.0) || !isfinite(p.tau1) || !isfinite(p.tau2))
         return fail(nullptr, UOT_E_INVALID, "tau1, tau2 must be finite and >= 0");
@@ -435,7 +445,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
         if (p.tau1 == 0.0) p.tau1 = t1;
         if (p.tau2 == 0.0) p.tau2 = t2;
     }
-    const double bound = 1.0 / chain_norm2(p.nx, p.ny, p.n_frames, prox);
+    const double bound = 1.0 / chain_norm2(p.nx, p.ny, p.n_frames, prox, (p.flags & UOT_FIX_FIRST_FRAME) != 0);
     if (!(p.flags & UOT_FORCE_STEPS) && !(p.tau1 * p.tau2 < bound))
         return fail(nullptr, UOT_E_INVALID, "tau1*tau2 = %g violates Theorem 1 bound %g (set UOT_FORCE_STEPS)",
                     p.tau1 * p.tau2, bound);
@@ -468,6 +478,9 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->geo = choose_geometry(p.nx, p.ny, c->G, vec4_ok);
     c->bpp = blocks_per_pair(c->N);
     c->tau1 = p.tau1; c->tau2 = p.tau2;
+    c->r_mode = !isfinite(p.alpha) ? 2 : ((p.flags & UOT_RESIDUAL_L2) ? 1 : 0);
+    c->r_scale = c->r_mode == 1 ? (float)(1.0 / (1.0 + 2.0 * p.alpha * p.tau1)) : 1.f;
+    c->fix_first = (prox && (p.flags & UOT_FIX_FIRST_FRAME)) ? 1 : 0;
     c->tau1f = (float)p.tau1; c->tau2f = (float)p.tau2;
     c->iter = 0;
     c->launches = 0;
@@ -525,7 +538,8 @@ int uot_reset(uot_ctx* c, uint32_t flags) {
     if (rc) return rc;
     if (c->prox) {
         const long long n = (long long)c->B * c->T * c->N;
-        k_init_x<<<4 * kSMs, 256, 0, c->s>>>(c->b.frames, c->b.x[0], n, (flags & UOT_RESET_X_FROM_P) ? 1 : 0);
+        k_init_x<<<4 * kSMs, 256, 0, c->s>>>(c->b.frames, c->b.x[0], n, (flags & UOT_RESET_X_FROM_P) ? 1 : 0,
+                                             (c->p.flags & UOT_FIX_FIRST_FRAME) ? 1 : 0, c->N, c->T);
         rc = check_launch(c, "k_init_x");
         if (rc) return rc;
     }
@@ -582,6 +596,7 @@ static int launch_one(uot_ctx* c, int part, bool red, const int* stop, double to
         A.mx_out = c->b.mx[o]; A.my_out = c->b.my[o]; A.a_out = c->b.a[o];
         A.r = c->b.r;
         A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
+        A.r_mode = c->r_mode; A.r_scale = c->r_scale; A.fix_first = c->fix_first;
         A.G = c->G; A.T = c->T; A.P = c->P;
         if (c->prox) {
             const double rt = c->p.rho * c->tau1;
@@ -640,6 +655,7 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
     }
     A.r = c->b.r; A.p = c->b.frames;
     A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
+    A.r_mode = c->r_mode; A.r_scale = c->r_scale; A.fix_first = c->fix_first;
     if (c->prox) {
         const double rt = c->p.rho * c->tau1;
         A.c1 = (float)(rt / (1.0 + rt)); A.c2 = (float)(1.0 / (1.0 + rt)); A.c3 = (float)(c->tau1 / (1.0 + rt));
@@ -691,12 +707,13 @@ static void fill_report(const uot_ctx* c, const double* h, uot_report* out) {
     memset(out, 0, sizeof(*out));
     const double a = c->p.alpha;
     out->transport = h[GL_TR];
-    out->growth = a * h[GL_GR];
+    const bool bal = c->r_mode == 2;
+    out->growth = bal ? 0.0 : a * h[GL_GR];
     out->prox_term = c->prox ? 0.5 * c->p.rho * h[GL_PX] : 0.0;
     out->objective = out->transport + out->growth + out->prox_term;
     out->primal_res = sqrt(h[GL_K2]);
     out->dual_res = sqrt(h[GL_DZ]) / c->tau1;
-    out->upper_bound = out->transport + a * h[GL_UB];
+    out->upper_bound = bal ? (h[GL_UB] == 0.0 ? out->transport : INFINITY) : out->transport + a * h[GL_UB];
     out->lower_bound = NAN;
     out->f_norm = sqrt(h[GL_FSQ]);
     out->iterations = c->iter;
@@ -777,6 +794,7 @@ int uot_objective(uot_ctx* c, double* per_pair, uot_report* out) {
     O.p = c->prox ? c->b.frames : nullptr;
     O.mx = c->b.mx[slot]; O.my = c->b.my[slot]; O.r = c->b.r; O.a = c->b.a[slot];
     O.partials = c->part;
+    O.p2 = c->r_mode == 1;
     k_objective<<<dim3(c->bpp, c->G), 256, 0, c->s>>>(O);
     int rc = check_launch(c, "k_objective");
     if (rc) return rc;
@@ -798,18 +816,21 @@ int uot_objective(uot_ctx* c, double* per_pair, uot_report* out) {
     bool nonfinite = false;
     for (int g = 0; g < c->G; ++g) {
         const double* q = rows + (size_t)g * kRec;
+        // weak duality; c scales a into the dual-feasible set
+        const bool bal = c->r_mode == 2, p2 = c->r_mode == 1;
         double cc = 1.0;
         if (q[4] > cc) cc = q[4];
-        if (q[5] / a > cc) cc = q[5] / a;
-        const double U = q[0] + a * q[2];
-        const double L = -q[3] / cc;                  // weak duality
+        if (!bal && !p2 && q[5] / a > cc) cc = q[5] / a;
+        const double U = bal ? (q[2] == 0.0 ? q[0] : INFINITY) : q[0] + a * q[2];
+        const double L = p2 ? -q[3] / cc - q[7] / (4.0 * a * cc * cc) : -q[3] / cc;
+        const double obj = bal ? q[0] : q[0] + a * q[1];
         if (per_pair) {
             double* P = per_pair + (size_t)g * 8;
             P[0] = q[0]; P[1] = q[1]; P[2] = U; P[3] = q[3]; P[4] = q[4]; P[5] = q[5]; P[6] = L;
-            P[7] = q[0] + a * q[1];
+            P[7] = obj;
         }
-        tr += q[0]; gr += q[1]; ub += U; lb += L; px += q[6];
-        for (int k = 0; k < 7; ++k) nonfinite |= !isfinite(q[k]);
+        tr += q[0]; gr += bal ? 0.0 : q[1]; ub += U; lb += L; px += q[6];
+        for (int k = 0; k < 8; ++k) if (k != 2) nonfinite |= !isfinite(q[k]);
     }
     free(rows);
     if (out) {

@@ -45,7 +45,10 @@ struct IterArgs {
     float* my_out;
     float* a_out;
     float* r;                         // [G][N] in place
-    float tau1, tau2, atau1;          // atau1 = alpha * tau1
+    float tau1, tau2, atau1;          // atau1 = alpha * tau1 (+inf when balanced)
+    int r_mode;                       // 0: l1 soft threshold, 1: l2 averaging (p = 2), 2: balanced (r = 0)
+    float r_scale;                    // 1/(1 + 2 alpha tau1) for r_mode 1
+    int fix_first;                    // prox: frame 0 of each chain is constant
     // prox mode
     const float* x_in;                // [B][T][N] iteration k
     float* x_out;                     // [B][T][N] iteration k+1
@@ -113,6 +116,14 @@ __device__ __forceinline__ float shrink_factor(float n2, float inv, float t1) {
 __device__ __forceinline__ float soft(float q, float s) {
     return copysignf(fmaxf(fabsf(q) - s, 0.f), q);
 }
+
+// r-update on q = r + tau1 a: l1 soft threshold, l2 averaging, or 0 (balanced)
+__device__ __forceinline__ float r_update(float q, int mode, float at1, float rscale) {
+    return mode == 0 ? soft(q, at1) : (mode == 1 ? q * rscale : 0.f);
+}
+
+// |v|^p for the growth / repaired-bound reductions
+__device__ __forceinline__ float pw(float v, int mode) { return mode == 1 ? v * v : fabsf(v); }
 
 // Fused iteration.  PROX = false: fixed marginals (rho = inf), K = div M - r - f.
 // PROX = true: Alg.1 line 4 as well: frames x are iterates with
@@ -304,16 +315,18 @@ k_iter(const IterArgs A) {
             const float s = shrink_factor(n2, inv, t1);
             mxn[v] = s * qx;
             myn[v] = s * qy;
-            // Alg.1 line 5: r <- shrink^{l1}_{alpha tau1}(r + tau1 a)
-            rn[v] = soft(fmaf(t1, a_c[v], c_r[v]), at1);
+            // Alg.1 line 5: r <- shrink^{l1}_{alpha tau1}(r + tau1 a); p = 2 averaging
+            // update; balanced: r dropped
+            rn[v] = r_update(fmaf(t1, a_c[v], c_r[v]), A.r_mode, at1, A.r_scale);
             if constexpr (RED) s_tr += (n2 > 0.f) ? fmaxf(n2 * inv - t1, 0.f) : 0.f;
         }
         // Alg.1 line 4 (prox): x_t and x_{t+1} from the iteration-k duals
         float x0n[V], x1n[V], fk[V], fn[V];
+        const bool fix0 = PROX && A.fix_first && (pair % A.P == 0);     // constant first argument
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             if constexpr (PROX) {
-                x0n[v] = fmaxf(fmaf(c1, c_p0[v], fmaf(c2, c_x0[v], -c3 * (a_c[v] - c_am[v]))), 0.f);
+                x0n[v] = fix0 ? c_x0[v] : fmaxf(fmaf(c1, c_p0[v], fmaf(c2, c_x0[v], -c3 * (a_c[v] - c_am[v]))), 0.f);
                 x1n[v] = fmaxf(fmaf(c1, c_p1[v], fmaf(c2, c_x1[v], -c3 * (c_ap[v] - a_c[v]))), 0.f);
                 fk[v] = c_x1[v] - c_x0[v];
                 fn[v] = x1n[v] - x0n[v];
@@ -353,10 +366,10 @@ k_iter(const IterArgs A) {
             an[v] = fmaf(t2, 2.f * Kn - Kk, a_c[v]);
             if constexpr (RED) {
                 const float dmx = mxn[v] - mxk[v], dmy = myn[v] - myk[v], dr = rn[v] - c_r[v];
-                s_gr += fabsf(rn[v]);
+                s_gr += pw(rn[v], A.r_mode);
                 s_k2 += Kn * Kn;
                 s_dz += dmx * dmx + dmy * dmy + dr * dr;
-                s_ub += fabsf(divn - fn[v]);
+                s_ub += pw(divn - fn[v], A.r_mode);
                 if constexpr (PROX) {
                     const float d0 = x0n[v] - c_x0[v], e0 = x0n[v] - c_p0[v];
                     s_dz += d0 * d0;
@@ -427,6 +440,7 @@ struct ObjArgs {
     const float* p;           // [B][T][N] prox centres (prox) or nullptr
     const float* mx; const float* my; const float* r; const float* a;
     double* partials;
+    int p2;                   // p = 2 sums (r^2, (div M - f)^2)
 };
 __global__ void __launch_bounds__(256) k_objective(const ObjArgs O);
 

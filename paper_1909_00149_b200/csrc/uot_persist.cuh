@@ -42,6 +42,7 @@ struct PersistArgs {
     float* r;
     float* xb[2]; const float* p;
     float tau1, tau2, atau1, c1, c2, c3;
+    int r_mode; float r_scale; int fix_first;
     float* xchg;                      // [ctas][2][4*TW + 4*TH]
     int* flags;                       // [ctas], zeroed before the launch
     int* bar;                         // [2] grid barrier (count, generation), zeroed before the launch
@@ -198,10 +199,10 @@ k_persist(const PersistArgs A) {
             const int km = (jj + 1) * L.wm + (ii + 1);
             const float ac = sA[ka];
             const float rk = sR[e];
-            const float rn = soft(fmaf(t1, ac, rk), at1);
+            const float rn = r_update(fmaf(t1, ac, rk), A.r_mode, at1, A.r_scale);
             float fk, fn, x0n = 0.f, x1n = 0.f;
             if constexpr (PROX) {
-                x0n = fmaxf(fmaf(A.c1, sP0[e], fmaf(A.c2, sF[e], -A.c3 * (ac - 0.f))), 0.f);
+                x0n = A.fix_first ? sF[e] : fmaxf(fmaf(A.c1, sP0[e], fmaf(A.c2, sF[e], -A.c3 * (ac - 0.f))), 0.f);
                 x1n = fmaxf(fmaf(A.c1, sP1[e], fmaf(A.c2, sX1[e], -A.c3 * (0.f - ac))), 0.f);
                 fk = sX1[e] - sF[e];
                 fn = x1n - x0n;
@@ -218,10 +219,10 @@ k_persist(const PersistArgs A) {
                 const float mx2 = MXn[km] * MXn[km] + MYn[km] * MYn[km];
                 const float dmx = MXn[km] - MXk[km], dmy = MYn[km] - MYk[km], dr = rn - rk;
                 s_tr += sqrtf(mx2);
-                s_gr += fabsf(rn);
+                s_gr += pw(rn, A.r_mode);
                 s_k2 += Kn * Kn;
                 s_dz += dmx * dmx + dmy * dmy + dr * dr;
-                s_ub += fabsf(divn - fn);
+                s_ub += pw(divn - fn, A.r_mode);
                 if constexpr (PROX) {
                     const float d0 = x0n - sF[e], d1 = x1n - sX1[e], e0 = x0n - sP0[e], e1 = x1n - sP1[e];
                     s_dz += d0 * d0 + d1 * d1;

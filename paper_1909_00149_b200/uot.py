@@ -24,10 +24,10 @@ def _params(nx, ny, B, T, alpha, rho, tau1, tau2, flags=0) -> Params:
                   float(tau1 or 0.0), float(tau2 or 0.0), int(flags))
 
 
-def default_steps(nx, ny, n_frames=2, rho=math.inf, safety=0.99):
+def default_steps(nx, ny, n_frames=2, rho=math.inf, safety=0.99, fix_first=False):
     """Theorem-1 steps (L11/L12) from the library."""
     t1, t2 = ctypes.c_double(), ctypes.c_double()
-    p = _params(nx, ny, 1, n_frames, 1.0, rho, 0, 0)
+    p = _params(nx, ny, 1, n_frames, 1.0, rho, 0, 0, _lib.UOT_FIX_FIRST_FRAME if fix_first else 0)
     check(lib().uot_default_steps(ctypes.byref(p), float(safety), ctypes.byref(t1), ctypes.byref(t2)))
     return t1.value, t2.value
 
@@ -56,7 +56,8 @@ class Problem:
 
     def __init__(self, frames: torch.Tensor, alpha: float, rho: float = math.inf,
                  tau1: float | None = None, tau2: float | None = None, *, stream: torch.cuda.Stream | None = None,
-                 force_steps: bool = False, reset: bool = True, halos: bool = False):
+                 force_steps: bool = False, reset: bool = True, halos: bool = False,
+                 p_norm: int = 1, fix_first: bool = False):
         if frames.dim() != 4:
             raise ValueError("frames must be [B][T][ny][nx]")
         if not frames.is_cuda or frames.dtype != torch.float32:
@@ -81,8 +82,12 @@ class Problem:
         # chain-prox shard halos (L19): duals of the pairs just outside this shard, [B][ny][nx]
         self.a_prev_halo = torch.zeros((B, ny, nx), dtype=torch.float32, device=dev) if halos else None
         self.a_next_halo = torch.zeros((B, ny, nx), dtype=torch.float32, device=dev) if halos else None
-        self._params = _params(nx, ny, B, T, alpha, rho, tau1, tau2,
-                               _lib.UOT_FORCE_STEPS if force_steps else 0)
+        flags = (_lib.UOT_FORCE_STEPS if force_steps else 0) | (_lib.UOT_RESIDUAL_L2 if p_norm == 2 else 0) | \
+            (_lib.UOT_FIX_FIRST_FRAME if fix_first else 0)
+        if p_norm not in (1, 2):
+            raise ValueError("p_norm must be 1 or 2")
+        self.p_norm, self.fix_first = p_norm, fix_first
+        self._params = _params(nx, ny, B, T, alpha, rho, tau1, tau2, flags)
         nsc = int(lib().uot_scratch_doubles(ctypes.byref(self._params)))
         self.scratch = torch.zeros(nsc, dtype=torch.float64, device=dev)
         self._bufs = self._make_buffers()
@@ -91,7 +96,7 @@ class Problem:
                                ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx)))
         self._ctx = ctx
         if tau1 is None or tau2 is None:
-            d1, d2 = default_steps(nx, ny, T, rho)
+            d1, d2 = default_steps(nx, ny, T, rho, fix_first=fix_first)
             self.tau1 = float(tau1) if tau1 is not None else d1
             self.tau2 = float(tau2) if tau2 is not None else d2
         else:
