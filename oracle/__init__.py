@@ -45,6 +45,13 @@ class _Params(ctypes.Structure):
                 ("fix_first", ctypes.c_int32)]
 
 
+class _DfParams(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("n_problems", ctypes.c_int32),
+                ("mu", ctypes.c_double), ("kappa", ctypes.c_double), ("rho", ctypes.c_double),
+                ("tau1", ctypes.c_double), ("tau2", ctypes.c_double), ("inner_iters", ctypes.c_int32),
+                ("p_norm", ctypes.c_int32)]
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -61,6 +68,8 @@ def lib():
         L.uot_ref_iterate.restype = ctypes.c_int
         L.uot_ref_certificate.argtypes = [ctypes.POINTER(_Params), dp, dp, dp, dp, dp, dp, dp]
         L.uot_ref_certificate.restype = ctypes.c_int
+        L.uot_ref_df_admm.argtypes = [ctypes.POINTER(_DfParams), dp, dp] + [dp] * 9 + [ctypes.c_int, dp]
+        L.uot_ref_df_admm.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -222,3 +231,28 @@ def evaluate(p, q, alpha, iters=20000, tol=1e-9, tau=None, chunk=2000, p_norm: i
         if U - L <= tol * max(abs(U), 1e-12):
             break
     return cert[0, 2], cert[0, 6], cert[0, 7]
+
+
+# --------------------------------------------------------------------------- Algorithm 2
+DF_STATE = ("s", "x", "z", "a", "b", "mx", "my", "r", "ain")
+
+
+def df_zero_state(B, ny, nx):
+    """Alg. 2 line 2: s = x = z = a = b = 0; inner prox state 0."""
+    return {k: np.zeros((B, ny, nx)) for k in DF_STATE}
+
+
+def df_admm(y, s0, mu, kappa, rho, tau1, tau2, n_outer, inner_iters=1, state=None, p_norm=1):
+    """Algorithm 2, Phi = I, R = 0, for B problems y, s0 [B][ny][nx].
+    Returns (state dict, res[n_outer][2] = primal, dual residuals of P:562-567)."""
+    y, s0 = _f64(y), _f64(s0)
+    B, ny, nx = y.shape
+    st = {k: _f64(v).copy() for k, v in (state or df_zero_state(B, ny, nx)).items()}
+    prm = _DfParams(nx, ny, B, float(mu), float(kappa), float(rho), float(tau1), float(tau2),
+                    int(inner_iters), int(p_norm))
+    res = np.zeros((n_outer, 2))
+    rc = lib().uot_ref_df_admm(ctypes.byref(prm), _p(y), _p(s0), *[_p(st[k]) for k in DF_STATE],
+                               int(n_outer), _p(res))
+    if rc == 4:
+        raise FloatingPointError("non-finite iterate")
+    return st, res

@@ -151,3 +151,48 @@ def uot_1d_p2_enum(p, q, alpha):
             M[free] = Mf
             best = min(best, F(M))
     return float(best)
+
+
+def uot_df_1d_qp(y, s0, kappa, mu):
+    """Exact optimum of eq:UOT-DF with Phi = I on a 1 x n grid,
+        min_{s >= 0} 1/2 ||y - s||^2 + kappa V_mu(s0, s),
+    written as one QP in (s, M+, M-, r+, r-) >= 0 with the Beckmann constraint
+    M_i - M_{i-1} - r_i = s_i - s0_i (L1) and solved by scipy SLSQP (independent
+    of Algorithms 1-2).  Returns (value, s)."""
+    from scipy.optimize import minimize
+    y, s0 = np.asarray(y, float), np.asarray(s0, float)
+    n = y.size
+    m = n - 1
+    nv = n + 2 * m + 2 * n
+
+    def unpack(v):
+        return v[:n], v[n:n + m] - v[n + m:n + 2 * m], v[n + 2 * m:n + 2 * m + n] - v[n + 2 * m + n:]
+
+    def obj(v):
+        s = v[:n]
+        return 0.5 * ((y - s) ** 2).sum() + kappa * (v[n:n + 2 * m].sum() + mu * v[n + 2 * m:].sum())
+
+    def grad(v):
+        g = np.empty(nv)
+        g[:n] = v[:n] - y
+        g[n:n + 2 * m] = kappa
+        g[n + 2 * m:] = kappa * mu
+        return g
+
+    A = np.zeros((n, nv))
+    for i in range(n):
+        A[i, i] = -1.0                                        # - s_i
+        if i < m:
+            A[i, n + i] += 1.0; A[i, n + m + i] -= 1.0        # + M_i
+        if i >= 1:
+            A[i, n + i - 1] -= 1.0; A[i, n + m + i - 1] += 1.0   # - M_{i-1}
+        A[i, n + 2 * m + i] -= 1.0; A[i, n + 2 * m + n + i] += 1.0   # - r_i
+    cons = {"type": "eq", "fun": lambda v: A @ v + s0, "jac": lambda v: A}
+    x0 = np.concatenate([np.maximum(y, 0), np.zeros(2 * m + 2 * n)])
+    best = None
+    for start in (x0, np.concatenate([np.maximum(s0, 0), np.zeros(2 * m + 2 * n)])):
+        res = minimize(obj, start, jac=grad, constraints=[cons], bounds=[(0, None)] * nv, method="SLSQP",
+                       options={"ftol": 1e-15, "maxiter": 2000})
+        if best is None or res.fun < best.fun:
+            best = res
+    return float(best.fun), unpack(best.x)[0]

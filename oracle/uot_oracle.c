@@ -360,3 +360,76 @@ int uot_ref_certificate(const uot_ref_params* prm, const double* frames,
     free(dv); free(gx); free(gy);
     return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Algorithm 2 (UOT-DF ADMM) for eq:UOT-DF with
+ * Phi = I and R = 0 (the denoising setting of Fig. 1), on B
+ * independent problems (y_b, s0_b):
+ *   min_{s >= 0} 1/2 ||y - s||^2 + kappa V_mu(s0, s)
+ * (V is symmetric, P13, so the prior is the constant FIRST argument of the
+ * prox as in Alg. 2 line 6 / eq:Prox_UOT_specialcase, reading L22).
+ * Per outer iteration, in the paper's order:
+ *   line 4: s <- Pi_+((x + a + z + b)/2): the minimiser over s of the printed
+ *           augmented Lagrangian; the printed line 4 / P:487-492
+ *           "prox(x + a)" drops the (z - s + b) term, with which the UOT term
+ *           could never reach s (reading L23, pinned by DF3's KKT check)
+ *   line 5: x <- (y + rho (s - a)) / (1 + rho)                (Phi = I)
+ *   line 6: z <- prox^mu_{kappa/rho V_{s0}}(s - b): inner_iters warm-started
+ *           iterations of Alg. 1 with the first argument fixed (A := I,
+ *           P:343-349); in the L2 rho convention its weight is rho/kappa (L2)
+ *   line 7: a <- a + x - s;  line 8: b <- b + z - s
+ * res[it*2 + 0/1] = primal ||[x - s; z - s]||_2, dual rho ||[x - x_prev; z - z_prev]||_2
+ * (stopping criterion of P:562-567).  State arrays [B][N]; inner state
+ * mx, my, r, ain [B][N] (the inner "pair" of each problem).  Returns 0 or 4. */
+typedef struct {
+    int32_t nx, ny, n_problems;
+    double mu, kappa, rho, tau1, tau2;
+    int32_t inner_iters, p_norm;
+} uot_ref_df_params;
+
+int uot_ref_df_admm(const uot_ref_df_params* prm, const double* y, const double* s0,
+                    double* s, double* x, double* z, double* a, double* b,
+                    double* mx, double* my, double* r, double* ain, int n_outer, double* res) {
+    const int B = prm->n_problems;
+    const size_t N = (size_t)prm->nx * prm->ny;
+    double* fr = malloc(sizeof(double) * N * 2 * B);    /* inner frames [B][2][N]: (s0, v) */
+    double* xin = malloc(sizeof(double) * N * 2 * B);   /* inner x [B][2][N]: (s0, z)      */
+    double* xn = malloc(sizeof(double) * N * B);
+    uot_ref_params ip;
+    ip.nx = prm->nx; ip.ny = prm->ny; ip.n_chains = B; ip.n_frames = 2;
+    ip.alpha = prm->mu; ip.rho = prm->rho / prm->kappa; ip.tau1 = prm->tau1; ip.tau2 = prm->tau2;
+    ip.p_norm = prm->p_norm; ip.fix_first = 1;
+    int status = 0;
+    for (int it = 0; it < n_outer; ++it) {
+        double pr = 0.0, du = 0.0;
+        for (size_t k = 0; k < N * B; ++k) {
+            double v = 0.5 * (x[k] + a[k] + z[k] + b[k]);
+            s[k] = v > 0.0 ? v : 0.0;                                  /* line 4 (L23) */
+            xn[k] = (y[k] + prm->rho * (s[k] - a[k])) / (1.0 + prm->rho);   /* line 5 */
+        }
+        for (int bb = 0; bb < B; ++bb)
+            for (size_t k = 0; k < N; ++k) {
+                size_t q = (size_t)bb * N + k;
+                fr[((size_t)bb * 2) * N + k] = s0[q];
+                fr[((size_t)bb * 2 + 1) * N + k] = s[q] - b[q];        /* prox centre v = s - b */
+                xin[((size_t)bb * 2) * N + k] = s0[q];
+                xin[((size_t)bb * 2 + 1) * N + k] = z[q];
+            }
+        int rc = uot_ref_iterate(&ip, fr, mx, my, r, ain, xin, prm->inner_iters, NULL);   /* line 6 */
+        if (rc) status = rc;
+        for (int bb = 0; bb < B; ++bb)
+            for (size_t k = 0; k < N; ++k) {
+                size_t q = (size_t)bb * N + k;
+                double zn = xin[((size_t)bb * 2 + 1) * N + k];
+                a[q] += xn[q] - s[q];                                  /* line 7 */
+                b[q] += zn - s[q];                                     /* line 8 */
+                pr += (xn[q] - s[q]) * (xn[q] - s[q]) + (zn - s[q]) * (zn - s[q]);
+                du += (xn[q] - x[q]) * (xn[q] - x[q]) + (zn - z[q]) * (zn - z[q]);
+                x[q] = xn[q];
+                z[q] = zn;
+            }
+        if (res) { res[2 * it] = sqrt(pr); res[2 * it + 1] = prm->rho * sqrt(du); }
+    }
+    free(fr); free(xin); free(xn);
+    return status;
+}

@@ -13,6 +13,8 @@ muts=(
 's/uot_ref_shrink_l1((int64_t)N, gx + o, alpha \* tau1, rn + o);/uot_ref_shrink_l1((int64_t)N, gx + o, alpha, rn + o);/'
 's/rn\[o + k\] = gx\[o + k\] \/ (1.0 + 2.0 \* alpha \* tau1);/rn[o + k] = gx[o + k] \/ (1.0 + alpha * tau1);/'
 's/if (s == 0 \&\& prm->fix_first) {/if (s == 1 \&\& prm->fix_first) {/'
+'s/double v = 0.5 \* (x\[k\] + a\[k\] + z\[k\] + b\[k\]);/double v = x[k] + a[k];/'
+'s/xn\[k\] = (y\[k\] + prm->rho \* (s\[k\] - a\[k\])) \/ (1.0 + prm->rho);/xn[k] = (y[k] + prm->rho * (s[k] + a[k])) \/ (1.0 + prm->rho);/'
 )
 for m in "${muts[@]}"; do
   rm -rf w; mkdir w; cp -r /root/repo/oracle /root/repo/tests /root/repo/paper_1909_00149_b200 w/; rm -f w/oracle/liboracle.so

@@ -483,3 +483,58 @@ def test_P5d_fixed_first_step_norm():
     K = np.hstack([D, -I, -I])
     t1, t2 = oracle.default_steps(nx, ny, prox=True, fix_first=True, safety=1.0)
     assert 1.0 / (t1 * t2) == pytest.approx(np.linalg.norm(K, 2) ** 2, rel=1e-10)
+
+
+# ----------------------------------------------------------------------------- DF1-DF4 Algorithm 2
+def _df_tau(nx, ny):
+    return oracle.default_steps(nx, ny, prox=True, fix_first=True, safety=0.95)[0]
+
+
+def test_DF1_DF2_limits():
+    """DF1: kappa -> 0 gives s = Pi_+(y); DF2: noiseless y = s0 >= 0 gives s = y."""
+    g = np.random.default_rng(40)
+    y = g.normal(size=(2, 6, 7))
+    s0 = g.random((2, 6, 7))
+    t = _df_tau(7, 6)
+    st, res = oracle.df_admm(y, s0, 1.0, 1e-9, 1.0, t, t, 400)
+    np.testing.assert_allclose(st["s"], np.maximum(y, 0), atol=1e-6)
+    st, res = oracle.df_admm(s0, s0, 1.0, 2.0, 1.0, t, t, 3000)
+    np.testing.assert_allclose(st["s"], s0, atol=1e-6)
+
+
+def test_DF3_kkt_of_uot_df():
+    """DF3: the ADMM fixed point solves eq:UOT-DF: s = x = z (splitting) and
+    s = Pi_+(y + kappa a*) with a* a dual certificate of V(s0, s): K = 0, |a*| <= mu,
+    ||div* a*|| <= 1 (Lagrangian P:235-242, subgradient of V in its argument is -a*)."""
+    g = np.random.default_rng(41)
+    s0 = g.random((1, 8, 8)) * (g.random((1, 8, 8)) < 0.3)
+    y = np.roll(s0, 1, axis=2) * 1.3 + 0.02 * g.normal(size=(1, 8, 8))
+    mu, kappa, rho = 0.8, 0.6, 1.0
+    t = _df_tau(8, 8)
+    st, res = oracle.df_admm(y, s0, mu, kappa, rho, t, t, 20000)
+    assert res[-1, 0] < 1e-9 and res[-1, 1] < 1e-9
+    np.testing.assert_allclose(st["x"], st["s"], atol=1e-8)
+    np.testing.assert_allclose(st["z"], st["s"], atol=1e-8)
+    np.testing.assert_allclose(st["s"], np.maximum(y + kappa * st["ain"], 0), atol=1e-7)
+    K = oracle.div(st["mx"][0], st["my"][0]) - st["r"][0] - st["z"][0] + s0[0]
+    assert np.abs(K).max() < 1e-8
+    assert np.abs(st["ain"]).max() <= mu + 1e-8
+    gx, gy = oracle.div_adj(st["ain"][0])
+    assert np.hypot(gx, gy).max() <= 1 + 1e-8
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_DF4_uot_df_1d_bruteforce_qp(seed):
+    """DF4: 1-D eq:UOT-DF optimum by an independent QP (SLSQP over (s, M, r)) equals the
+    value at the ADMM limit; V evaluated by the HiGHS LP of P12."""
+    g = np.random.default_rng(50 + seed)
+    s0 = g.random(6) * (g.random(6) < 0.6)
+    y = np.roll(s0, 1) + 0.1 * g.normal(size=6)
+    mu, kappa = 0.7, 0.9
+    v_qp, s_qp = lp.uot_df_1d_qp(y, s0, kappa, mu)
+    t = _df_tau(6, 1)
+    st, res = oracle.df_admm(y[None, None, :], s0[None, None, :], mu, kappa, 1.0, t, t, 30000)
+    s = st["s"][0, 0]
+    v_admm = 0.5 * ((y - s) ** 2).sum() + kappa * lp.uot_1d_linprog(s0, s, mu)
+    assert v_admm == pytest.approx(v_qp, rel=1e-6, abs=1e-9)
+    np.testing.assert_allclose(s, s_qp, atol=1e-4)
