@@ -197,6 +197,74 @@ void uot_destroy(uot_ctx* ctx);
 /* Last error message of ctx (or of the last failed uot_create if ctx == NULL). */
 const char* uot_last_error(const uot_ctx* ctx);
 
+/* ===========================================================================
+ * UOT-DF ADMM: Algorithm 2 for eq:UOT-DF
+ * with Phi = I and R = 0 -- the denoising setting of the paper's
+ * runtime experiment (Fig. 1) -- on B independent problems:
+ *     min_{s >= 0} 1/2 ||y - s||^2 + kappa V_mu(s0, s)
+ * Per ADMM iteration (readings L22, L23 in DESIGN.md):
+ *   s <- Pi_+((x + a + z + b)/2)   (minimiser of the printed augmented
+ *                                    Lagrangian P:479-484; L23)
+ *   x <- (y + rho (s - a))/(1 + rho)                          (line 5, Phi = I)
+ *   z <- inner_iters warm-started Alg.1 iterations of the fixed-first-argument
+ *        prox (eq:Prox_UOT_specialcase) of V_{s0} with weight rho/kappa (L2)
+ *        and centre s - b                                      (line 6)
+ *   a <- a + x - s;  b <- b + z - s                            (lines 7-8)
+ * inner_iters = 1 (the paper's setting) runs as ONE fused streaming
+ * kernel per ADMM iteration; inner_iters > 1 composes a pointwise kernel, the
+ * prox kernels above and a pointwise dual update.
+ * Stopping: ||[x-s; z-s]||_2 < eps and rho ||[dx; dz]||_2 < eps,
+ * tested on the device every check_every iterations.
+ * ======================================================================== */
+typedef struct uot_df_ctx uot_df_ctx;
+
+typedef struct {
+    int32_t  nx, ny, n_problems;   /* grid, B >= 1                                            */
+    double   mu;                   /* UOT unbalance weight (alpha elsewhere), > 0 or +inf (balanced) */
+    double   kappa;                /* dynamics weight kappa > 0                       */
+    double   rho;                  /* ADMM penalty rho > 0                            */
+    double   tau1, tau2;           /* inner Alg.1 steps; 0 = Theorem-1 default for K = [D,-I,-I] */
+    int32_t  inner_iters;          /* Alg.1 iterations per ADMM iteration, >= 1 (1)     */
+    uint32_t flags;                /* UOT_RESIDUAL_L2, UOT_FORCE_STEPS                        */
+} uot_df_params;
+
+typedef struct {                   /* caller-owned device buffers, fp32, [B][ny][nx] unless noted */
+    const float* y;                /* measurements (Phi = I)                                   */
+    const float* s0;               /* prior s~, the constant first argument            */
+    float* s;                      /* estimate s^k (output; written on checked iterations)     */
+    float* x; float* a; float* b;  /* ADMM split variable and scaled duals        */
+    float* pf;                     /* [B][2][ny][nx] inner prox frames (s0, centre)            */
+    float* xz[2];                  /* [B][2][ny][nx] inner frames (s0, z), ping-pong           */
+    float* mx[2]; float* my[2];    /* inner flux, ping-pong                                    */
+    float* r;                      /* inner transport residual                                 */
+    float* ain[2];                 /* inner dual, ping-pong                                    */
+    float* tmp[2];                 /* scratch planes (inner_iters > 1 only; may be NULL otherwise) */
+    double* scratch;               /* uot_df_scratch_doubles(&params) doubles                  */
+} uot_df_buffers;
+
+typedef struct {
+    double primal_res;             /* ||[x - s; z - s]||_2                                      */
+    double dual_res;               /* rho ||[x - x_prev; z - z_prev]||_2                        */
+    double data_term;              /* 1/2 ||y - s||^2                                           */
+    double transport, growth;      /* inner ||M||_{2,1}, mu ||r||_p^p (fused path; NaN otherwise) */
+    double objective;              /* data_term + kappa (transport + growth) (estimate)        */
+    int64_t iterations;            /* ADMM iterations since uot_df_reset                       */
+    int32_t converged, nonfinite;
+} uot_df_report;
+
+size_t uot_df_scratch_doubles(const uot_df_params* params);
+int uot_df_create(const uot_df_params* params, const uot_df_buffers* buffers, void* cuda_stream, uot_df_ctx** out);
+/* cold start (Alg.2 line 2: s = x = z = a = b = 0; inner state 0). Async. */
+int uot_df_reset(uot_df_ctx* ctx);
+/* up to max_iters ADMM iterations; eps <= 0 runs exactly max_iters. Fills *out (may be NULL).
+ * Returns UOT_OK, UOT_E_NOT_CONVERGED (eps > 0 not met), UOT_E_NONFINITE, ... */
+int uot_df_solve(uot_df_ctx* ctx, int32_t max_iters, double eps, int32_t check_every, uot_df_report* out);
+int uot_df_set_timing(uot_df_ctx* ctx, int enable);
+int uot_df_get_timing(uot_df_ctx* ctx, double* ms_total, int64_t* n_launches);
+int64_t uot_df_launch_count(const uot_df_ctx* ctx);
+void uot_df_destroy(uot_df_ctx* ctx);
+const char* uot_df_last_error(const uot_df_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,9 @@ UOT_PART_ALL, UOT_PART_INTERIOR, UOT_PART_BOUNDARY = 0, 1, 2
 EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset", "uot_load_frames",
             "uot_iterate", "uot_iterate_part", "uot_get_report", "uot_prox_step", "uot_solve", "uot_objective", "uot_set_timing", "uot_get_timing",
             "uot_state_slot", "uot_launch_count",
-            "uot_destroy", "uot_last_error")
+            "uot_destroy", "uot_last_error",
+            "uot_df_scratch_doubles", "uot_df_create", "uot_df_reset", "uot_df_solve", "uot_df_set_timing",
+            "uot_df_get_timing", "uot_df_launch_count", "uot_df_destroy", "uot_df_last_error")
 
 
 class Params(ctypes.Structure):
@@ -48,6 +50,28 @@ class Report(ctypes.Structure):
     _fields_ = [("objective", ctypes.c_double), ("transport", ctypes.c_double), ("growth", ctypes.c_double),
                 ("prox_term", ctypes.c_double), ("primal_res", ctypes.c_double), ("dual_res", ctypes.c_double),
                 ("upper_bound", ctypes.c_double), ("lower_bound", ctypes.c_double), ("f_norm", ctypes.c_double),
+                ("iterations", ctypes.c_int64), ("converged", ctypes.c_int32), ("nonfinite", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class DfParams(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("n_problems", ctypes.c_int32),
+                ("mu", ctypes.c_double), ("kappa", ctypes.c_double), ("rho", ctypes.c_double),
+                ("tau1", ctypes.c_double), ("tau2", ctypes.c_double), ("inner_iters", ctypes.c_int32),
+                ("flags", ctypes.c_uint32)]
+
+
+class DfBuffers(ctypes.Structure):
+    _fields_ = [("y", _fp), ("s0", _fp), ("s", _fp), ("x", _fp), ("a", _fp), ("b", _fp), ("pf", _fp),
+                ("xz", _fp * 2), ("mx", _fp * 2), ("my", _fp * 2), ("r", _fp), ("ain", _fp * 2),
+                ("tmp", _fp * 2), ("scratch", _fp)]
+
+
+class DfReport(ctypes.Structure):
+    _fields_ = [("primal_res", ctypes.c_double), ("dual_res", ctypes.c_double), ("data_term", ctypes.c_double),
+                ("transport", ctypes.c_double), ("growth", ctypes.c_double), ("objective", ctypes.c_double),
                 ("iterations", ctypes.c_int64), ("converged", ctypes.c_int32), ("nonfinite", ctypes.c_int32)]
 
     def as_dict(self):
@@ -97,12 +121,24 @@ def lib():
     L.uot_launch_count.argtypes = [ctypes.c_void_p]; L.uot_launch_count.restype = ctypes.c_int64
     L.uot_destroy.argtypes = [ctypes.c_void_p]; L.uot_destroy.restype = None
     L.uot_last_error.argtypes = [ctypes.c_void_p]; L.uot_last_error.restype = ctypes.c_char_p
+    DP, DB, DR = ctypes.POINTER(DfParams), ctypes.POINTER(DfBuffers), ctypes.POINTER(DfReport)
+    L.uot_df_scratch_doubles.argtypes = [DP]; L.uot_df_scratch_doubles.restype = ctypes.c_size_t
+    L.uot_df_create.argtypes = [DP, DB, ctypes.c_void_p, ctx_pp]; L.uot_df_create.restype = ctypes.c_int
+    L.uot_df_reset.argtypes = [ctypes.c_void_p]; L.uot_df_reset.restype = ctypes.c_int
+    L.uot_df_solve.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, DR]
+    L.uot_df_solve.restype = ctypes.c_int
+    L.uot_df_set_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]; L.uot_df_set_timing.restype = ctypes.c_int
+    L.uot_df_get_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+    L.uot_df_get_timing.restype = ctypes.c_int
+    L.uot_df_launch_count.argtypes = [ctypes.c_void_p]; L.uot_df_launch_count.restype = ctypes.c_int64
+    L.uot_df_destroy.argtypes = [ctypes.c_void_p]; L.uot_df_destroy.restype = None
+    L.uot_df_last_error.argtypes = [ctypes.c_void_p]; L.uot_df_last_error.restype = ctypes.c_char_p
     _lib = L
     return L
 
 
-def check(rc, ctx=None, allow=()):
+def check(rc, ctx=None, allow=(), df=False):
     if rc == UOT_OK or rc in allow:
         return rc
-    msg = lib().uot_last_error(ctx)
+    msg = (lib().uot_df_last_error if df else lib().uot_last_error)(ctx)
     raise UotError(rc, msg.decode() if msg else "")

@@ -188,11 +188,16 @@ __global__ void __launch_bounds__(256) k_pair_reduce(const ReduceArgs R) {
         return;
     }
     if (R.tol > 0.0 && R.stop != nullptr) {
-        // L13: primal ||K|| and dual ||dz||/tau1 relative to ||f||
-        const double scale = R.tol * fmax(sqrt(R.glob[GL_FSQ]), 1e-30);
-        const double primal = sqrt(tot[2]);
-        const double dual = sqrt(tot[3]) / R.tau1;
-        if (primal <= scale && dual <= scale) {
+        bool ok;
+        if (R.stop_kind == 1) {
+            // Alg.2 stopping rule: ||[x-s; z-s]|| < eps and rho ||[dx; dz]|| < eps
+            ok = sqrt(tot[3]) < R.tol && R.rho_admm * sqrt(tot[4]) < R.tol;
+        } else {
+            // L13: primal ||K|| and dual ||dz||/tau1 relative to ||f||
+            const double scale = R.tol * fmax(sqrt(R.glob[GL_FSQ]), 1e-30);
+            ok = sqrt(tot[2]) <= scale && sqrt(tot[3]) / R.tau1 <= scale;
+        }
+        if (ok) {
             R.glob[GL_CONV] = (double)R.iteration;
             __threadfence();
             *R.stop = 1;
@@ -887,3 +892,6 @@ void uot_destroy(uot_ctx* c) {
 const char* uot_last_error(const uot_ctx* c) { return c ? c->err : g_err; }
 
 }  // extern "C"
+
+// UOT-DF ADMM (Algorithm 2) on top of the kernels above
+#include "uot_df.inc"

@@ -58,6 +58,13 @@ struct IterArgs {
     float c1, c2, c3;                 // rho tau1/(1+rho tau1), 1/(1+rho tau1), tau1/(1+rho tau1)
     double* partials;                 // [items][kRec] when reducing
     const int* stop;                  // device stop flag or nullptr
+    // UOT-DF ADMM (MODE 2): ADMM state in place, inner prox frames = (s0, z) in x_in/x_out
+    const float* y;                   // [B][N] measurements (Phi = I)
+    float* xa;                        // [B][N] ADMM x
+    float* aa;                        // [B][N] ADMM scaled dual a
+    float* ba;                        // [B][N] ADMM scaled dual b
+    float* s_out;                     // [B][N] s^{k+1} (written on reducing iterations)
+    float rho_admm, inv1prho;         // rho, 1/(1+rho)
 };
 
 template <int V>
@@ -132,7 +139,7 @@ __device__ __forceinline__ float pw(float v, int mode) { return mode == 1 ? v * 
 //   x_s' = max(0, c1 p_s + c2 x_s - c3 (A^T a)_s),  (A^T a)_s = a_s - a_{s-1},
 //   c1 = rho tau1/(1+rho tau1), c2 = 1/(1+rho tau1), c3 = tau1/(1+rho tau1),
 // with a_{-1} / a_{T-1} taken from the shard halos (or 0 at a chain end).
-template <int V, bool RED, bool PROX>
+template <int V, bool RED, bool PROX, bool DF = false>
 __global__ void __launch_bounds__(kWarps * 32)
 k_iter(const IterArgs A) {
     if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
@@ -193,7 +200,16 @@ k_iter(const IterArgs A) {
     const float* __restrict__ ami = nullptr; const float* __restrict__ api = nullptr;
     float* __restrict__ x0o = nullptr; float* __restrict__ x1o = nullptr;
     bool last_pair = false;
-    if constexpr (PROX) {
+    const float* __restrict__ ypi = nullptr;
+    float* __restrict__ xap = nullptr; float* __restrict__ aap = nullptr; float* __restrict__ bap = nullptr;
+    float* __restrict__ sop = nullptr;
+    if constexpr (DF) {
+        // pair g = problem b (T = 2): frame 0 = s0 (constant), frame 1 = z; x_out gets z^{k+1}
+        const size_t f0 = (size_t)pair * 2 * (size_t)A.N;
+        x0i = A.x_in + f0; x1i = x0i + A.N;
+        x1o = A.x_out + f0 + A.N;
+        ypi = A.y + po; xap = A.xa + po; aap = A.aa + po; bap = A.ba + po; sop = A.s_out + po;
+    } else if constexpr (PROX) {
         const int b = pair / A.P, t = pair % A.P;
         const size_t f0 = ((size_t)b * A.T + t) * (size_t)A.N;
         x0i = A.x_in + f0; x1i = x0i + A.N;
@@ -254,7 +270,14 @@ k_iter(const IterArgs A) {
             ld_ro<V>(n_mx, mxi + rj + ib);
             ld_ro<V>(n_my, myi + rj + ib);
             ld_rw<V>(n_r, rp + rj + ib);
-            if constexpr (PROX) {
+            if constexpr (DF) {
+                ld_ro<V>(n_x0, x0i + rj + ib);            // s0
+                ld_ro<V>(n_x1, x1i + rj + ib);            // z
+                ld_ro<V>(n_p1, ypi + rj + ib);            // y
+                ld_rw<V>(n_p0, xap + rj + ib);            // ADMM x
+                ld_rw<V>(n_am, aap + rj + ib);            // ADMM a
+                ld_rw<V>(n_ap, bap + rj + ib);            // ADMM b
+            } else if constexpr (PROX) {
                 ld_ro<V>(n_x0, x0i + rj + ib);
                 ld_ro<V>(n_x1, x1i + rj + ib);
                 ld_ro<V>(n_p0, p0i + rj + ib);
@@ -267,7 +290,7 @@ k_iter(const IterArgs A) {
             if (has_next) ld_ro<V>(n_a, ai + rj + nx + ib); else zero<V>(n_a);
         } else {
             zero<V>(n_mx); zero<V>(n_my); zero<V>(n_r); zero<V>(n_a);
-            if constexpr (PROX) { zero<V>(n_x0); zero<V>(n_x1); zero<V>(n_p0); zero<V>(n_p1); zero<V>(n_am); zero<V>(n_ap); }
+            if constexpr (PROX || DF) { zero<V>(n_x0); zero<V>(n_x1); zero<V>(n_p0); zero<V>(n_p1); zero<V>(n_am); zero<V>(n_ap); }
             else zero<V>(n_f);
         }
         if (lane == 0 && hasL) {
@@ -287,7 +310,7 @@ k_iter(const IterArgs A) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             c_a[v] = n_a[v]; c_mx[v] = n_mx[v]; c_my[v] = n_my[v]; c_r[v] = n_r[v];
-            if constexpr (PROX) {
+            if constexpr (PROX || DF) {
                 c_x0[v] = n_x0[v]; c_x1[v] = n_x1[v]; c_p0[v] = n_p0[v]; c_p1[v] = n_p1[v];
                 c_am[v] = n_am[v]; c_ap[v] = n_ap[v];
             } else {
@@ -322,10 +345,24 @@ k_iter(const IterArgs A) {
         }
         // Alg.1 line 4 (prox): x_t and x_{t+1} from the iteration-k duals
         float x0n[V], x1n[V], fk[V], fn[V];
+        float sn[V], xan[V], aan[V], ban[V];
         const bool fix0 = PROX && A.fix_first && (pair % A.P == 0);     // constant first argument
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            if constexpr (PROX) {
+            if constexpr (DF) {
+                // Alg.2 lines 4-5 (L23: s-update from the printed augmented Lagrangian; Phi = I)
+                sn[v] = fmaxf(0.5f * (c_p0[v] + c_am[v] + c_x1[v] + c_ap[v]), 0.f);
+                xan[v] = (c_p1[v] + A.rho_admm * (sn[v] - c_am[v])) * A.inv1prho;
+                // Alg.2 line 6: one warm-started Alg.1 iteration of prox_{kappa/rho V_{s0}}(s - b):
+                // z' = Pi_+(c1 v + c2 z + c3 a_in) (A := I with K = div M - r - z + s0)
+                x1n[v] = fmaxf(fmaf(c1, sn[v] - c_ap[v], fmaf(c2, c_x1[v], c3 * a_c[v])), 0.f);
+                x0n[v] = c_x0[v];
+                fk[v] = c_x1[v] - c_x0[v];
+                fn[v] = x1n[v] - c_x0[v];
+                // lines 7-8
+                aan[v] = c_am[v] + xan[v] - sn[v];
+                ban[v] = c_ap[v] + x1n[v] - sn[v];
+            } else if constexpr (PROX) {
                 x0n[v] = fix0 ? c_x0[v] : fmaxf(fmaf(c1, c_p0[v], fmaf(c2, c_x0[v], -c3 * (a_c[v] - c_am[v]))), 0.f);
                 x1n[v] = fmaxf(fmaf(c1, c_p1[v], fmaf(c2, c_x1[v], -c3 * (c_ap[v] - a_c[v]))), 0.f);
                 fk[v] = c_x1[v] - c_x0[v];
@@ -364,7 +401,17 @@ k_iter(const IterArgs A) {
             const float Kn = divn - rn[v] - fn[v];
             const float Kk = divk - c_r[v] - fk[v];
             an[v] = fmaf(t2, 2.f * Kn - Kk, a_c[v]);
-            if constexpr (RED) {
+            if constexpr (RED && DF) {
+                // ADMM residuals and the data term
+                const float p0 = xan[v] - sn[v], p1 = x1n[v] - sn[v];
+                const float d0 = xan[v] - c_p0[v], d1 = x1n[v] - c_x1[v];
+                const float e = c_p1[v] - sn[v];
+                s_gr += pw(rn[v], A.r_mode);
+                s_k2 += Kn * Kn;
+                s_dz += p0 * p0 + p1 * p1;
+                s_ub += d0 * d0 + d1 * d1;
+                s_px += 0.5f * e * e;
+            } else if constexpr (RED) {
                 const float dmx = mxn[v] - mxk[v], dmy = myn[v] - myk[v], dr = rn[v] - c_r[v];
                 s_gr += pw(rn[v], A.r_mode);
                 s_k2 += Kn * Kn;
@@ -388,7 +435,13 @@ k_iter(const IterArgs A) {
             st<V>(myo + rj, myn);
             st<V>(rp + rj, rn);
             st<V>(ao + rj, an);
-            if constexpr (PROX) {
+            if constexpr (DF) {
+                st<V>(x1o + rj, x1n);
+                st<V>(xap + rj, xan);
+                st<V>(aap + rj, aan);
+                st<V>(bap + rj, ban);
+                if constexpr (RED) st<V>(sop + rj, sn);
+            } else if constexpr (PROX) {
                 st<V>(x0o + rj, x0n);
                 if (last_pair) st<V>(x1o + rj, x1n);
             }
@@ -408,11 +461,11 @@ k_iter(const IterArgs A) {
             d2 += __shfl_xor_sync(kFull, d2, o);
             d3 += __shfl_xor_sync(kFull, d3, o);
             d4 += __shfl_xor_sync(kFull, d4, o);
-            if constexpr (PROX) d5 += __shfl_xor_sync(kFull, d5, o);
+            if constexpr (PROX || DF) d5 += __shfl_xor_sync(kFull, d5, o);
         }
         if (lane == 0) {
             double* P = A.partials + (size_t)rec * kRec;
-            P[0] = d0; P[1] = d1; P[2] = d2; P[3] = d3; P[4] = d4; P[5] = PROX ? d5 : 0.0; P[6] = 0.0; P[7] = 0.0;
+            P[0] = d0; P[1] = d1; P[2] = d2; P[3] = d3; P[4] = d4; P[5] = (PROX || DF) ? d5 : 0.0; P[6] = 0.0; P[7] = 0.0;
         }
     }
 }
@@ -461,6 +514,8 @@ struct ReduceArgs {
     long long iteration;      // iteration index just completed
     double tol;               // <= 0: no stop test
     double tau1;
+    int stop_kind;            // 0: L13 relative (K, dz); 1: ADMM absolute: sqrt(f3) < tol, rho sqrt(f4) < tol
+    double rho_admm;
 };
 __global__ void __launch_bounds__(256) k_pair_reduce(const ReduceArgs R);
 

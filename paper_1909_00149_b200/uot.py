@@ -14,9 +14,9 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import Buffers, Params, Report, check, lib
+from ._lib import Buffers, DfBuffers, DfParams, DfReport, Params, Report, check, lib
 
-__all__ = ["Problem", "default_steps", "scratch_doubles", "Report"]
+__all__ = ["Problem", "DFProblem", "default_steps", "scratch_doubles", "Report"]
 
 
 def _params(nx, ny, B, T, alpha, rho, tau1, tau2, flags=0) -> Params:
@@ -211,6 +211,104 @@ class Problem:
     def close(self):
         if getattr(self, "_ctx", None):
             lib().uot_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DFProblem:
+    """UOT-DF ADMM (Algorithm 2) with Phi = I, R = 0 on B problems:
+    min_{s >= 0} 1/2 ||y - s||^2 + kappa V_mu(s0, s)   (eq:UOT-DF).
+
+    y, s0: float32 CUDA tensors [B][ny][nx].  inner_iters = 1 runs one
+    fused kernel per ADMM iteration.  All steps run in libuot_b200.so."""
+
+    STATE = ("s", "x", "a", "b")
+
+    def __init__(self, y: torch.Tensor, s0: torch.Tensor, mu: float, kappa: float, rho: float = 1.0,
+                 tau1: float | None = None, tau2: float | None = None, inner_iters: int = 1, p_norm: int = 1,
+                 *, stream: torch.cuda.Stream | None = None, reset: bool = True):
+        if y.dim() != 3 or y.shape != s0.shape:
+            raise ValueError("y and s0 must be [B][ny][nx] of the same shape")
+        if not (y.is_cuda and s0.is_cuda) or y.dtype != torch.float32 or s0.dtype != torch.float32:
+            raise ValueError("y, s0 must be float32 CUDA tensors")
+        self.y, self.s0 = y.contiguous(), s0.contiguous()
+        B, ny, nx = self.y.shape
+        self.B, self.ny, self.nx = B, ny, nx
+        dev = self.y.device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        e = lambda *shape: torch.zeros(shape, dtype=torch.float32, device=dev)
+        self.s, self.x, self.a, self.b = e(B, ny, nx), e(B, ny, nx), e(B, ny, nx), e(B, ny, nx)
+        self.pf = e(B, 2, ny, nx)
+        self.xz = [e(B, 2, ny, nx), e(B, 2, ny, nx)]
+        self.mx, self.my, self.ain = [e(B, ny, nx), e(B, ny, nx)], [e(B, ny, nx), e(B, ny, nx)], [e(B, ny, nx), e(B, ny, nx)]
+        self.r = e(B, ny, nx)
+        self.tmp = [e(B, ny, nx), e(B, ny, nx)] if inner_iters > 1 else [None, None]
+        flags = _lib.UOT_RESIDUAL_L2 if p_norm == 2 else 0
+        self._p = DfParams(nx, ny, B, float(mu), float(kappa), float(rho), float(tau1 or 0.0), float(tau2 or 0.0),
+                           int(inner_iters), flags)
+        nsc = int(lib().uot_df_scratch_doubles(ctypes.byref(self._p)))
+        self.scratch = torch.zeros(nsc, dtype=torch.float64, device=dev)
+        bf = DfBuffers()
+        bf.y, bf.s0, bf.s, bf.x = self.y.data_ptr(), self.s0.data_ptr(), self.s.data_ptr(), self.x.data_ptr()
+        bf.a, bf.b, bf.pf = self.a.data_ptr(), self.b.data_ptr(), self.pf.data_ptr()
+        for k in range(2):
+            bf.xz[k] = self.xz[k].data_ptr()
+            bf.mx[k] = self.mx[k].data_ptr()
+            bf.my[k] = self.my[k].data_ptr()
+            bf.ain[k] = self.ain[k].data_ptr()
+            bf.tmp[k] = self.tmp[k].data_ptr() if self.tmp[k] is not None else None
+        bf.r = self.r.data_ptr()
+        bf.scratch = self.scratch.data_ptr()
+        self._bufs = bf
+        ctx = ctypes.c_void_p()
+        check(lib().uot_df_create(ctypes.byref(self._p), ctypes.byref(bf), ctypes.c_void_p(self.stream.cuda_stream),
+                                  ctypes.byref(ctx)), None, df=True)
+        self._ctx = ctx
+        self.iterations = 0
+        if reset:
+            self.reset()
+
+    def reset(self):
+        check(lib().uot_df_reset(self._ctx), self._ctx, df=True)
+        self.iterations = 0
+
+    def solve(self, max_iters: int, eps: float = 0.0, check_every: int = 10) -> dict:
+        rep = DfReport()
+        rc = check(lib().uot_df_solve(self._ctx, int(max_iters), float(eps), int(check_every), ctypes.byref(rep)),
+                   self._ctx, allow=(_lib.UOT_E_NOT_CONVERGED,), df=True)
+        d = rep.as_dict()
+        d["status"] = rc
+        self.iterations = d["iterations"]
+        return d
+
+    def inner_state(self) -> dict:
+        """Inner prox state (M, r, a_in, z) of the current iterate."""
+        s = int(self.iterations_inner() & 1)
+        return {"mx": self.mx[s], "my": self.my[s], "r": self.r, "ain": self.ain[s], "z": self.xz[s][:, 1]}
+
+    def iterations_inner(self) -> int:
+        return self.iterations * int(self._p.inner_iters)
+
+    def set_timing(self, enable=True):
+        check(lib().uot_df_set_timing(self._ctx, int(bool(enable))), self._ctx, df=True)
+
+    def get_timing(self):
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        check(lib().uot_df_get_timing(self._ctx, ctypes.byref(ms), ctypes.byref(n)), self._ctx, df=True)
+        return ms.value, n.value
+
+    @property
+    def launches(self) -> int:
+        return int(lib().uot_df_launch_count(self._ctx))
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().uot_df_destroy(self._ctx)
             self._ctx = None
 
     def __del__(self):

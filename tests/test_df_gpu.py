@@ -1,0 +1,66 @@
+"""GPU parity of the UOT-DF ADMM (Algorithm 2) vs the oracle's
+df_admm (fixed iteration counts), fused (inner_iters = 1) and composed
+(inner_iters > 1) paths, plus the device-side stopping rule of P:562-567."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1909_00149_b200 import inputs
+from paper_1909_00149_b200.uot import DFProblem
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(B, ny, nx, seed):
+    g = np.random.default_rng(seed)
+    s0 = (g.random((B, ny, nx)) * (g.random((B, ny, nx)) < 0.2)).astype(np.float32)
+    y = (np.roll(s0, 1, axis=2) * 1.2 + 0.02 * g.normal(size=(B, ny, nx))).astype(np.float32)
+    return y, s0
+
+
+def _cmp(name, g, r, scale, tol=1e-3):
+    e = np.abs(g - r).max() / scale
+    assert e <= tol, (name, e)
+
+
+@pytest.mark.parametrize("persist", ["0", "1"])
+@pytest.mark.parametrize("inner", [1, 3])
+@pytest.mark.parametrize("shape", [(1, 16, 16), (2, 33, 64), (1, 64, 130)])
+def test_df_parity(monkeypatch, shape, inner, persist):
+    monkeypatch.setenv("UOT_PERSIST", persist)
+    B, ny, nx = shape
+    y, s0 = _problem(B, ny, nx, seed=nx + inner)
+    mu, kappa, rho = 0.8, 0.5, 1.0
+    t = oracle.default_steps(nx, ny, prox=True, fix_first=True, safety=0.95)[0]
+    n = 60
+    dfp = DFProblem(torch.from_numpy(y).cuda(), torch.from_numpy(s0).cuda(), mu, kappa, rho, tau1=t, tau2=t,
+                    inner_iters=inner)
+    rep = dfp.solve(n, eps=0.0, check_every=n)
+    st, res = oracle.df_admm(y, s0, mu, kappa, rho, t, t, n, inner_iters=inner)
+    scale = max(np.abs(y).max(), np.abs(s0).max())
+    for k in ("s", "x", "a", "b"):
+        _cmp(k, getattr(dfp, k).double().cpu().numpy(), st[k], scale)
+    inn = dfp.inner_state()
+    for k, ok in (("mx", "mx"), ("my", "my"), ("r", "r"), ("ain", "ain"), ("z", "z")):
+        _cmp(k, inn[k].double().cpu().numpy(), st[ok], max(scale, np.abs(st[ok]).max()))
+    assert rep["primal_res"] == pytest.approx(res[-1, 0], rel=2e-3, abs=1e-6)
+    assert rep["dual_res"] == pytest.approx(res[-1, 1], rel=2e-3, abs=1e-6)
+    assert rep["data_term"] == pytest.approx(0.5 * ((y - st["s"]) ** 2).sum(), rel=1e-4)
+    assert rep["iterations"] == n
+
+
+def test_df_device_stop_matches_oracle_residuals():
+    """eps = 1e-3: the device stops at the first checked iteration where both
+    residuals are below eps; the oracle run to that count satisfies the same test."""
+    y, s0 = _problem(1, 32, 32, seed=3)
+    t = oracle.default_steps(32, 32, prox=True, fix_first=True, safety=0.95)[0]
+    dfp = DFProblem(torch.from_numpy(y).cuda(), torch.from_numpy(s0).cuda(), 0.8, 0.5, 1.0, tau1=t, tau2=t)
+    rep = dfp.solve(5000, eps=1e-3, check_every=5)
+    assert rep["converged"] == 1 and rep["status"] == 0
+    kc = rep["iterations"]
+    st, res = oracle.df_admm(y, s0, 0.8, 0.5, 1.0, t, t, kc)
+    assert res[-1, 0] < 1.05e-3 and res[-1, 1] < 1.05e-3
+    np.testing.assert_allclose(dfp.s.double().cpu().numpy(), st["s"], atol=2e-3 * max(y.max(), 1))
