@@ -234,6 +234,47 @@ struct Geometry {
     int vec, strips, segs, H, items;
 };
 
+// Host-side early exit for device-side stopping: after every chunk of launches the
+// stop flag is copied (async) to pinned host memory with an event; before
+// enqueueing chunk k+2 the host waits for chunk k's event and stops enqueueing if
+// the flag was set.  The GPU always has the next chunk queued.
+struct StopPoller {
+    int* h = nullptr;                 // pinned [2]
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    bool pending[2] = {false, false};
+    int chunk = 0;
+    bool init() {
+        if (h) return true;
+        if (cudaHostAlloc(&h, 2 * sizeof(int), cudaHostAllocDefault) != cudaSuccess) { h = nullptr; return false; }
+        for (int q = 0; q < 2; ++q)
+            if (cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming) != cudaSuccess) return false;
+        return true;
+    }
+    void begin() { pending[0] = pending[1] = false; chunk = 0; }
+    // after a chunk: snapshot the flag
+    void post(const int* dstop, cudaStream_t s) {
+        const int q = chunk & 1;
+        cudaMemcpyAsync(&h[q], dstop, sizeof(int), cudaMemcpyDeviceToHost, s);
+        cudaEventRecord(ev[q], s);
+        pending[q] = true;
+        ++chunk;
+    }
+    // before the next chunk: true if the device already stopped (checks the older snapshot)
+    bool stopped() {
+        const int q = chunk & 1;           // the slot about to be reused = two chunks ago
+        if (!pending[q]) return false;
+        cudaEventSynchronize(ev[q]);
+        pending[q] = false;
+        return h[q] != 0;
+    }
+    void release() {
+        for (int q = 0; q < 2; ++q) if (ev[q]) cudaEventDestroy(ev[q]);
+        if (h) cudaFreeHost(h);
+        h = nullptr;
+    }
+};
+static const int kPollChunk = 128;
+
 struct uot_ctx {
     uot_params p;
     uot_buffers b;
@@ -257,6 +298,7 @@ struct uot_ctx {
     int* pflags;        // [kMaxPersistCtas] + barrier[2]
     struct { bool ok; int TW, TH, tx, ty, ctas, threads; size_t smem; } pg;
     int64_t persist_launches;
+    StopPoller poll;
     int r_mode;          // 0 l1, 1 l2 (p = 2), 2 balanced
     float r_scale;
     int fix_first;
@@ -693,7 +735,16 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
 
 static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
     if (c->pg.ok && n >= 2) return launch_persist(c, n, reduce_every, reduce_last, stop, tol);
+    const bool poll = stop != nullptr && n > 2 * kPollChunk && c->poll.init();
+    if (poll) c->poll.begin();
     for (int k = 0; k < n; ++k) {
+        if (poll && k > 0 && k % kPollChunk == 0) {
+            c->poll.post(stop, c->s);
+            if (c->poll.stopped()) {            // the device stopped >= one chunk ago: skip the rest
+                c->iter += n - k;               // uot_get_report corrects the count from the device
+                return UOT_OK;
+            }
+        }
         const bool red = (reduce_last && k == n - 1) || (reduce_every > 0 && ((k + 1) % reduce_every == 0));
         int rc = launch_one(c, UOT_PART_ALL, red, stop, tol);
         if (rc) return rc;
@@ -885,6 +936,7 @@ int64_t uot_launch_count(const uot_ctx* c) { return c ? c->launches : -1; }
 
 void uot_destroy(uot_ctx* c) {
     if (!c) return;
+    c->poll.release();
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     delete c;
 }
