@@ -196,3 +196,56 @@ def uot_df_1d_qp(y, s0, kappa, mu):
         if best is None or res.fun < best.fun:
             best = res
     return float(best.fun), unpack(best.x)[0]
+
+
+def rpca_pair_1d_qp(y0, y1, lam, kappa, mu):
+    """Exact optimum of eq:RPCA_UOTDF on a 1 x n grid with T = 2, Phi = I and
+    the low-rank part absent (L = 0, the gamma -> infinity limit):
+        min_{s0, s1 >= 0} 1/2||y0 - s0||^2 + 1/2||y1 - s1||^2 + lam (|s0|_1 + |s1|_1)
+                          + kappa V_mu(s0, s1),
+    one QP in (s0, s1, M+, M-, r+, r-) >= 0 with the Beckmann constraint
+    M_i - M_{i-1} - r_i = s1_i - s0_i (L1), solved by scipy SLSQP (independent of
+    Algorithms 1 and 3).  Returns (value, s0, s1)."""
+    from scipy.optimize import minimize
+    y0, y1 = np.asarray(y0, float), np.asarray(y1, float)
+    n = y0.size
+    m = n - 1
+    o_m = 2 * n
+    o_r = 2 * n + 2 * m
+    nv = o_r + 2 * n
+
+    def obj(v):
+        s0, s1 = v[:n], v[n:2 * n]
+        return (0.5 * ((y0 - s0) ** 2).sum() + 0.5 * ((y1 - s1) ** 2).sum() + lam * (s0.sum() + s1.sum())
+                + kappa * (v[o_m:o_r].sum() + mu * v[o_r:].sum()))
+
+    def grad(v):
+        g = np.empty(nv)
+        g[:n] = v[:n] - y0 + lam
+        g[n:2 * n] = v[n:2 * n] - y1 + lam
+        g[o_m:o_r] = kappa
+        g[o_r:] = kappa * mu
+        return g
+
+    A = np.zeros((n, nv))
+    for i in range(n):
+        A[i, i] = 1.0                                                # + s0_i
+        A[i, n + i] = -1.0                                           # - s1_i
+        if i < m:
+            A[i, o_m + i] += 1.0; A[i, o_m + m + i] -= 1.0           # + M_i
+        if i >= 1:
+            A[i, o_m + i - 1] -= 1.0; A[i, o_m + m + i - 1] += 1.0   # - M_{i-1}
+        A[i, o_r + i] -= 1.0; A[i, o_r + n + i] += 1.0               # - r_i
+    cons = {"type": "eq", "fun": lambda v: A @ v, "jac": lambda v: A}
+    best = None
+    for s0i, s1i in ((np.maximum(y0 - lam, 0), np.maximum(y1 - lam, 0)), (np.zeros(n), np.zeros(n))):
+        x0 = np.concatenate([s0i, s1i, np.zeros(2 * m + 2 * n)])
+        # start feasible: r = s0 - s1 (pure creation / destruction)
+        d = s1i - s0i
+        x0[o_r:o_r + n] = np.maximum(-d, 0)
+        x0[o_r + n:] = np.maximum(d, 0)
+        res = minimize(obj, x0, jac=grad, constraints=[cons], bounds=[(0, None)] * nv, method="SLSQP",
+                       options={"ftol": 1e-15, "maxiter": 3000})
+        if best is None or res.fun < best.fun:
+            best = res
+    return float(best.fun), best.x[:n].copy(), best.x[n:2 * n].copy()
