@@ -265,6 +265,85 @@ int64_t uot_df_launch_count(const uot_df_ctx* ctx);
 void uot_df_destroy(uot_df_ctx* ctx);
 const char* uot_df_last_error(const uot_df_ctx* ctx);
 
+/* ===========================================================================
+ * RPCA+UOT-DF ADMM: Algorithm 3 for
+ * eq:RPCA_UOTDF on one video of T frames y_t (ny x nx):
+ *   min_{S, L >= 0} 1/2 sum_t ||y_t - Phi_t(s_t + l_t)||^2 + lambda ||S||_1
+ *                   + gamma ||L||_* + kappa sum_{t<T-1} V_mu(s_t, s_{t+1})
+ * with Phi_t DIAGONAL (per-pixel weights phi_t >= 0, e.g. masks; NULL = I),
+ * the O(TN) case of P:861-862.  Per ADMM iteration, in the paper's order:
+ *   lines 5-9 + 12 : one pointwise kernel: s (one-sided shrink, L25), L, x
+ *                    (rho restored, L26), A <- A + X - S - L (L27), and the
+ *                    prox centres (s_t - b_t, s_{t+1} - c_{t+1}) of line 11
+ *   line 10        : T <- svt_{gamma/rho}(L + D) by the Gram route: G = M^T M
+ *                    (fp64, M = L + D is N x T), eigen-decomposition of the
+ *                    T x T matrix G by a warm-started parallel Jacobi solver in
+ *                    one CTA, W = V diag(max(1 - tau/sqrt(lambda), 0)) V^T,
+ *                    T = M W; fused with line 13 (D <- D + L - T)
+ *   line 11        : inner_iters warm-started iterations of Algorithm 1 on the
+ *                    T-1 independent pair proxes (weight rho/kappa, L2)
+ *   lines 14-15    : b_t <- b_t + z_t - s_t, c_{t+1} <- c_{t+1} + w_{t+1} - s_{t+1}
+ * Residuals (L28): primal ||[X-S-L; L-T; z-s; w-s]||, dual rho||[dX; dT; dz; dw]||;
+ * stop when both < eps, tested on the device every check_every iterations.
+ * Limits: 2 <= T <= UOT_RPCA_MAX_T.
+ * ======================================================================== */
+#define UOT_RPCA_MAX_T 128
+typedef struct uot_rpca_ctx uot_rpca_ctx;
+
+typedef struct {
+    int32_t  nx, ny, n_frames;     /* grid and T                                                */
+    double   lambda, gamma;        /* sparsity and low-rank weights, > 0             */
+    double   kappa, mu;            /* OT weight kappa > 0 and unbalance weight mu > 0 (or +inf)  */
+    double   rho;                  /* ADMM penalty > 0                                           */
+    double   tau1, tau2;           /* inner Alg.1 steps; 0 = Theorem-1 default (pair prox)       */
+    int32_t  inner_iters;          /* Alg.1 iterations per ADMM iteration, >= 1      */
+    uint32_t flags;                /* UOT_RESIDUAL_L2, UOT_FORCE_STEPS                           */
+} uot_rpca_params;
+
+typedef struct {                   /* caller-owned device buffers, fp32, 16-B aligned           */
+    const float* y;                /* [T][ny][nx] observations                                   */
+    const float* phi;              /* [T][ny][nx] diagonal of Phi_t, or NULL (Phi = I)            */
+    float *S, *L, *X, *Tm, *A, *D; /* [T][ny][nx] ADMM state (Tm = the paper's T)                */
+    float* pc;                     /* [T-1][2][ny][nx] prox centres (inner frames)               */
+    float* zw[2];                  /* [T-1][2][ny][nx] (z_t, w_{t+1}) = inner x, ping-pong       */
+    float* bc;                     /* [T-1][2][ny][nx] (b_t, c_{t+1})                            */
+    float* zprev;                  /* [T-1][2][ny][nx] scratch (inner_iters > 1 only, else NULL) */
+    float* mx[2]; float* my[2];    /* [T-1][ny][nx] inner flux, ping-pong                        */
+    float* r;                      /* [T-1][ny][nx] inner residual                               */
+    float* ain[2];                 /* [T-1][ny][nx] inner dual, ping-pong                        */
+    double* scratch;               /* uot_rpca_scratch_doubles(&params) doubles                  */
+} uot_rpca_buffers;
+
+typedef struct {
+    double primal_res, dual_res;   /* L28                                                        */
+    double data_term;              /* 1/2 sum ||y - Phi(s + l)||^2                               */
+    double l1_term;                /* lambda ||S||_1                                             */
+    double nuclear;                /* ||T||_* after line 10 (from the eigenvalues)               */
+    double transport, growth;      /* inner ||M||_{2,1}, mu ||r||_p^p summed over pairs          */
+    double objective;              /* data + l1 + gamma nuclear + kappa (transport + growth)     */
+    int64_t iterations;            /* ADMM iterations since uot_rpca_reset                      */
+    int32_t converged, nonfinite;
+    int32_t jacobi_sweeps;         /* sweeps of the last eigen-decomposition                     */
+} uot_rpca_report;
+
+size_t uot_rpca_scratch_doubles(const uot_rpca_params* params);
+/* Validates params/buffers (UOT_E_INVALID) and builds the inner Alg.1 context. */
+int uot_rpca_create(const uot_rpca_params* params, const uot_rpca_buffers* buffers, void* cuda_stream,
+                    uot_rpca_ctx** out);
+/* Cold start (Alg.3 line 2: every variable 0; inner states 0; no eigenvector warm start). Async. */
+int uot_rpca_reset(uot_rpca_ctx* ctx);
+/* Up to max_iters ADMM iterations; eps <= 0 runs exactly max_iters.  Fills *out (may be NULL;
+ * then the call is fully asynchronous).  Returns UOT_OK, UOT_E_NOT_CONVERGED, UOT_E_NONFINITE, ... */
+int uot_rpca_solve(uot_rpca_ctx* ctx, int32_t max_iters, double eps, int32_t check_every, uot_rpca_report* out);
+/* Per-launch CUDA-event timing of the line-1..15 kernels (summed ms, launches), as uot_set_timing. */
+int uot_rpca_set_timing(uot_rpca_ctx* ctx, int enable);
+int uot_rpca_get_timing(uot_rpca_ctx* ctx, double* ms_by_kernel /*[6]: pre, gram, eig, apply, prox, post*/,
+                        int64_t* n_iters);
+int uot_rpca_state_slot(const uot_rpca_ctx* ctx);   /* ping-pong slot of zw/mx/my/ain holding the iterate */
+int64_t uot_rpca_launch_count(const uot_rpca_ctx* ctx);
+void uot_rpca_destroy(uot_rpca_ctx* ctx);
+const char* uot_rpca_last_error(const uot_rpca_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,7 +28,11 @@ EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset
             "uot_state_slot", "uot_launch_count",
             "uot_destroy", "uot_last_error",
             "uot_df_scratch_doubles", "uot_df_create", "uot_df_reset", "uot_df_solve", "uot_df_set_timing",
-            "uot_df_get_timing", "uot_df_launch_count", "uot_df_destroy", "uot_df_last_error")
+            "uot_df_get_timing", "uot_df_launch_count", "uot_df_destroy", "uot_df_last_error",
+            "uot_rpca_scratch_doubles", "uot_rpca_create", "uot_rpca_reset", "uot_rpca_solve",
+            "uot_rpca_set_timing", "uot_rpca_get_timing", "uot_rpca_state_slot", "uot_rpca_launch_count",
+            "uot_rpca_destroy", "uot_rpca_last_error")
+UOT_RPCA_MAX_T = 128
 
 
 class Params(ctypes.Structure):
@@ -73,6 +77,29 @@ class DfReport(ctypes.Structure):
     _fields_ = [("primal_res", ctypes.c_double), ("dual_res", ctypes.c_double), ("data_term", ctypes.c_double),
                 ("transport", ctypes.c_double), ("growth", ctypes.c_double), ("objective", ctypes.c_double),
                 ("iterations", ctypes.c_int64), ("converged", ctypes.c_int32), ("nonfinite", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class RpcaParams(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("n_frames", ctypes.c_int32),
+                ("lam", ctypes.c_double), ("gamma", ctypes.c_double), ("kappa", ctypes.c_double),
+                ("mu", ctypes.c_double), ("rho", ctypes.c_double), ("tau1", ctypes.c_double),
+                ("tau2", ctypes.c_double), ("inner_iters", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+
+
+class RpcaBuffers(ctypes.Structure):
+    _fields_ = [("y", _fp), ("phi", _fp), ("S", _fp), ("L", _fp), ("X", _fp), ("Tm", _fp), ("A", _fp), ("D", _fp),
+                ("pc", _fp), ("zw", _fp * 2), ("bc", _fp), ("zprev", _fp), ("mx", _fp * 2), ("my", _fp * 2),
+                ("r", _fp), ("ain", _fp * 2), ("scratch", _fp)]
+
+
+class RpcaReport(ctypes.Structure):
+    _fields_ = [("primal_res", ctypes.c_double), ("dual_res", ctypes.c_double), ("data_term", ctypes.c_double),
+                ("l1_term", ctypes.c_double), ("nuclear", ctypes.c_double), ("transport", ctypes.c_double),
+                ("growth", ctypes.c_double), ("objective", ctypes.c_double), ("iterations", ctypes.c_int64),
+                ("converged", ctypes.c_int32), ("nonfinite", ctypes.c_int32), ("jacobi_sweeps", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -133,12 +160,26 @@ def lib():
     L.uot_df_launch_count.argtypes = [ctypes.c_void_p]; L.uot_df_launch_count.restype = ctypes.c_int64
     L.uot_df_destroy.argtypes = [ctypes.c_void_p]; L.uot_df_destroy.restype = None
     L.uot_df_last_error.argtypes = [ctypes.c_void_p]; L.uot_df_last_error.restype = ctypes.c_char_p
+    RP, RB, RR = ctypes.POINTER(RpcaParams), ctypes.POINTER(RpcaBuffers), ctypes.POINTER(RpcaReport)
+    L.uot_rpca_scratch_doubles.argtypes = [RP]; L.uot_rpca_scratch_doubles.restype = ctypes.c_size_t
+    L.uot_rpca_create.argtypes = [RP, RB, ctypes.c_void_p, ctx_pp]; L.uot_rpca_create.restype = ctypes.c_int
+    L.uot_rpca_reset.argtypes = [ctypes.c_void_p]; L.uot_rpca_reset.restype = ctypes.c_int
+    L.uot_rpca_solve.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, RR]
+    L.uot_rpca_solve.restype = ctypes.c_int
+    L.uot_rpca_set_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]; L.uot_rpca_set_timing.restype = ctypes.c_int
+    L.uot_rpca_get_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+    L.uot_rpca_get_timing.restype = ctypes.c_int
+    L.uot_rpca_state_slot.argtypes = [ctypes.c_void_p]; L.uot_rpca_state_slot.restype = ctypes.c_int
+    L.uot_rpca_launch_count.argtypes = [ctypes.c_void_p]; L.uot_rpca_launch_count.restype = ctypes.c_int64
+    L.uot_rpca_destroy.argtypes = [ctypes.c_void_p]; L.uot_rpca_destroy.restype = None
+    L.uot_rpca_last_error.argtypes = [ctypes.c_void_p]; L.uot_rpca_last_error.restype = ctypes.c_char_p
     _lib = L
     return L
 
 
-def check(rc, ctx=None, allow=(), df=False):
+def check(rc, ctx=None, allow=(), df=False, rpca=False):
     if rc == UOT_OK or rc in allow:
         return rc
-    msg = (lib().uot_df_last_error if df else lib().uot_last_error)(ctx)
+    fn = lib().uot_rpca_last_error if rpca else (lib().uot_df_last_error if df else lib().uot_last_error)
+    msg = fn(ctx)
     raise UotError(rc, msg.decode() if msg else "")

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libuot_b200.so")
 SOURCES = [os.path.join(CSRC, "uot_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, n) for n in os.listdir(CSRC) if n.endswith((".cuh", ".h"))] + \
+DEPS = SOURCES + [os.path.join(CSRC, n) for n in os.listdir(CSRC) if n.endswith((".cuh", ".h", ".inc"))] + \
     [os.path.join(ROOT, "include", "uot.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -947,3 +947,4 @@ const char* uot_last_error(const uot_ctx* c) { return c ? c->err : g_err; }
 
 // UOT-DF ADMM (Algorithm 2) on top of the kernels above
 #include "uot_df.inc"
+#include "uot_rpca.inc"

@@ -272,6 +272,38 @@ def gen_two_delta(ny: int, nx: int, p_at, q_at, m_p: float = 1.0, m_q: float = 1
     return f
 
 
+# ------------------------------------------------------------------------------- Algorithm 3 (RPCA)
+def gen_rpca(T: int, ny: int, nx: int, seed: int, K: int = 5, R: int = 1, noise: float = 0.001,
+             observed: float = 0.6, mass_rate: float = 1.0):
+    """Synthetic RPCA+UOT-DF instance after the paper's protocol with a
+    DIAGONAL Phi stand-in (dense Gaussian Phi is out of scope):
+    K targets of intensity U[0.5,1.5] in s_1, each moving by a random step in
+    {-1,0,1}^2 per frame (bouncing) with intensity drift U[-mass_rate,mass_rate]*0.1 per
+    frame clipped to [0.5,1.5]; L = U V^T/(4R), U, V entries U(0,1); Phi_t =
+    diag(m_t) with m_t a Bernoulli(observed) mask (observed = the compression ratio M/N,
+    P:957); y_t = Phi_t(s_t + l_t) + N(0, noise^2).  Returns (Y, phi, S, L) float32
+    [T][ny][nx]."""
+    g = _rng(seed, 77, T, ny, nx)
+    S = np.zeros((T, ny, nx))
+    pos = np.stack([g.integers(0, ny, K), g.integers(0, nx, K)], axis=1)
+    amp = g.uniform(0.5, 1.5, K)
+    for t in range(T):
+        for k in range(K):
+            S[t, pos[k, 0], pos[k, 1]] += amp[k]
+        pos = pos + g.integers(-1, 2, (K, 2))
+        pos[:, 0] = np.abs(pos[:, 0]) % (2 * ny)
+        pos[:, 0] = np.where(pos[:, 0] >= ny, 2 * ny - 1 - pos[:, 0], pos[:, 0])
+        pos[:, 1] = np.abs(pos[:, 1]) % (2 * nx)
+        pos[:, 1] = np.where(pos[:, 1] >= nx, 2 * nx - 1 - pos[:, 1], pos[:, 1])
+        amp = np.clip(amp + 0.1 * mass_rate * g.uniform(-1, 1, K), 0.5, 1.5)
+    U, V = g.uniform(0, 1, (ny * nx, R)), g.uniform(0, 1, (T, R))
+    L = ((U @ V.T) / (4 * R)).T.reshape(T, ny, nx)
+    phi = (g.random((T, ny, nx)) < observed).astype(np.float64)
+    Y = phi * (S + L) + noise * g.normal(size=(T, ny, nx))
+    f = lambda a: a.astype(np.float32)
+    return f(Y), f(phi), f(S), f(L)
+
+
 def generate(name: str, **kw) -> np.ndarray:
     """Frames [B][T][ny][nx] float32 of config `name` (C5: 8 pairs by default)."""
     if name == "C1":

@@ -14,9 +14,10 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import Buffers, DfBuffers, DfParams, DfReport, Params, Report, check, lib
+from ._lib import (Buffers, DfBuffers, DfParams, DfReport, Params, Report, RpcaBuffers, RpcaParams, RpcaReport,
+                   check, lib)
 
-__all__ = ["Problem", "DFProblem", "default_steps", "scratch_doubles", "Report"]
+__all__ = ["Problem", "DFProblem", "RPCAProblem", "default_steps", "scratch_doubles", "Report"]
 
 
 def _params(nx, ny, B, T, alpha, rho, tau1, tau2, flags=0) -> Params:
@@ -309,6 +310,129 @@ class DFProblem:
     def close(self):
         if getattr(self, "_ctx", None):
             lib().uot_df_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class RPCAProblem:
+    """RPCA+UOT-DF ADMM (Algorithm 3) on one video Y [T][ny][nx]:
+    min_{S, L >= 0} 1/2 sum_t ||y_t - Phi_t(s_t + l_t)||^2 + lambda||S||_1 + gamma||L||_*
+                    + kappa sum_t V_mu(s_t, s_{t+1})          (eq:RPCA_UOTDF)
+    with diagonal Phi (``phi`` [T][ny][nx] per-pixel weights, None = identity).
+
+    Every line of Algorithm 3 (including the SVT of line 10) runs in libuot_b200.so;
+    this class only allocates the torch buffers and marshals pointers."""
+
+    STATE = ("S", "L", "X", "Tm", "A", "D")
+
+    def __init__(self, Y: torch.Tensor, lam: float, gamma: float, kappa: float, mu: float, rho: float = 1.0,
+                 phi: torch.Tensor | None = None, tau1: float | None = None, tau2: float | None = None,
+                 inner_iters: int = 1, p_norm: int = 1, *, stream: torch.cuda.Stream | None = None,
+                 reset: bool = True):
+        if Y.dim() != 3:
+            raise ValueError("Y must be [T][ny][nx]")
+        if not Y.is_cuda or Y.dtype != torch.float32:
+            raise ValueError("Y must be a float32 CUDA tensor")
+        if phi is not None and (phi.shape != Y.shape or not phi.is_cuda or phi.dtype != torch.float32):
+            raise ValueError("phi must be a float32 CUDA tensor shaped like Y")
+        self.Y = Y.contiguous()
+        self.phi = phi.contiguous() if phi is not None else None
+        T, ny, nx = self.Y.shape
+        self.T, self.ny, self.nx = T, ny, nx
+        P = T - 1
+        dev = self.Y.device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        e = lambda *shape: torch.zeros(shape, dtype=torch.float32, device=dev)
+        for k in self.STATE:
+            setattr(self, k, e(T, ny, nx))
+        self.pc, self.bc = e(P, 2, ny, nx), e(P, 2, ny, nx)
+        self.zw = [e(P, 2, ny, nx), e(P, 2, ny, nx)]
+        self.zprev = e(P, 2, ny, nx) if inner_iters > 1 else None
+        self.mx, self.my, self.ain = [e(P, ny, nx), e(P, ny, nx)], [e(P, ny, nx), e(P, ny, nx)], [e(P, ny, nx), e(P, ny, nx)]
+        self.r = e(P, ny, nx)
+        flags = _lib.UOT_RESIDUAL_L2 if p_norm == 2 else 0
+        self._p = RpcaParams(nx, ny, T, float(lam), float(gamma), float(kappa), float(mu), float(rho),
+                             float(tau1 or 0.0), float(tau2 or 0.0), int(inner_iters), flags)
+        nsc = int(lib().uot_rpca_scratch_doubles(ctypes.byref(self._p)))
+        if nsc == 0:
+            raise ValueError(f"unsupported shape (2 <= T <= {_lib.UOT_RPCA_MAX_T})")
+        self.scratch = torch.zeros(nsc, dtype=torch.float64, device=dev)
+        bf = RpcaBuffers()
+        bf.y = self.Y.data_ptr()
+        bf.phi = self.phi.data_ptr() if self.phi is not None else None
+        for k in self.STATE:
+            setattr(bf, k, getattr(self, k).data_ptr())
+        bf.pc, bf.bc = self.pc.data_ptr(), self.bc.data_ptr()
+        bf.zprev = self.zprev.data_ptr() if self.zprev is not None else None
+        for k in range(2):
+            bf.zw[k] = self.zw[k].data_ptr()
+            bf.mx[k] = self.mx[k].data_ptr()
+            bf.my[k] = self.my[k].data_ptr()
+            bf.ain[k] = self.ain[k].data_ptr()
+        bf.r = self.r.data_ptr()
+        bf.scratch = self.scratch.data_ptr()
+        self._bufs = bf
+        ctx = ctypes.c_void_p()
+        check(lib().uot_rpca_create(ctypes.byref(self._p), ctypes.byref(bf), ctypes.c_void_p(self.stream.cuda_stream),
+                                    ctypes.byref(ctx)), None, rpca=True)
+        self._ctx = ctx
+        self.iterations = 0
+        if reset:
+            self.reset()
+
+    def reset(self):
+        check(lib().uot_rpca_reset(self._ctx), self._ctx, rpca=True)
+        self.iterations = 0
+
+    def solve(self, max_iters: int, eps: float = 0.0, check_every: int = 10, report: bool = True):
+        """Up to max_iters ADMM iterations (eps <= 0: exactly max_iters).  report=False keeps
+        the call asynchronous (no host synchronisation)."""
+        if not report:
+            check(lib().uot_rpca_solve(self._ctx, int(max_iters), float(eps), int(check_every), None),
+                  self._ctx, rpca=True)
+            self.iterations += int(max_iters)
+            return None
+        rep = RpcaReport()
+        rc = check(lib().uot_rpca_solve(self._ctx, int(max_iters), float(eps), int(check_every), ctypes.byref(rep)),
+                   self._ctx, allow=(_lib.UOT_E_NOT_CONVERGED,), rpca=True)
+        d = rep.as_dict()
+        d["status"] = rc
+        self.iterations = d["iterations"]
+        return d
+
+    def state(self) -> dict:
+        """Current iterate: S, L, X, Tm, A, D [T][ny][nx]; Z, W, Bd, Cd [T-1][ny][nx] (z_t, w_{t+1},
+        b_t, c_{t+1} at index t, the oracle's layout); inner mx, my, r, ain."""
+        s = int(lib().uot_rpca_state_slot(self._ctx))
+        d = {k: getattr(self, k) for k in self.STATE}
+        d.update(Z=self.zw[s][:, 0], W=self.zw[s][:, 1], Bd=self.bc[:, 0], Cd=self.bc[:, 1],
+                 mx=self.mx[s], my=self.my[s], r=self.r, ain=self.ain[s])
+        return d
+
+    def set_timing(self, enable=True):
+        check(lib().uot_rpca_set_timing(self._ctx, int(bool(enable))), self._ctx, rpca=True)
+
+    STAGES = ("pre", "gram", "eig", "apply", "prox", "post")
+
+    def get_timing(self):
+        """({stage: summed ms}, timed iterations) since set_timing."""
+        ms = (ctypes.c_double * 6)()
+        n = ctypes.c_int64()
+        check(lib().uot_rpca_get_timing(self._ctx, ms, ctypes.byref(n)), self._ctx, rpca=True)
+        return dict(zip(self.STAGES, list(ms))), n.value
+
+    @property
+    def launches(self) -> int:
+        return int(lib().uot_rpca_launch_count(self._ctx))
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().uot_rpca_destroy(self._ctx)
             self._ctx = None
 
     def __del__(self):
