@@ -101,6 +101,20 @@ def test_rpca_parity_fixed_iterations(T, ny, nx, n, inner, persist, masked):
     assert prob.launches > 6 * n // 2
 
 
+def test_rpca_parity_growth_term_active():
+    """Small mu (0.2 < the 1-px transport cost): the inner prox creates/destroys mass (r != 0),
+    exercising the l1 soft threshold of the growth term inside Algorithm 3."""
+    from paper_1909_00149_b200 import inputs
+    prm = dict(PRM, mu=0.2, kappa=1.0)
+    Y, phi, _, _ = inputs.gen_rpca(6, 20, 24, seed=11, K=6, observed=0.8)
+    prob, rep, st_g = _gpu(Y, phi, prm, 30)
+    st_o, res, nuc = _oracle(Y, phi, prm, 30)
+    _compare(Y, st_g, st_o)
+    assert np.abs(st_o["r"]).sum() > 1e-3
+    obj = _oracle_objective(Y.astype(np.float64), phi, st_o, nuc[-1], prm)
+    assert rep["objective"] == pytest.approx(obj, rel=1e-4)
+
+
 def test_rpca_converges_to_oracle_limit():
     """Converged comparison on the R5 KKT instance: the device-side stopping test fires and
     the fp32 limit matches the fp64 limit (pinned by the KKT conditions, R5)."""
