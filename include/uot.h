@@ -288,6 +288,12 @@ const char* uot_df_last_error(const uot_df_ctx* ctx);
  * Limits: 2 <= T <= UOT_RPCA_MAX_T.
  * ======================================================================== */
 #define UOT_RPCA_MAX_T 128
+/* Signed split eq:RPCA_UOTDF_PN: S = S+ - S-, S+/- >= 0,
+ * each with its own l1 term and its own chain of UOT terms (reading L30: the split of
+ * Algorithm 3 extended with z+/-, w+/-, b+/-, c+/-; s+ and s- updated jointly, exactly, per
+ * pixel).  buffers.S holds S+, buffers.Sm S-; every per-pair buffer then has 2(T-1) pairs:
+ * the S+ chain's T-1 pairs first, then the S- chain's. */
+#define UOT_RPCA_SIGNED 8u
 typedef struct uot_rpca_ctx uot_rpca_ctx;
 
 typedef struct {
@@ -297,27 +303,29 @@ typedef struct {
     double   rho;                  /* ADMM penalty > 0                                           */
     double   tau1, tau2;           /* inner Alg.1 steps; 0 = Theorem-1 default (pair prox)       */
     int32_t  inner_iters;          /* Alg.1 iterations per ADMM iteration, >= 1      */
-    uint32_t flags;                /* UOT_RESIDUAL_L2, UOT_FORCE_STEPS                           */
+    uint32_t flags;                /* UOT_RESIDUAL_L2, UOT_FORCE_STEPS, UOT_RPCA_SIGNED          */
 } uot_rpca_params;
 
 typedef struct {                   /* caller-owned device buffers, fp32, 16-B aligned           */
     const float* y;                /* [T][ny][nx] observations                                   */
     const float* phi;              /* [T][ny][nx] diagonal of Phi_t, or NULL (Phi = I)            */
-    float *S, *L, *X, *Tm, *A, *D; /* [T][ny][nx] ADMM state (Tm = the paper's T)                */
-    float* pc;                     /* [T-1][2][ny][nx] prox centres (inner frames)               */
-    float* zw[2];                  /* [T-1][2][ny][nx] (z_t, w_{t+1}) = inner x, ping-pong       */
-    float* bc;                     /* [T-1][2][ny][nx] (b_t, c_{t+1})                            */
-    float* zprev;                  /* [T-1][2][ny][nx] scratch (inner_iters > 1 only, else NULL) */
-    float* mx[2]; float* my[2];    /* [T-1][ny][nx] inner flux, ping-pong                        */
-    float* r;                      /* [T-1][ny][nx] inner residual                               */
-    float* ain[2];                 /* [T-1][ny][nx] inner dual, ping-pong                        */
+    float *S, *L, *X, *Tm, *A, *D; /* [T][ny][nx] ADMM state (Tm = the paper's T; S = S+ if signed) */
+    float* Sm;                     /* [T][ny][nx] S- (UOT_RPCA_SIGNED only, else NULL)           */
+    /* per-pair buffers: Q = T-1 pairs, or 2(T-1) with UOT_RPCA_SIGNED                           */
+    float* pc;                     /* [Q][2][ny][nx] prox centres (inner frames)                 */
+    float* zw[2];                  /* [Q][2][ny][nx] (z_t, w_{t+1}) = inner x, ping-pong         */
+    float* bc;                     /* [Q][2][ny][nx] (b_t, c_{t+1})                              */
+    float* zprev;                  /* [Q][2][ny][nx] scratch (inner_iters > 1 only, else NULL)   */
+    float* mx[2]; float* my[2];    /* [Q][ny][nx] inner flux, ping-pong                          */
+    float* r;                      /* [Q][ny][nx] inner residual                                 */
+    float* ain[2];                 /* [Q][ny][nx] inner dual, ping-pong                          */
     double* scratch;               /* uot_rpca_scratch_doubles(&params) doubles                  */
 } uot_rpca_buffers;
 
 typedef struct {
     double primal_res, dual_res;   /* L28                                                        */
     double data_term;              /* 1/2 sum ||y - Phi(s + l)||^2                               */
-    double l1_term;                /* lambda ||S||_1                                             */
+    double l1_term;                /* lambda ||S||_1 (signed: lambda (||S+||_1 + ||S-||_1))       */
     double nuclear;                /* ||T||_* after line 10 (from the eigenvalues)               */
     double transport, growth;      /* inner ||M||_{2,1}, mu ||r||_p^p summed over pairs          */
     double objective;              /* data + l1 + gamma nuclear + kappa (transport + growth)     */

@@ -147,3 +147,110 @@ def admm(Y, lam, gamma, kappa, mu, rho, tau1, tau2, n_outer, inner_iters=1, phi=
             raise FloatingPointError("non-finite iterate")
     st.update(S=S, L=L, X=X, Tm=Tm, A=A, D=D, Z=Z, W=W, Bd=Bd, Cd=Cd)
     return st, res, nuc
+
+
+# ----------------------------------------------------------------------------- signed split
+SIGNED_STATE = ("Sp", "Sm", "L", "X", "Tm", "A", "D", "Zp", "Wp", "Bp", "Cp", "Zm", "Wm", "Bm", "Cm",
+                "mx", "my", "r", "ain")
+
+
+def zero_state_signed(T, ny, nx):
+    """Cold start of the signed split (eq:RPCA_UOTDF_PN): every variable 0; the
+    inner prox states cover 2(T-1) pairs (the S+ chain's pairs, then the S- chain's)."""
+    st = {k: np.zeros((T, ny, nx)) for k in ("Sp", "Sm", "L", "X", "Tm", "A", "D")}
+    for k in ("Zp", "Wp", "Bp", "Cp", "Zm", "Wm", "Bm", "Cm"):
+        st[k] = np.zeros((T - 1, ny, nx))
+    for k in ("mx", "my", "r", "ain"):
+        st[k] = np.zeros((2 * (T - 1), ny, nx))
+    return st
+
+
+def signed_s_update(u, kp, km, m, lam_rho):
+    """Exact joint minimiser over s+, s- >= 0 (reading L30) of
+        lam_rho (s+ + s-) + 1/2 (u - s+ + s-)^2 + 1/2 (m s+^2 - 2 kp s+) + 1/2 (m s-^2 - 2 km s-),
+    the s-block of the split augmented Lagrangian divided by rho (u = x - l + a; kp, km the
+    summed z + b / w + c targets of each sign; m = number of those terms, >= 1).  A strictly
+    convex quadratic on the quadrant: the minimiser is the best of the face minimisers
+    (interior stationary point, the two clipped edge minimisers, the origin)."""
+    def F(sp, sm):
+        return lam_rho * (sp + sm) + 0.5 * (u - sp + sm) ** 2 + 0.5 * (m * sp * sp - 2 * kp * sp) \
+            + 0.5 * (m * sm * sm - 2 * km * sm)
+    r1 = u + kp - lam_rho
+    r2 = -u + km - lam_rho
+    det = (1.0 + m) ** 2 - 1.0
+    ip = ((1.0 + m) * r1 + r2) / det                       # interior: [[1+m, -1], [-1, 1+m]] s = r
+    im = (r1 + (1.0 + m) * r2) / det
+    cands = [(np.maximum(r1 / (1.0 + m), 0.0), np.zeros_like(u)),      # s- = 0 edge
+             (np.zeros_like(u), np.maximum(r2 / (1.0 + m), 0.0)),      # s+ = 0 edge
+             (np.zeros_like(u), np.zeros_like(u))]
+    best_p, best_m = cands[0]
+    best = F(best_p, best_m)
+    for cp, cm in cands[1:] + [(ip, im)]:
+        ok = (cp >= 0) & (cm >= 0)
+        val = np.where(ok, F(cp, cm), np.inf)
+        take = val < best
+        best_p = np.where(take, cp, best_p)
+        best_m = np.where(take, cm, best_m)
+        best = np.where(take, val, best)
+    return best_p, best_m
+
+
+def admm_signed(Y, lam, gamma, kappa, mu, rho, tau1, tau2, n_outer, inner_iters=1, phi=None, state=None):
+    """Signed split of Algorithm 3 for eq:RPCA_UOTDF_PN: S = S+ - S-, S+/- >= 0,
+    each with its own l1 weight lambda and its own chain of UOT terms; L >= 0.  The split
+    (not printed; reading L30) extends Algorithm 3's: X = S+ - S- + L, T = L, z+/-_t = s+/-_t,
+    w+/-_{t+1} = s+/-_{t+1}; per iteration, in Algorithm 3's order:
+      s+, s- jointly (signed_s_update) with u = x - l + a and the z/w targets of each sign;
+      L = Pi_+((T - D + X - (S+ - S-) + A)/2);  x = (phi y + rho(s+ - s- + l - a))/(phi^2 + rho);
+      T = svt_{gamma/rho}(L + D);  the 2(T-1) pair proxes of the S+ and S- chains;
+      A += X - (S+ - S-) - L;  D += L - T;  b/c of each sign += z/w - s.
+    Returns (state dict, res [n_outer][2] (L28 with both signs' terms), nuc)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    T, ny, nx = Y.shape
+    if T < 2:
+        raise ValueError("Algorithm 3 needs T >= 2 frames")
+    P = T - 1
+    phi = np.ones_like(Y) if phi is None else np.asarray(phi, dtype=np.float64)
+    st = {k: np.array(v, dtype=np.float64, copy=True) for k, v in (state or zero_state_signed(T, ny, nx)).items()}
+    res = np.zeros((n_outer, 2))
+    nuc = np.zeros(n_outer)
+    wz = np.array([1.0 if t < T - 1 else 0.0 for t in range(T)])
+    ww = np.array([1.0 if t > 0 else 0.0 for t in range(T)])
+    m = (wz + ww)[:, None, None]
+    for it in range(n_outer):
+        Sp, Sm, L, X, Tm, A, D = (st[k] for k in ("Sp", "Sm", "L", "X", "Tm", "A", "D"))
+        u = X - L + A
+        kp, km = np.zeros_like(Y), np.zeros_like(Y)
+        for t in range(T):
+            if wz[t]:
+                kp[t] += st["Zp"][t] + st["Bp"][t]
+                km[t] += st["Zm"][t] + st["Bm"][t]
+            if ww[t]:
+                kp[t] += st["Wp"][t - 1] + st["Cp"][t - 1]
+                km[t] += st["Wm"][t - 1] + st["Cm"][t - 1]
+        Spn, Smn = signed_s_update(u, kp, km, m, lam / rho)
+        Sn = Spn - Smn
+        Ln = np.maximum(0.5 * (Tm - D + X - Sn + A), 0.0)
+        Xn = (phi * Y + rho * (Sn + Ln - A)) / (phi * phi + rho)
+        Tn = svt((Ln + D).reshape(T, -1).T, gamma / rho).T.reshape(T, ny, nx)
+        nuc[it] = nuclear_norm(Tn.reshape(T, -1).T)
+        centres = np.concatenate([np.stack([Spn[:-1] - st["Bp"], Spn[1:] - st["Cp"]], axis=1),
+                                  np.stack([Smn[:-1] - st["Bm"], Smn[1:] - st["Cm"]], axis=1)])   # [2P][2]
+        zw = np.concatenate([np.stack([st["Zp"], st["Wp"]], axis=1), np.stack([st["Zm"], st["Wm"]], axis=1)])
+        inner = State(st["mx"], st["my"], st["r"], st["ain"], zw)
+        inner, _ = iterate(centres, mu, rho / kappa, tau1, tau2, inner_iters, inner)
+        Zp, Wp, Zm, Wm = inner.x[:P, 0], inner.x[:P, 1], inner.x[P:, 0], inner.x[P:, 1]
+        pr = ((Xn - Sn - Ln) ** 2).sum() + ((Ln - Tn) ** 2).sum()
+        du = ((Xn - X) ** 2).sum() + ((Tn - Tm) ** 2).sum()
+        for (z, w, s_new, zo, wo) in ((Zp, Wp, Spn, st["Zp"], st["Wp"]), (Zm, Wm, Smn, st["Zm"], st["Wm"])):
+            pr += ((z - s_new[:-1]) ** 2).sum() + ((w - s_new[1:]) ** 2).sum()
+            du += ((z - zo) ** 2).sum() + ((w - wo) ** 2).sum()
+        res[it] = (math.sqrt(pr), rho * math.sqrt(du))
+        st.update(Bp=st["Bp"] + Zp - Spn[:-1], Cp=st["Cp"] + Wp - Spn[1:],
+                  Bm=st["Bm"] + Zm - Smn[:-1], Cm=st["Cm"] + Wm - Smn[1:])
+        st.update(Sp=Spn, Sm=Smn, L=Ln, X=Xn, Tm=Tn, A=A + Xn - Sn - Ln, D=D + Ln - Tn,
+                  Zp=Zp.copy(), Wp=Wp.copy(), Zm=Zm.copy(), Wm=Wm.copy(),
+                  mx=inner.mx, my=inner.my, r=inner.r, ain=inner.a)
+        if not all(np.isfinite(st[k]).all() for k in ("Sp", "Sm", "L", "X", "A", "D")):
+            raise FloatingPointError("non-finite iterate")
+    return st, res, nuc

@@ -33,6 +33,7 @@ EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset
             "uot_rpca_set_timing", "uot_rpca_get_timing", "uot_rpca_state_slot", "uot_rpca_launch_count",
             "uot_rpca_destroy", "uot_rpca_last_error")
 UOT_RPCA_MAX_T = 128
+UOT_RPCA_SIGNED = 8
 
 
 class Params(ctypes.Structure):
@@ -91,7 +92,7 @@ class RpcaParams(ctypes.Structure):
 
 class RpcaBuffers(ctypes.Structure):
     _fields_ = [("y", _fp), ("phi", _fp), ("S", _fp), ("L", _fp), ("X", _fp), ("Tm", _fp), ("A", _fp), ("D", _fp),
-                ("pc", _fp), ("zw", _fp * 2), ("bc", _fp), ("zprev", _fp), ("mx", _fp * 2), ("my", _fp * 2),
+                ("Sm", _fp), ("pc", _fp), ("zw", _fp * 2), ("bc", _fp), ("zprev", _fp), ("mx", _fp * 2), ("my", _fp * 2),
                 ("r", _fp), ("ain", _fp * 2), ("scratch", _fp)]
 
 

@@ -324,6 +324,8 @@ class RPCAProblem:
     min_{S, L >= 0} 1/2 sum_t ||y_t - Phi_t(s_t + l_t)||^2 + lambda||S||_1 + gamma||L||_*
                     + kappa sum_t V_mu(s_t, s_{t+1})          (eq:RPCA_UOTDF)
     with diagonal Phi (``phi`` [T][ny][nx] per-pixel weights, None = identity).
+    signed=True: the signed split eq:RPCA_UOTDF_PN, S = S+ - S-, with one
+    UOT chain per sign (reading L30).
 
     Every line of Algorithm 3 (including the SVT of line 10) runs in libuot_b200.so;
     this class only allocates the torch buffers and marshals pointers."""
@@ -332,8 +334,8 @@ class RPCAProblem:
 
     def __init__(self, Y: torch.Tensor, lam: float, gamma: float, kappa: float, mu: float, rho: float = 1.0,
                  phi: torch.Tensor | None = None, tau1: float | None = None, tau2: float | None = None,
-                 inner_iters: int = 1, p_norm: int = 1, *, stream: torch.cuda.Stream | None = None,
-                 reset: bool = True):
+                 inner_iters: int = 1, p_norm: int = 1, signed: bool = False, *,
+                 stream: torch.cuda.Stream | None = None, reset: bool = True):
         if Y.dim() != 3:
             raise ValueError("Y must be [T][ny][nx]")
         if not Y.is_cuda or Y.dtype != torch.float32:
@@ -344,18 +346,21 @@ class RPCAProblem:
         self.phi = phi.contiguous() if phi is not None else None
         T, ny, nx = self.Y.shape
         self.T, self.ny, self.nx = T, ny, nx
+        self.signed = bool(signed)
         P = T - 1
+        Q = 2 * P if self.signed else P
         dev = self.Y.device
         self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
         e = lambda *shape: torch.zeros(shape, dtype=torch.float32, device=dev)
         for k in self.STATE:
             setattr(self, k, e(T, ny, nx))
-        self.pc, self.bc = e(P, 2, ny, nx), e(P, 2, ny, nx)
-        self.zw = [e(P, 2, ny, nx), e(P, 2, ny, nx)]
-        self.zprev = e(P, 2, ny, nx) if inner_iters > 1 else None
-        self.mx, self.my, self.ain = [e(P, ny, nx), e(P, ny, nx)], [e(P, ny, nx), e(P, ny, nx)], [e(P, ny, nx), e(P, ny, nx)]
-        self.r = e(P, ny, nx)
-        flags = _lib.UOT_RESIDUAL_L2 if p_norm == 2 else 0
+        self.Sm = e(T, ny, nx) if self.signed else None
+        self.pc, self.bc = e(Q, 2, ny, nx), e(Q, 2, ny, nx)
+        self.zw = [e(Q, 2, ny, nx), e(Q, 2, ny, nx)]
+        self.zprev = e(Q, 2, ny, nx) if inner_iters > 1 else None
+        self.mx, self.my, self.ain = [e(Q, ny, nx), e(Q, ny, nx)], [e(Q, ny, nx), e(Q, ny, nx)], [e(Q, ny, nx), e(Q, ny, nx)]
+        self.r = e(Q, ny, nx)
+        flags = (_lib.UOT_RESIDUAL_L2 if p_norm == 2 else 0) | (_lib.UOT_RPCA_SIGNED if self.signed else 0)
         self._p = RpcaParams(nx, ny, T, float(lam), float(gamma), float(kappa), float(mu), float(rho),
                              float(tau1 or 0.0), float(tau2 or 0.0), int(inner_iters), flags)
         nsc = int(lib().uot_rpca_scratch_doubles(ctypes.byref(self._p)))
@@ -367,6 +372,7 @@ class RPCAProblem:
         bf.phi = self.phi.data_ptr() if self.phi is not None else None
         for k in self.STATE:
             setattr(bf, k, getattr(self, k).data_ptr())
+        bf.Sm = self.Sm.data_ptr() if self.Sm is not None else None
         bf.pc, bf.bc = self.pc.data_ptr(), self.bc.data_ptr()
         bf.zprev = self.zprev.data_ptr() if self.zprev is not None else None
         for k in range(2):
@@ -410,8 +416,14 @@ class RPCAProblem:
         b_t, c_{t+1} at index t, the oracle's layout); inner mx, my, r, ain."""
         s = int(lib().uot_rpca_state_slot(self._ctx))
         d = {k: getattr(self, k) for k in self.STATE}
-        d.update(Z=self.zw[s][:, 0], W=self.zw[s][:, 1], Bd=self.bc[:, 0], Cd=self.bc[:, 1],
-                 mx=self.mx[s], my=self.my[s], r=self.r, ain=self.ain[s])
+        d.update(mx=self.mx[s], my=self.my[s], r=self.r, ain=self.ain[s])
+        if not self.signed:
+            d.update(Z=self.zw[s][:, 0], W=self.zw[s][:, 1], Bd=self.bc[:, 0], Cd=self.bc[:, 1])
+            return d
+        P = self.T - 1
+        d["Sp"] = d.pop("S")
+        d.update(Sm=self.Sm, Zp=self.zw[s][:P, 0], Wp=self.zw[s][:P, 1], Zm=self.zw[s][P:, 0], Wm=self.zw[s][P:, 1],
+                 Bp=self.bc[:P, 0], Cp=self.bc[:P, 1], Bm=self.bc[P:, 0], Cm=self.bc[P:, 1])
         return d
 
     def set_timing(self, enable=True):

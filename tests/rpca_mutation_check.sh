@@ -23,3 +23,16 @@ for m in "${muts[@]}"; do
   if cmp -s w/oracle/rpca.py /root/repo/oracle/rpca.py; then echo "MUTATION DID NOT APPLY: $m"; continue; fi
   (cd w && timeout 900 python -m pytest tests/test_rpca_pins.py -x -q -p no:cacheprovider 2>&1 | tail -1) | sed "s|^|[$m] |" | cut -c1-200
 done
+# signed split (admm_signed, signed_s_update)
+muts2=(
+'s/    r2 = -u + km - lam_rho/    r2 = u + km - lam_rho/'
+'s/        Sn = Spn - Smn/        Sn = Spn + Smn/'
+'s/st.update(Bp=st\["Bp"\] + Zp - Spn\[:-1\], Cp=st\["Cp"\] + Wp - Spn\[1:\],/st.update(Bp=st["Bp"] + Zp - Spn[:-1], Cp=st["Cp"] + Wp - Smn[1:],/'
+'s/    ip = ((1.0 + m) \* r1 + r2) \/ det /    ip = ((1.0 + m) * r1 - r2) \/ det /'
+)
+for m in "${muts2[@]}"; do
+  rm -rf w; mkdir w; cp -r /root/repo/oracle /root/repo/tests w/
+  sed -i "$m" w/oracle/rpca.py
+  if cmp -s w/oracle/rpca.py /root/repo/oracle/rpca.py; then echo "MUTATION DID NOT APPLY: $m"; continue; fi
+  (cd w && timeout 900 python -m pytest tests/test_rpca_pins.py -x -q -p no:cacheprovider -k SG 2>&1 | tail -1) | sed "s|^|[$m] |" | cut -c1-200
+done

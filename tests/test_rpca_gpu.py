@@ -177,3 +177,38 @@ def test_rpca_invalid_arguments():
         RPCAProblem(torch.zeros(200, 4, 4, device="cuda"), 1.0, 1.0, 1.0, 1.0)
     with pytest.raises(ValueError):
         RPCAProblem(torch.zeros(1, 4, 4, device="cuda"), 1.0, 1.0, 1.0, 1.0)
+
+
+SKEYS = ("Sp", "Sm", "L", "X", "Tm", "A", "D", "Zp", "Wp", "Bp", "Cp", "Zm", "Wm", "Bm", "Cm")
+
+
+@pytest.mark.parametrize("T,ny,nx,n,inner", [(6, 10, 10, 40, 1), (7, 37, 52, 30, 3), (2, 16, 16, 30, 1)])
+def test_rpca_signed_parity(T, ny, nx, n, inner):
+    """Signed split (eq:RPCA_UOTDF_PN) against oracle.rpca.admm_signed:
+    data with bright and dark targets so both S+ and S- are active."""
+    import torch
+    from paper_1909_00149_b200 import inputs
+    from paper_1909_00149_b200.uot import RPCAProblem
+    Y, phi, S, L = inputs.gen_rpca(T, ny, nx, seed=T * 100 + nx, K=max(2, nx // 4), observed=0.7)
+    Y = (Y - 0.8 * phi * np.roll(S, 3, axis=2)).astype(np.float32)          # dark copies of the targets
+    t = _tau(nx, ny)
+    prob = RPCAProblem(torch.from_numpy(Y).cuda(), PRM["lam"], PRM["gamma"], PRM["kappa"], PRM["mu"], PRM["rho"],
+                       phi=torch.from_numpy(phi).cuda(), tau1=t, tau2=t, inner_iters=inner, signed=True)
+    rep = prob.solve(n, 0.0, n)
+    st_g = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
+    st_o, res, nuc = rpca.admm_signed(Y.astype(np.float64), PRM["lam"], PRM["gamma"], PRM["kappa"], PRM["mu"],
+                                      PRM["rho"], t, t, n, inner_iters=inner, phi=phi.astype(np.float64))
+    assert st_o["Sm"].max() > 1e-3 and st_o["Sp"].max() > 1e-3
+    scale = np.abs(Y).max()
+    for k in SKEYS:
+        r = st_o[k]
+        e = np.abs(st_g[k] - r).max() / max(np.abs(r).max(), scale)
+        assert e <= 1e-3, (k, e)
+    Sd = st_o["Sp"] - st_o["Sm"]
+    mx, my = st_o["mx"].copy(), st_o["my"].copy()
+    mx[..., :, -1] = 0.0
+    my[..., -1, :] = 0.0
+    obj = 0.5 * ((Y - phi * (Sd + st_o["L"])) ** 2).sum() + PRM["lam"] * (st_o["Sp"].sum() + st_o["Sm"].sum()) \
+        + PRM["gamma"] * nuc[-1] + PRM["kappa"] * (np.sqrt(mx**2 + my**2).sum() + PRM["mu"] * np.abs(st_o["r"]).sum())
+    assert rep["objective"] == pytest.approx(obj, rel=1e-4)
+    assert rep["primal_res"] == pytest.approx(res[-1, 0], rel=2e-2, abs=1e-5)

@@ -250,3 +250,124 @@ def test_R7_kappa_couples_frames_and_inner_iters_converge_to_same_limit():
     lo = rpca.admm(Y, lam, gamma, 0.05, mu, rho, t, t, 8000, inner_iters=3, phi=phi)[0]
     hi = rpca.admm(Y, lam, gamma, 1.0, mu, rho, t, t, 8000, inner_iters=3, phi=phi)[0]
     assert ot(hi) < ot(lo)
+
+
+# ----------------------------------------------------------------------------- signed split (NEXT(4))
+def test_SG0_signed_s_update_bruteforce():
+    """SG0 (reading L30): the joint (s+, s-) update is the exact minimiser over the quadrant
+    (checked against a 601 x 601 grid search on random scalar instances)."""
+    g = np.random.default_rng(0)
+    grid = np.linspace(0, 6, 601)
+    A_, B_ = np.meshgrid(grid, grid)
+    for _ in range(300):
+        u, kp, km = g.normal(size=3) * 2
+        m = int(g.integers(1, 3))
+        lr = abs(g.normal()) * 0.5
+        sp, sm = rpca.signed_s_update(np.array(u), np.array(kp), np.array(km), m, lr)
+        F = lambda a, b: lr * (a + b) + 0.5 * (u - a + b) ** 2 + 0.5 * (m * a * a - 2 * kp * a) + 0.5 * (m * b * b - 2 * km * b)
+        assert sp >= 0 and sm >= 0
+        assert F(sp, sm) <= F(A_, B_).min() + 1e-12
+
+
+def test_SG1_signed_soft_threshold_limit():
+    """SG1: gamma -> inf (L = 0), kappa -> 0: s+ - s- solves the signed lasso
+    min 1/2||y - phi s||^2 + lambda||s||_1: s+ = max(phi y - lambda, 0)/phi^2, s- = max(-phi y - lambda, 0)/phi^2."""
+    g = np.random.default_rng(31)
+    T, ny, nx = 3, 5, 4
+    Y = g.normal(size=(T, ny, nx))
+    phi = g.uniform(0.5, 1.5, (T, ny, nx))
+    lam = 0.2
+    t = _tau(nx, ny)
+    st, res, _ = rpca.admm_signed(Y, lam, 1e6, 1e-9, 1.0, 1.0, t, t, 4000, phi=phi)
+    np.testing.assert_allclose(st["Sp"], np.maximum(phi * Y - lam, 0) / phi**2, atol=1e-7)
+    np.testing.assert_allclose(st["Sm"], np.maximum(-phi * Y - lam, 0) / phi**2, atol=1e-7)
+
+
+def test_SG2_sign_flip_symmetry():
+    """SG2 (S:306 'sign-flipped data swaps the roles of S+ and S-'): with L = 0 (gamma -> inf)
+    eq:RPCA_UOTDF_PN is symmetric under Y -> -Y, (S+, S-) -> (S-, S+) (compared at the
+    limits: L >= 0 makes the transients differ)."""
+    Y, phi = _instance(9, T=4, mask=True)
+    Y = Y - 0.4
+    t = _tau(6, 6)
+    a = rpca.admm_signed(Y, 0.05, 1e6, 0.3, 1.5, 2.0, t, t, 6000, inner_iters=3, phi=phi)[0]
+    b = rpca.admm_signed(-Y, 0.05, 1e6, 0.3, 1.5, 2.0, t, t, 6000, inner_iters=3, phi=phi)[0]
+    np.testing.assert_allclose(a["Sp"], b["Sm"], atol=1e-8)
+    np.testing.assert_allclose(a["Sm"], b["Sp"], atol=1e-8)
+
+
+def _signed_instance():
+    Y, phi = _instance(12, T=4, neg=0.0)
+    Y[:, 3, 2] -= 0.8                                     # a dark target: needs S-
+    return Y, phi
+
+
+def test_SG3_signed_kkt_at_the_limit():
+    """SG3: the limit of the signed split satisfies the optimality conditions of
+    eq:RPCA_UOTDF_PN: feasibility of every split, x-stationarity, rho(a + b+ + c+) and
+    rho(-a + b- + c-) in lambda + N_+(s+/-), the L and nuclear-norm conditions, and the
+    OT subgradient identity for each sign's chain."""
+    Y, phi = _signed_instance()
+    lam, gamma, kappa, mu, rho = 0.05, 0.4, 0.3, 1.5, 2.0
+    t = _tau(6, 6)
+    st, res, _ = rpca.admm_signed(Y, lam, gamma, kappa, mu, rho, t, t, 20000, inner_iters=3, phi=phi)
+    assert res[-1, 0] < 5e-8 and res[-1, 1] < 5e-8     # slow tail: L16-type non-uniqueness
+    Sp, Sm, L, X, Tm, A, D = (st[k] for k in ("Sp", "Sm", "L", "X", "Tm", "A", "D"))
+    assert Sm.max() > 0.1 and Sp.max() > 0.1                # both signs active
+    z = np.zeros((1, 6, 6))
+    assert np.abs(X - (Sp - Sm) - L).max() < 1e-6 and np.abs(L - Tm).max() < 1e-6
+    for zk, wk, s in (("Zp", "Wp", Sp), ("Zm", "Wm", Sm)):
+        assert np.abs(st[zk] - s[:-1]).max() < 1e-6 and np.abs(st[wk] - s[1:]).max() < 1e-6
+    assert np.abs(rho * A - phi * (Y - phi * X)).max() < 1e-6
+    for sgn, s, bk, ck in ((1.0, Sp, "Bp", "Cp"), (-1.0, Sm, "Bm", "Cm")):
+        G = rho * (sgn * A + np.concatenate([st[bk], z]) + np.concatenate([z, st[ck]]))
+        pos = s > 1e-9
+        assert np.abs(G - lam)[pos].max() < 1e-6
+        assert (G - lam)[~pos].max() < 1e-6
+    pos = L > 1e-9
+    assert np.abs(A - D)[pos].max(initial=0) < 1e-6 and (A - D)[~pos].max(initial=-1) < 1e-6
+    Lm, Dm = L.reshape(4, -1).T, rho * D.reshape(4, -1).T
+    assert np.linalg.norm(Dm, 2) <= gamma + 1e-6
+    assert abs(np.sum(Dm * Lm) - gamma * rpca.nuclear_norm(Lm)) < 1e-6
+    for zk, wk, bk, ck in (("Zp", "Wp", "Bp", "Cp"), ("Zm", "Wm", "Bm", "Cm")):
+        for p in range(3):
+            U_, L_, _ = oracle.evaluate(st[zk][p], st[wk][p], mu, iters=200000, tol=1e-10)
+            hom = -(rho / kappa) * ((st[bk][p] * st[zk][p]).sum() + (st[ck][p] * st[wk][p]).sum())
+            assert abs(hom - 0.5 * (U_ + L_)) <= 0.5 * (U_ - L_) + 1e-6
+
+
+def test_SG4_signed_objective_not_above_unsigned():
+    """SG4: S- = 0 is feasible for eq:RPCA_UOTDF_PN, so at the limits its objective
+    is <= that of eq:RPCA_UOTDF; on data with a dark target it is strictly lower."""
+    Y, phi = _signed_instance()
+    lam, gamma, kappa, mu, rho = 0.05, 0.4, 0.3, 1.5, 2.0
+    t = _tau(6, 6)
+    su = rpca.admm(Y, lam, gamma, kappa, mu, rho, t, t, 6000, inner_iters=3, phi=phi)[0]
+    ss = rpca.admm_signed(Y, lam, gamma, kappa, mu, rho, t, t, 6000, inner_iters=3, phi=phi)[0]
+
+    def V(s):
+        return sum(oracle.evaluate(s[p], s[p + 1], mu, iters=100000, tol=1e-9)[0] for p in range(3))
+    fu = rpca.objective(Y, su["S"], su["L"], lam, gamma, kappa, mu, phi) + kappa * V(su["S"])
+    S = ss["Sp"] - ss["Sm"]
+    data = 0.5 * ((Y - phi * (S + ss["L"])) ** 2).sum()
+    fs = data + lam * (ss["Sp"].sum() + ss["Sm"].sum()) + gamma * rpca.nuclear_norm(ss["L"].reshape(4, -1).T) \
+        + kappa * (V(ss["Sp"]) + V(ss["Sm"]))
+    assert fs < fu - 1e-3
+
+
+def test_SG5_signed_second_iteration_closed_form():
+    """SG5: from the cold start, iteration 1 gives x1 = phi y/(phi^2 + rho) = A1, all else 0;
+    iteration 2 gives s+ = max((2 x1 - lambda/rho)/sigma, 0), s- = max((-2 x1 - lambda/rho)/sigma, 0)
+    (sigma = 1 + number of pair terms), L = Pi_+(x1 - (s+ - s-)/2)."""
+    Y, phi = _instance(4, T=5, neg=0.5)
+    lam, gamma, kappa, mu, rho = 0.05, 0.4, 0.3, 1.5, 2.0
+    t = _tau(6, 6)
+    st = rpca.admm_signed(Y, lam, gamma, kappa, mu, rho, t, t, 2, phi=phi)[0]
+    x1 = phi * Y / (phi**2 + rho)
+    sig = np.array([2.0, 3.0, 3.0, 3.0, 2.0])[:, None, None]
+    sp = np.maximum((2 * x1 - lam / rho) / sig, 0.0)
+    sm = np.maximum((-2 * x1 - lam / rho) / sig, 0.0)
+    assert sm.max() > 1e-3
+    np.testing.assert_allclose(st["Sp"], sp, atol=1e-14)
+    np.testing.assert_allclose(st["Sm"], sm, atol=1e-14)
+    np.testing.assert_allclose(st["L"], np.maximum(x1 - (sp - sm) / 2, 0.0), atol=1e-14)
