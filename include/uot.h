@@ -92,6 +92,10 @@ typedef struct {
     const float* a_prev_halo; /* [B][ny][nx] dual of the pair preceding frame 0 (chain prox shard), or NULL = 0 */
     const float* a_next_halo; /* [B][ny][nx] dual of the pair following frame T-1, or NULL = 0          */
     double* scratch;       /* uot_scratch_doubles(&params) doubles (reduction partials, flags)  */
+    float*  r_alt;         /* [B][P][ny][nx] second r buffer, or NULL.  Fixed marginals only:
+                              enables the temporally blocked kernel (two iterations per HBM pass,
+                              DESIGN.md "k_iter2"), which cannot update r in place.  Which of
+                              r / r_alt holds the current r: uot_r_slot().                     */
 } uot_buffers;
 
 /* Reductions (fp64) summed over this context's pairs, DESIGN.md "Reductions". */
@@ -188,6 +192,8 @@ int uot_get_timing(uot_ctx* ctx, double* ms_total, int64_t* n_launches);
 
 /* Which ping-pong slot (0/1) of mx/my/a/x holds the current iterate. */
 int uot_state_slot(const uot_ctx* ctx);
+/* Which r buffer holds the current r: 0 = buffers.r, 1 = buffers.r_alt. */
+int uot_r_slot(const uot_ctx* ctx);
 
 /* CUDA kernels launched by this context since creation (for accounting). */
 int64_t uot_launch_count(const uot_ctx* ctx);

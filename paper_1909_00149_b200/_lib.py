@@ -25,7 +25,7 @@ UOT_PART_ALL, UOT_PART_INTERIOR, UOT_PART_BOUNDARY = 0, 1, 2
 
 EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset", "uot_load_frames",
             "uot_iterate", "uot_iterate_part", "uot_get_report", "uot_prox_step", "uot_solve", "uot_objective", "uot_set_timing", "uot_get_timing",
-            "uot_state_slot", "uot_launch_count",
+            "uot_state_slot", "uot_r_slot", "uot_launch_count",
             "uot_destroy", "uot_last_error",
             "uot_df_scratch_doubles", "uot_df_create", "uot_df_reset", "uot_df_solve", "uot_df_set_timing",
             "uot_df_get_timing", "uot_df_launch_count", "uot_df_destroy", "uot_df_last_error",
@@ -48,7 +48,7 @@ _fp = ctypes.c_void_p
 class Buffers(ctypes.Structure):
     _fields_ = [("frames", _fp), ("f", _fp), ("mx", _fp * 2), ("my", _fp * 2), ("r", _fp),
                 ("a", _fp * 2), ("x", _fp * 2), ("a_prev_halo", _fp), ("a_next_halo", _fp),
-                ("scratch", _fp)]
+                ("scratch", _fp), ("r_alt", _fp)]
 
 
 class Report(ctypes.Structure):
@@ -146,6 +146,7 @@ def lib():
     L.uot_get_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
     L.uot_get_timing.restype = ctypes.c_int
     L.uot_state_slot.argtypes = [ctypes.c_void_p]; L.uot_state_slot.restype = ctypes.c_int
+    L.uot_r_slot.argtypes = [ctypes.c_void_p]; L.uot_r_slot.restype = ctypes.c_int
     L.uot_launch_count.argtypes = [ctypes.c_void_p]; L.uot_launch_count.restype = ctypes.c_int64
     L.uot_destroy.argtypes = [ctypes.c_void_p]; L.uot_destroy.restype = None
     L.uot_last_error.argtypes = [ctypes.c_void_p]; L.uot_last_error.restype = ctypes.c_char_p

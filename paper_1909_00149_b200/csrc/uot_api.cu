@@ -18,6 +18,7 @@
 #include "uot.h"
 #include "uot_kernels.cuh"
 #include "uot_persist.cuh"
+#include "uot_temporal.cuh"
 
 using namespace uotk;
 
@@ -304,6 +305,12 @@ struct uot_ctx {
     int fix_first;
     bool timing;
     bool stop_armed;
+    int slot;            // ping-pong slot of mx/my/a(/x) holding the current iterate
+    int rcur;            // 0: r holds the current r, 1: r_alt (after an odd number of k_iter2 passes)
+    bool t2ok;           // temporally blocked fixed-marginal kernel available (r_alt given)
+    int t2x, t2y;        // its tiles per pair
+    struct LogE { int64_t iter; int slot, rcur; };
+    std::vector<LogE> log;           // launches since the stop was armed (device-stop correction)
     std::vector<cudaEvent_t> ev;     // event pool, pairs (start, stop)
     size_t ev_used;
     char err[512];
@@ -458,6 +465,8 @@ size_t uot_scratch_doubles(const uot_params* p) {
     Geometry g1{1, (p->nx + 31) / 32, (p->ny + 3) / 4, 4, 0};
     size_t r1 = (size_t)G * g1.strips * g1.segs;
     if (r1 > recs) recs = r1;
+    const size_t r2 = (size_t)G * ((p->nx + kTW - 1) / kTW) * ((p->ny + kTH - 1) / kTH);   // k_iter2 tiles
+    if (r2 > recs) recs = r2;
     return recs * kRec + 2 * (size_t)G * kRec + GL_N + 4 + persist_scratch_doubles();
 }
 
@@ -531,7 +540,10 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->tau1f = (float)p.tau1; c->tau2f = (float)p.tau2;
     c->iter = 0;
     c->launches = 0;
-    const size_t recs = part_records(c->geo, c->G, c->bpp);
+    c->t2x = (p.nx + kTW - 1) / kTW;
+    c->t2y = (p.ny + kTH - 1) / kTH;
+    size_t recs = part_records(c->geo, c->G, c->bpp);
+    if ((size_t)c->G * c->t2x * c->t2y > recs) recs = (size_t)c->G * c->t2x * c->t2y;
     c->part = b.scratch;
     c->pair_it = c->part + recs * kRec;
     c->pair_obj = c->pair_it + (size_t)c->G * kRec;
@@ -542,6 +554,16 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->pxchg = reinterpret_cast<float*>(c->glob + GL_N + 4);
     c->pflags = reinterpret_cast<int*>(c->pxchg + (size_t)kMaxPersistCtas * 2 * kMaxTileEdge);
     plan_persist(c);
+    c->slot = 0;
+    c->rcur = 0;
+    c->t2ok = !prox && b.r_alt != nullptr && env_int("UOT_TEMPORAL", 1) != 0;
+    if (c->t2ok) {
+        if (cudaFuncSetAttribute((const void*)k_iter2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT2Smem) != cudaSuccess ||
+            cudaFuncSetAttribute((const void*)k_iter2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT2Smem) != cudaSuccess) {
+            cudaGetLastError();
+            c->t2ok = false;
+        }
+    }
     c->err[0] = 0;
     c->timing = false;
     c->stop_armed = false;
@@ -578,6 +600,9 @@ int uot_reset(uot_ctx* c, uint32_t flags) {
     cudaMemsetAsync(c->b.my[0], 0, bytes, c->s);
     cudaMemsetAsync(c->b.r, 0, bytes, c->s);
     cudaMemsetAsync(c->b.a[0], 0, bytes, c->s);
+    c->slot = 0;
+    c->rcur = 0;
+    c->log.clear();
     int rc = check_launch(c, "memset", false);
     if (rc) return rc;
     k_init_glob<<<1, 32, 0, c->s>>>(c->glob, c->stop, c->counter, 1);
@@ -628,8 +653,13 @@ static int pairs_in_part(const uot_ctx* c, int part) {
 
 // One kernel launch of iteration c->iter for `part`; part ALL / BOUNDARY completes
 // the iteration (slot flip, reductions when `red`).
+static float* rbuf(const uot_ctx* c) { return c->rcur ? c->b.r_alt : c->b.r; }
+static void log_launch(uot_ctx* c) {
+    if (c->stop_armed) c->log.push_back({c->iter, c->slot, c->rcur});
+}
+
 static int launch_one(uot_ctx* c, int part, bool red, const int* stop, double tol) {
-    const int in = (int)(c->iter & 1), o = in ^ 1;
+    const int in = c->slot, o = in ^ 1;
     const int gsel = pairs_in_part(c, part);
     if (gsel > 0) {
         IterArgs A{};
@@ -641,7 +671,7 @@ static int launch_one(uot_ctx* c, int part, bool red, const int* stop, double to
         A.f = c->b.f;
         A.mx_in = c->b.mx[in]; A.my_in = c->b.my[in]; A.a_in = c->b.a[in];
         A.mx_out = c->b.mx[o]; A.my_out = c->b.my[o]; A.a_out = c->b.a[o];
-        A.r = c->b.r;
+        A.r = rbuf(c);
         A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
         A.r_mode = c->r_mode; A.r_scale = c->r_scale; A.fix_first = c->fix_first;
         A.G = c->G; A.T = c->T; A.P = c->P;
@@ -675,6 +705,8 @@ static int launch_one(uot_ctx* c, int part, bool red, const int* stop, double to
     }
     if (part == UOT_PART_INTERIOR) return UOT_OK;
     c->iter++;
+    c->slot ^= 1;
+    log_launch(c);
     if (red) {
         ReduceArgs R{};
         R.partials = c->part; R.recs_per_pair = c->geo.strips * c->geo.segs; R.G = c->G;
@@ -700,7 +732,7 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
     for (int q = 0; q < 2; ++q) {
         A.mxb[q] = c->b.mx[q]; A.myb[q] = c->b.my[q]; A.ab[q] = c->b.a[q]; A.xb[q] = c->b.x[q];
     }
-    A.r = c->b.r; A.p = c->b.frames;
+    A.r = rbuf(c); A.p = c->b.frames;
     A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
     A.r_mode = c->r_mode; A.r_scale = c->r_scale; A.fix_first = c->fix_first;
     if (c->prox) {
@@ -728,8 +760,56 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
     if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "k_persist launch: %s", cudaGetErrorString(e));
     int rc = check_launch(c, "k_persist");
     if (rc) return rc;
+    c->slot = (int)((c->iter + n) & 1);   // the kernel writes iterate iter0 + done to slot (iter0 + done) & 1
     c->iter += n;            // uot_get_report corrects it if the device stopped early
     c->persist_launches++;
+    return UOT_OK;
+}
+
+// Two fixed-marginal iterations in one HBM pass (k_iter2, uot_temporal.cuh): iterations
+// iter+1, iter+2; reductions (red) for iteration iter+2.
+static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
+    const int in = c->slot, o = in ^ 1;
+    Iter2Args A{};
+    A.nx = c->nx; A.ny = c->ny; A.tiles_x = c->t2x; A.tiles_y = c->t2y; A.N = c->N;
+    A.f = c->b.f;
+    A.mx_in = c->b.mx[in]; A.my_in = c->b.my[in]; A.a_in = c->b.a[in]; A.r_in = rbuf(c);
+    A.mx_out = c->b.mx[o]; A.my_out = c->b.my[o]; A.a_out = c->b.a[o];
+    A.r_out = c->rcur ? c->b.r : c->b.r_alt;
+    A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
+    A.r_mode = c->r_mode; A.r_scale = c->r_scale;
+    A.partials = c->part; A.stop = stop;
+    const unsigned blocks = (unsigned)c->G * c->t2x * c->t2y;
+    cudaEvent_t e1 = nullptr;
+    if (c->timing) {
+        while (c->ev_used + 2 > c->ev.size()) {
+            cudaEvent_t ev;
+            if (cudaEventCreate(&ev) != cudaSuccess) return fail(c, UOT_E_CUDA, "cudaEventCreate");
+            c->ev.push_back(ev);
+        }
+        cudaEventRecord(c->ev[c->ev_used], c->s);
+        e1 = c->ev[c->ev_used + 1];
+        c->ev_used += 2;
+    }
+    if (red) k_iter2<true><<<blocks, kT2Threads, kT2Smem, c->s>>>(A);
+    else k_iter2<false><<<blocks, kT2Threads, kT2Smem, c->s>>>(A);
+    if (e1) cudaEventRecord(e1, c->s);
+    int rc = check_launch(c, "k_iter2");
+    if (rc) return rc;
+    c->iter += 2;
+    c->slot ^= 1;
+    c->rcur ^= 1;
+    log_launch(c);
+    if (red) {
+        ReduceArgs R{};
+        R.partials = c->part; R.recs_per_pair = c->t2x * c->t2y; R.G = c->G;
+        R.pair_out = c->pair_it; R.glob = c->glob; R.counter = c->counter;
+        R.stop = const_cast<int*>(stop); R.max_mask = 0u; R.is_iteration = 1; R.is_setup = 0;
+        R.iteration = c->iter; R.tol = tol; R.tau1 = c->tau1;
+        k_pair_reduce<<<c->G, 256, 0, c->s>>>(R);
+        rc = check_launch(c, "k_pair_reduce(iter2)");
+        if (rc) return rc;
+    }
     return UOT_OK;
 }
 
@@ -737,16 +817,27 @@ static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, c
     if (c->pg.ok && n >= 2) return launch_persist(c, n, reduce_every, reduce_last, stop, tol);
     const bool poll = stop != nullptr && n > 2 * kPollChunk && c->poll.init();
     if (poll) c->poll.begin();
-    for (int k = 0; k < n; ++k) {
-        if (poll && k > 0 && k % kPollChunk == 0) {
+    auto need_red = [&](int k) {
+        return (reduce_last && k == n - 1) || (reduce_every > 0 && ((k + 1) % reduce_every == 0));
+    };
+    int next_poll = kPollChunk;
+    for (int k = 0; k < n;) {
+        if (poll && k >= next_poll) {
+            next_poll += kPollChunk;
             c->poll.post(stop, c->s);
             if (c->poll.stopped()) {            // the device stopped >= one chunk ago: skip the rest
                 c->iter += n - k;               // uot_get_report corrects the count from the device
                 return UOT_OK;
             }
         }
-        const bool red = (reduce_last && k == n - 1) || (reduce_every > 0 && ((k + 1) % reduce_every == 0));
-        int rc = launch_one(c, UOT_PART_ALL, red, stop, tol);
+        int rc;
+        if (c->t2ok && n - k >= 2 && !need_red(k)) {   // two iterations per pass (reductions of the 2nd)
+            rc = launch_pass(c, need_red(k + 1), stop, tol);
+            k += 2;
+        } else {
+            rc = launch_one(c, UOT_PART_ALL, need_red(k), stop, tol);
+            k += 1;
+        }
         if (rc) return rc;
     }
     return UOT_OK;
@@ -787,6 +878,8 @@ int uot_iterate(uot_ctx* c, int32_t n, int32_t check_every, double tol) {
         if (rc) return rc;
         stop = c->stop;
         c->stop_armed = true;
+        c->log.clear();
+        c->log.push_back({c->iter, c->slot, c->rcur});
     }
     return launch_iters(c, n, check_every, n > 0, stop, tol);
 }
@@ -804,9 +897,19 @@ int uot_get_report(uot_ctx* c, uot_report* out) {
     int rc = read_glob(c, h);
     if (rc) return rc;
     if (c->stop_armed) {
+        const int64_t planned = c->iter;
         if (h[GL_CONV] >= 0.0) c->iter = (int64_t)h[GL_CONV];             // later launches exited early
         else if (h[GL_NONF] != 0.0 && h[GL_LASTRED] > 0) c->iter = (int64_t)h[GL_LASTRED];
+        if (c->iter != planned) {
+            // slot / r buffer of the iterate the device stopped at: replay the launch log
+            // (a k_iter2 pass advances 2 iterations but flips the slots once)
+            bool found = false;
+            for (const auto& e : c->log)
+                if (e.iter == c->iter) { c->slot = e.slot; c->rcur = e.rcur; found = true; break; }
+            if (!found) c->slot = (int)(c->iter & 1);                     // persistent / one-iteration launches
+        }
         c->stop_armed = false;
+        c->log.clear();
     }
     uot_report rep;
     fill_report(c, h, &rep);
@@ -831,6 +934,8 @@ int uot_solve(uot_ctx* c, int32_t max_iters, double tol, int32_t check_every, uo
     int rc = check_launch(c, "k_init_glob");
     if (rc) return rc;
     c->stop_armed = true;
+    c->log.clear();
+    c->log.push_back({c->iter, c->slot, c->rcur});
     rc = launch_iters(c, max_iters, check_every, max_iters > 0, c->stop, tol);
     if (rc) return rc;
     uot_report rep;
@@ -843,12 +948,12 @@ int uot_solve(uot_ctx* c, int32_t max_iters, double tol, int32_t check_every, uo
 
 int uot_objective(uot_ctx* c, double* per_pair, uot_report* out) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
-    const int slot = (int)(c->iter & 1);
+    const int slot = c->slot;
     ObjArgs O{};
     O.nx = c->nx; O.ny = c->ny; O.T = c->T; O.P = c->P; O.N = c->N; O.bpp = c->bpp;
     O.x = c->prox ? c->b.x[slot] : c->b.frames;
     O.p = c->prox ? c->b.frames : nullptr;
-    O.mx = c->b.mx[slot]; O.my = c->b.my[slot]; O.r = c->b.r; O.a = c->b.a[slot];
+    O.mx = c->b.mx[slot]; O.my = c->b.my[slot]; O.r = rbuf(c); O.a = c->b.a[slot];
     O.partials = c->part;
     O.p2 = c->r_mode == 1;
     k_objective<<<dim3(c->bpp, c->G), 256, 0, c->s>>>(O);
@@ -930,7 +1035,8 @@ int uot_get_timing(uot_ctx* c, double* ms_total, int64_t* n) {
     return UOT_OK;
 }
 
-int uot_state_slot(const uot_ctx* c) { return c ? (int)(c->iter & 1) : -1; }
+int uot_state_slot(const uot_ctx* c) { return c ? c->slot : -1; }
+int uot_r_slot(const uot_ctx* c) { return c ? c->rcur : -1; }
 
 int64_t uot_launch_count(const uot_ctx* c) { return c ? c->launches : -1; }
 

@@ -28,6 +28,10 @@
 namespace uotk {
 
 constexpr int kWarps = 4;          // warps (work items) per CTA in k_iter
+#ifndef UOT_PROX_MIN_BLOCKS
+#define UOT_PROX_MIN_BLOCKS 4
+#endif
+constexpr int kMinBlocksProx = UOT_PROX_MIN_BLOCKS;   // prox/DF: cap registers for 4 CTAs (16 warps) per SM
 constexpr int kRec = 8;            // doubles per partial record
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -140,7 +144,7 @@ __device__ __forceinline__ float pw(float v, int mode) { return mode == 1 ? v * 
 //   c1 = rho tau1/(1+rho tau1), c2 = 1/(1+rho tau1), c3 = tau1/(1+rho tau1),
 // with a_{-1} / a_{T-1} taken from the shard halos (or 0 at a chain end).
 template <int V, bool RED, bool PROX, bool DF = false>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, (PROX || DF) ? kMinBlocksProx : 1)
 k_iter(const IterArgs A) {
     if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
     const int lane = threadIdx.x & 31;

@@ -78,6 +78,8 @@ class Problem:
         self.mx = [e(plane), e(plane)]
         self.my = [e(plane), e(plane)]
         self.r = e(plane)
+        # fixed marginals: second r buffer for the two-iterations-per-pass kernel (k_iter2)
+        self.r_alt = e(plane) if not self.prox else None
         self.a = [e(plane), e(plane)]
         self.x = [e(self.frames.shape), e(self.frames.shape)] if self.prox else [None, None]
         # chain-prox shard halos (L19): duals of the pairs just outside this shard, [B][ny][nx]
@@ -115,6 +117,7 @@ class Problem:
             b.a[k] = self.a[k].data_ptr()
             b.x[k] = self.x[k].data_ptr() if self.x[k] is not None else None
         b.r = self.r.data_ptr()
+        b.r_alt = self.r_alt.data_ptr() if self.r_alt is not None else None
         b.a_prev_halo = self.a_prev_halo.data_ptr() if self.a_prev_halo is not None else None
         b.a_next_halo = self.a_next_halo.data_ptr() if self.a_next_halo is not None else None
         b.scratch = self.scratch.data_ptr()
@@ -194,7 +197,8 @@ class Problem:
     def state(self) -> dict:
         """Current iterate (views of the ping-pong slot)."""
         s = self.slot
-        d = {"mx": self.mx[s], "my": self.my[s], "r": self.r, "a": self.a[s]}
+        rs = int(lib().uot_r_slot(self._ctx))
+        d = {"mx": self.mx[s], "my": self.my[s], "r": self.r_alt if rs else self.r, "a": self.a[s]}
         if self.prox:
             d["x"] = self.x[s]
         return d

@@ -30,9 +30,12 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_struct_sizes_match_header():
-    # uot_params: 4 int32 + 4 double + uint32 (+pad); uot_buffers: 14 pointers
+    # uot_params: 4 int32 + 4 double + uint32 (+pad); uot_buffers: 15 pointers (r_alt last)
     assert ctypes.sizeof(_lib.Params) == 56
-    assert ctypes.sizeof(_lib.Buffers) == 14 * 8
+    assert ctypes.sizeof(_lib.Buffers) == 15 * 8
+    # uot_rpca_params: 3 int32 (+pad) + 7 double + int32 + uint32; uot_rpca_buffers: 22 pointers
+    assert ctypes.sizeof(_lib.RpcaParams) == 16 + 7 * 8 + 8
+    assert ctypes.sizeof(_lib.RpcaBuffers) == 22 * 8
     assert ctypes.sizeof(_lib.Report) == 9 * 8 + 8 + 4 + 4
 
 

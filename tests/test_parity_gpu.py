@@ -86,11 +86,16 @@ CASES = [
 ]
 
 
-# path variants: streaming kernel with lane width V and segment height H (UOT_PERSIST=0),
-# or the SMEM-resident persistent kernel (UOT_PERSIST=1, used when the grid fits)
-PATHS = [dict(UOT_VEC=1, UOT_SEG_H=0, UOT_PERSIST=0), dict(UOT_VEC=1, UOT_SEG_H=4, UOT_PERSIST=0),
-         dict(UOT_VEC=4, UOT_SEG_H=7, UOT_PERSIST=0), dict(UOT_VEC=4, UOT_SEG_H=0, UOT_PERSIST=0),
-         dict(UOT_VEC=2, UOT_SEG_H=5, UOT_PERSIST=0), dict(UOT_PERSIST=1)]
+# path variants: one-iteration streaming kernel with lane width V and segment height H
+# (UOT_PERSIST=0, UOT_TEMPORAL=0), the two-iterations-per-pass SMEM-tiled kernel k_iter2
+# (UOT_TEMPORAL=1; odd tails run the streaming kernel), or the SMEM-resident persistent
+# kernel (UOT_PERSIST=1, used when the grid fits)
+PATHS = [dict(UOT_VEC=1, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
+         dict(UOT_VEC=1, UOT_SEG_H=4, UOT_PERSIST=0, UOT_TEMPORAL=0),
+         dict(UOT_VEC=4, UOT_SEG_H=7, UOT_PERSIST=0, UOT_TEMPORAL=0),
+         dict(UOT_VEC=4, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
+         dict(UOT_VEC=2, UOT_SEG_H=5, UOT_PERSIST=0, UOT_TEMPORAL=0),
+         dict(UOT_PERSIST=0, UOT_TEMPORAL=1), dict(UOT_PERSIST=1)]
 
 
 @pytest.mark.parametrize("env", PATHS, ids=lambda e: "-".join(f"{k[4:]}{v}" for k, v in e.items()))
@@ -302,3 +307,55 @@ def test_persistent_solve_stops_on_device():
     ref, rrep = oracle.iterate(fr, 0.9, math.inf, tau, tau, kc)
     st = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
     compare(fr, st, ref)
+
+
+# ------------------------------------------------------------------------- temporal blocking (k_iter2)
+@pytest.mark.parametrize("n,check", [(40, 10), (41, 10), (35, 7), (12, 0)])
+def test_temporal_matches_streaming_and_oracle(n, check):
+    """Two iterations per HBM pass (k_iter2) give the one-iteration kernel's iterates (to
+    fp32 rounding; same arithmetic per iteration) and the oracle's, with reductions on
+    aligned (every 10) and misaligned (every 7: single launches fill in) iterations and
+    an odd tail; tiles ragged in both directions (150 x 200 = 2.3 x 4.7 tiles)."""
+    fr = inputs.gen_random(2, 3, 150, 200, seed=91, kind="sparse")
+    tau = tau_for(150, 200)
+    _, st_s, rep_s = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 0}, check_every=check)
+    prob, st_t, rep_t = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 1}, check_every=check)
+    for k in ("mx", "my", "r", "a"):
+        scale = max(np.abs(st_s[k]).max(), 1e-30)
+        assert np.abs(st_t[k] - st_s[k]).max() <= 1e-5 * scale, k
+    ref, rrep = oracle.iterate(fr, 1.4, math.inf, tau, tau, n)
+    compare(fr, st_t, ref)
+    assert rep_t["iterations"] == n
+    assert rep_t["objective"] == pytest.approx(rrep[:, 0].sum() + 1.4 * rrep[:, 1].sum(), rel=OBJ_RTOL)
+    assert rep_t["primal_res"] == pytest.approx(math.sqrt(rrep[:, 2].sum()), rel=1e-2, abs=1e-5)
+    assert rep_t["dual_res"] == pytest.approx(rep_s["dual_res"], rel=1e-3, abs=1e-6)
+    assert np.all(st_t["mx"][..., -1] == 0) and np.all(st_t["my"][..., -1, :] == 0)
+
+
+@pytest.mark.parametrize("check", [10, 7])
+def test_temporal_device_stop_replays_slots(check):
+    """A device-side stop inside a run of k_iter2 passes: the returned state is iterate
+    k_c (the r buffer and ping-pong slot are recovered from the launch log)."""
+    fr = inputs.gen_random(1, 2, 96, 130, seed=93, kind="uniform")
+    tau = tau_for(96, 130)
+    old = {k: os.environ.get(k) for k in ("UOT_PERSIST", "UOT_TEMPORAL")}
+    os.environ["UOT_PERSIST"], os.environ["UOT_TEMPORAL"] = "0", "1"
+    try:
+        prob = Problem(torch.from_numpy(fr).cuda(), 0.8, tau1=tau, tau2=tau)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    rep = prob.solve(20000, tol=1e-4, check_every=check)
+    assert rep["converged"] == 1
+    kc = rep["iterations"]
+    assert kc % check == 0 and 0 < kc < 20000
+    ref, _ = oracle.iterate(fr, 0.8, math.inf, tau, tau, kc)
+    st = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
+    compare(fr, st, ref)
+    # continuing from the recovered state (warm start) matches a fresh run of kc + 9 iterations
+    prob.step(9)
+    ref2, _ = oracle.iterate(fr, 0.8, math.inf, tau, tau, kc + 9)
+    compare(fr, {k: v.double().cpu().numpy() for k, v in prob.state().items()}, ref2)
