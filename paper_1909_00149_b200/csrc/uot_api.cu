@@ -22,6 +22,14 @@
 
 using namespace uotk;
 
+template <int TH>
+static bool iter2_attr_t() {
+    return cudaFuncSetAttribute((const void*)k_iter2<TH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)T2<TH>::smem) == cudaSuccess &&
+           cudaFuncSetAttribute((const void*)k_iter2<TH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)T2<TH>::smem) == cudaSuccess;
+}
+
 // ============================================================================ kernels
 namespace uotk {
 
@@ -308,7 +316,9 @@ struct uot_ctx {
     int slot;            // ping-pong slot of mx/my/a(/x) holding the current iterate
     int rcur;            // 0: r holds the current r, 1: r_alt (after an odd number of k_iter2 passes)
     bool t2ok;           // temporally blocked fixed-marginal kernel available (r_alt given)
+    int t2vec;           // its 16-byte loads (nx % 4 == 0, aligned planes)
     int t2x, t2y;        // its tiles per pair
+    int t2h;             // its interior tile rows (8, 16, 32)
     struct LogE { int64_t iter; int slot, rcur; };
     std::vector<LogE> log;           // launches since the stop was armed (device-stop correction)
     std::vector<cudaEvent_t> ev;     // event pool, pairs (start, stop)
@@ -465,7 +475,7 @@ size_t uot_scratch_doubles(const uot_params* p) {
     Geometry g1{1, (p->nx + 31) / 32, (p->ny + 3) / 4, 4, 0};
     size_t r1 = (size_t)G * g1.strips * g1.segs;
     if (r1 > recs) recs = r1;
-    const size_t r2 = (size_t)G * ((p->nx + kTW - 1) / kTW) * ((p->ny + kTH - 1) / kTH);   // k_iter2 tiles
+    const size_t r2 = (size_t)G * ((p->nx + kTW - 1) / kTW) * ((p->ny + 7) / 8);   // k_iter2 tiles (TH >= 8)
     if (r2 > recs) recs = r2;
     return recs * kRec + 2 * (size_t)G * kRec + GL_N + 4 + persist_scratch_doubles();
 }
@@ -540,8 +550,10 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->tau1f = (float)p.tau1; c->tau2f = (float)p.tau2;
     c->iter = 0;
     c->launches = 0;
+    c->t2h = env_int("UOT_T2_TH", kTH);
+    if (c->t2h != 8 && c->t2h != 32) c->t2h = 16;
     c->t2x = (p.nx + kTW - 1) / kTW;
-    c->t2y = (p.ny + kTH - 1) / kTH;
+    c->t2y = (p.ny + c->t2h - 1) / c->t2h;
     size_t recs = part_records(c->geo, c->G, c->bpp);
     if ((size_t)c->G * c->t2x * c->t2y > recs) recs = (size_t)c->G * c->t2x * c->t2y;
     c->part = b.scratch;
@@ -557,9 +569,11 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->slot = 0;
     c->rcur = 0;
     c->t2ok = !prox && b.r_alt != nullptr && env_int("UOT_TEMPORAL", 1) != 0;
+    c->t2vec = (p.nx % 4 == 0) && al16(b.f) && al16(b.mx[0]) && al16(b.mx[1]) && al16(b.my[0]) && al16(b.my[1]) &&
+               al16(b.a[0]) && al16(b.a[1]) && al16(b.r) && al16(b.r_alt);
     if (c->t2ok) {
-        if (cudaFuncSetAttribute((const void*)k_iter2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT2Smem) != cudaSuccess ||
-            cudaFuncSetAttribute((const void*)k_iter2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT2Smem) != cudaSuccess) {
+        const bool ok = c->t2h == 8 ? iter2_attr_t<8>() : (c->t2h == 32 ? iter2_attr_t<32>() : iter2_attr_t<16>());
+        if (!ok) {
             cudaGetLastError();
             c->t2ok = false;
         }
@@ -766,6 +780,14 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
     return UOT_OK;
 }
 
+extern "C++" {
+template <int TH>
+static void launch_iter2_t(uot_ctx* c, const Iter2Args& A, unsigned blocks, bool red) {
+    if (red) k_iter2<TH, true><<<blocks, kT2Threads, T2<TH>::smem, c->s>>>(A);
+    else k_iter2<TH, false><<<blocks, kT2Threads, T2<TH>::smem, c->s>>>(A);
+}
+}
+
 // Two fixed-marginal iterations in one HBM pass (k_iter2, uot_temporal.cuh): iterations
 // iter+1, iter+2; reductions (red) for iteration iter+2.
 static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
@@ -778,6 +800,7 @@ static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
     A.r_out = c->rcur ? c->b.r : c->b.r_alt;
     A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
     A.r_mode = c->r_mode; A.r_scale = c->r_scale;
+    A.vec = c->t2vec;
     A.partials = c->part; A.stop = stop;
     const unsigned blocks = (unsigned)c->G * c->t2x * c->t2y;
     cudaEvent_t e1 = nullptr;
@@ -791,8 +814,11 @@ static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
         e1 = c->ev[c->ev_used + 1];
         c->ev_used += 2;
     }
-    if (red) k_iter2<true><<<blocks, kT2Threads, kT2Smem, c->s>>>(A);
-    else k_iter2<false><<<blocks, kT2Threads, kT2Smem, c->s>>>(A);
+    switch (c->t2h) {
+        case 8: launch_iter2_t<8>(c, A, blocks, red); break;
+        case 32: launch_iter2_t<32>(c, A, blocks, red); break;
+        default: launch_iter2_t<16>(c, A, blocks, red); break;
+    }
     if (e1) cudaEventRecord(e1, c->s);
     int rc = check_launch(c, "k_iter2");
     if (rc) return rc;

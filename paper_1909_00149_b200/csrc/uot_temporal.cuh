@@ -17,10 +17,16 @@
 
 namespace uotk {
 
-constexpr int kTW = 64, kTH = 32, kHalo = 2;
-constexpr int kRW = kTW + 2 * kHalo, kRH = kTH + 2 * kHalo, kRA = kRW * kRH;
+constexpr int kTW = 64, kHalo = 2;
+constexpr int kLW = 4;                              // loaded columns left of the interior (16-B aligned)
+constexpr int kRW = kTW + 2 * kLW;                  // 72 loaded columns (18 float4), 2 extra unused
 constexpr int kT2Threads = 256;
-constexpr size_t kT2Smem = 9 * (size_t)kRA * sizeof(float);
+constexpr int kTH = 16;                             // default interior rows (tile 64 x kTH)
+template <int TH> struct T2 {
+    static constexpr int RH = TH + 2 * kHalo, RA = kRW * RH;
+    static constexpr size_t smem = 9 * (size_t)RA * sizeof(float);
+    static constexpr int minb = TH <= 8 ? 6 : (TH <= 16 ? 4 : 2);   // CTAs per SM the SMEM allows
+};
 
 struct Iter2Args {
     int nx, ny, tiles_x, tiles_y;
@@ -31,25 +37,34 @@ struct Iter2Args {
     float tau1, tau2, atau1;
     int r_mode;
     float r_scale;
+    int vec;                    // 16-byte loads (nx % 4 == 0, aligned planes)
     double* partials;           // [G * tiles][kRec] when reducing
     const int* stop;
 };
 
-// 4-byte async global -> shared copy; zero-fill when !valid (src-size 0)
+// async global -> shared copies; zero-fill when !valid (src-size 0)
 __device__ __forceinline__ void cp_async4(float* s, const float* g, bool valid) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
     const int sz = valid ? 4 : 0;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(g), "r"(sz) : "memory");
 }
+__device__ __forceinline__ void cp_async16(float* s, const float* g, bool valid) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(sz) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-template <bool RED>
-__global__ void __launch_bounds__(kT2Threads, 2) k_iter2(const Iter2Args A) {
-    extern __shared__ float sm[];
-    __shared__ double red_sh[40];
-    if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
+// Region coordinates: row r in [0, RH) <-> gj = ty*TH - kHalo + r; column c in [0, kRW)
+// <-> gi = tx*kTW - kLW + c.  Interior: r in [2, TH + 2), c in [4, 68).  Each warp walks rows
+// r = warp + 8k, each lane columns c = c0 + lane + 32m (no index division).
+// EDGE: the tile touches the grid border (bounds / pinned masks needed); else all in-grid.
+template <int TH, bool RED, bool EDGE>
+__device__ __forceinline__ void iter2_tile(const Iter2Args& A, float* sm, double* red_sh, int pair, int tile,
+                                           int gi0, int gj0) {
+    constexpr int kRH = T2<TH>::RH, kRA = T2<TH>::RA, kTH = TH;
     float* MX0 = sm;            // iteration k (masked: pinned / outside = 0), later M^{k+2}
     float* MY0 = MX0 + kRA;
     float* R0 = MY0 + kRA;
@@ -59,135 +74,251 @@ __global__ void __launch_bounds__(kT2Threads, 2) k_iter2(const Iter2Args A) {
     float* MY1 = MX1 + kRA;
     float* R1 = MY1 + kRA;
     float* A1 = R1 + kRA;
-    const int tiles = A.tiles_x * A.tiles_y;
-    const int pair = blockIdx.x / tiles, tile = blockIdx.x - pair * tiles;
-    const int tx = tile % A.tiles_x, ty = tile / A.tiles_x;
     const int nx = A.nx, ny = A.ny;
-    const int gi0 = tx * kTW - kHalo, gj0 = ty * kTH - kHalo;
     const size_t po = (size_t)pair * (size_t)A.N;
     const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1;
-    const int tid = threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = kT2Threads / 32;
+    auto inside = [&](int r, int c) {
+        if (!EDGE) return true;
+        const int gi = gi0 + c, gj = gj0 + r;
+        return gi >= 0 && gi < nx && gj >= 0 && gj < ny;
+    };
+    auto colx = [&](int r, int c) {                  // Mx exists (L3)
+        if (!EDGE) return true;
+        const int gi = gi0 + c, gj = gj0 + r;
+        return gi >= 0 && gi < nx - 1 && gj >= 0 && gj < ny;
+    };
+    auto rowy = [&](int r, int c) {                  // My exists (L3)
+        if (!EDGE) return true;
+        const int gi = gi0 + c, gj = gj0 + r;
+        return gi >= 0 && gi < nx && gj >= 0 && gj < ny - 1;
+    };
 
     // ---- load the tile + halo (iteration k) -------------------------------------------
-    for (int e = tid; e < kRA; e += kT2Threads) {
-        const int jj = e / kRW, ii = e - jj * kRW;
-        const int gi = gi0 + ii, gj = gj0 + jj;
-        const bool in = gi >= 0 && gi < nx && gj >= 0 && gj < ny;
-        const size_t g = in ? po + (size_t)gj * nx + gi : po;
-        cp_async4(MX0 + e, A.mx_in + g, in && gi < nx - 1);   // Mx[:, nx-1] pinned (L3)
-        cp_async4(MY0 + e, A.my_in + g, in && gj < ny - 1);   // My[ny-1, :] pinned
-        cp_async4(R0 + e, A.r_in + g, in);
-        cp_async4(A0 + e, A.a_in + g, in);
-        cp_async4(F + e, A.f + g, in);
+    if (A.vec) {
+        for (int e = threadIdx.x; e < kRH * (kRW / 4); e += kT2Threads) {
+            const int r = e / (kRW / 4), c = 4 * (e - r * (kRW / 4));
+            const int gi = gi0 + c, gj = gj0 + r;
+            const bool ok = gj >= 0 && gj < ny && gi >= 0 && gi < nx;   // whole float4 (nx % 4 == 0)
+            const size_t g = ok ? po + (size_t)gj * nx + gi : po;
+            const int s = r * kRW + c;
+            cp_async16(MX0 + s, A.mx_in + g, ok);
+            cp_async16(MY0 + s, A.my_in + g, ok);
+            cp_async16(R0 + s, A.r_in + g, ok);
+            cp_async16(A0 + s, A.a_in + g, ok);
+            cp_async16(F + s, A.f + g, ok);
+        }
+    } else {
+        for (int e = threadIdx.x; e < kRA; e += kT2Threads) {
+            const int r = e / kRW, c = e - r * kRW;
+            const int gi = gi0 + c, gj = gj0 + r;
+            const bool ok = gi >= 0 && gi < nx && gj >= 0 && gj < ny;
+            const size_t g = ok ? po + (size_t)gj * nx + gi : po;
+            cp_async4(MX0 + e, A.mx_in + g, ok);
+            cp_async4(MY0 + e, A.my_in + g, ok);
+            cp_async4(R0 + e, A.r_in + g, ok);
+            cp_async4(A0 + e, A.a_in + g, ok);
+            cp_async4(F + e, A.f + g, ok);
+        }
     }
     cp_async_wait_all();
+    if (EDGE) {                                      // pinned flux components read as 0 (L3)
+        __syncthreads();
+        for (int e = threadIdx.x; e < kRA; e += kT2Threads) {
+            const int r = e / kRW, c = e - r * kRW;
+            if (!colx(r, c)) MX0[e] = 0.f;
+            if (!rowy(r, c)) MY0[e] = 0.f;
+        }
+    }
     __syncthreads();
 
-    // ---- iteration k+1, line 3: M' on [0, RH-2] x [0, RW-2] (needs a at +i, +j) -------
-    for (int e = tid; e < (kRH - 1) * (kRW - 1); e += kT2Threads) {
-        const int jj = e / (kRW - 1), ii = e - jj * (kRW - 1);
-        const int idx = jj * kRW + ii;
-        const int gi = gi0 + ii, gj = gj0 + jj;
-        const bool in = gi >= 0 && gi < nx && gj >= 0 && gj < ny;
-        const bool colx = in && gi < nx - 1, rowy = in && gj < ny - 1;
-        const float a = A0[idx];
-        const float gx = colx ? a - A0[idx + 1] : 0.f;
-        const float gy = rowy ? a - A0[idx + kRW] : 0.f;
-        const float qx = MX0[idx] - t1 * gx;
-        const float qy = MY0[idx] - t1 * gy;
-        const float n2 = qx * qx + qy * qy;
-        const float s = shrink_factor(n2, rsqrtf(n2), t1);
-        MX1[idx] = s * qx;
-        MY1[idx] = s * qy;
+    // Phases 1a, 1b, 2a work on float4 quads of whole 72-column rows (18 quads per row):
+    // 4 pixels per thread with 128-bit SMEM accesses; the columns outside each phase's
+    // valid range (at most 2 per side) are computed from don't-care neighbours and never
+    // used.  The quad's right / left neighbours come from the next / previous 4 floats.
+    auto ld4 = [](const float* p) { return *reinterpret_cast<const float4*>(p); };
+    auto st4 = [](float* p, float a, float b, float c, float d) { *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d); };
+    // ---- iteration k+1, line 3: M' on rows [0, RH-2] (needs a at +i, +j) ----------------
+    for (int e = threadIdx.x; e < (kRH - 1) * (kRW / 4); e += kT2Threads) {
+        const int r = e / (kRW / 4), c = 4 * (e - r * (kRW / 4));
+        const int idx = r * kRW + c;
+        const float4 a4 = ld4(A0 + idx), ad4 = ld4(A0 + idx + kRW), mx4 = ld4(MX0 + idx), my4 = ld4(MY0 + idx);
+        const float a5 = A0[idx + 4];               // right neighbour of the 4th pixel (row end: unused)
+        const float av[5] = {a4.x, a4.y, a4.z, a4.w, a5}, adv[4] = {ad4.x, ad4.y, ad4.z, ad4.w};
+        const float mxv[4] = {mx4.x, mx4.y, mx4.z, mx4.w}, myv[4] = {my4.x, my4.y, my4.z, my4.w};
+        float ox[4], oy[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const float gx = colx(r, c + v) ? av[v] - av[v + 1] : 0.f;
+            const float gy = rowy(r, c + v) ? av[v] - adv[v] : 0.f;
+            const float qx = mxv[v] - t1 * gx;
+            const float qy = myv[v] - t1 * gy;
+            const float n2 = qx * qx + qy * qy;
+            const float sf = shrink_factor(n2, rsqrtf(n2), t1);
+            ox[v] = sf * qx;
+            oy[v] = sf * qy;
+        }
+        st4(MX1 + idx, ox[0], ox[1], ox[2], ox[3]);
+        st4(MY1 + idx, oy[0], oy[1], oy[2], oy[3]);
     }
     __syncthreads();
-    // ---- iteration k+1, lines 5-7: r', a' on [1, RH-2] x [1, RW-2] --------------------
-    for (int e = tid; e < (kRH - 2) * (kRW - 2); e += kT2Threads) {
-        const int jj = 1 + e / (kRW - 2), ii = 1 + e % (kRW - 2);
-        const int idx = jj * kRW + ii;
-        const int gi = gi0 + ii, gj = gj0 + jj;
-        const bool in = gi >= 0 && gi < nx && gj >= 0 && gj < ny;
-        const float r0 = R0[idx], a0 = A0[idx], f = F[idx];
-        const float rn = in ? r_update(fmaf(t1, a0, r0), A.r_mode, at1, A.r_scale) : 0.f;
-        const float divn = (MX1[idx] - MX1[idx - 1]) + (MY1[idx] - MY1[idx - kRW]);
-        const float divk = (MX0[idx] - MX0[idx - 1]) + (MY0[idx] - MY0[idx - kRW]);
-        const float Kn = divn - rn - f;
-        const float Kk = divk - r0 - f;
-        R1[idx] = rn;
-        A1[idx] = in ? fmaf(t2, 2.f * Kn - Kk, a0) : 0.f;
+    // ---- iteration k+1, lines 5-7: r', a' on rows [1, RH-2] ----------------------------
+    for (int e = threadIdx.x; e < (kRH - 2) * (kRW / 4); e += kT2Threads) {
+        const int rr = e / (kRW / 4), r = 1 + rr, c = 4 * (e - rr * (kRW / 4));
+        const int idx = r * kRW + c;
+        const float4 r04 = ld4(R0 + idx), a04 = ld4(A0 + idx), f4 = ld4(F + idx);
+        const float4 mx1 = ld4(MX1 + idx), my1 = ld4(MY1 + idx), my1u = ld4(MY1 + idx - kRW);
+        const float4 mx0 = ld4(MX0 + idx), my0 = ld4(MY0 + idx), my0u = ld4(MY0 + idx - kRW);
+        const float mx1l = MX1[idx - 1], mx0l = MX0[idx - 1];   // row start: don't-care column
+        const float r0v[4] = {r04.x, r04.y, r04.z, r04.w}, a0v[4] = {a04.x, a04.y, a04.z, a04.w};
+        const float fv[4] = {f4.x, f4.y, f4.z, f4.w};
+        const float mxn[5] = {mx1l, mx1.x, mx1.y, mx1.z, mx1.w}, myn[4] = {my1.x, my1.y, my1.z, my1.w};
+        const float mynu[4] = {my1u.x, my1u.y, my1u.z, my1u.w};
+        const float mxk[5] = {mx0l, mx0.x, mx0.y, mx0.z, mx0.w}, myk[4] = {my0.x, my0.y, my0.z, my0.w};
+        const float myku[4] = {my0u.x, my0u.y, my0u.z, my0u.w};
+        float ro[4], ao[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const bool in = inside(r, c + v);
+            const float rn = in ? r_update(fmaf(t1, a0v[v], r0v[v]), A.r_mode, at1, A.r_scale) : 0.f;
+            const float divn = (mxn[v + 1] - mxn[v]) + (myn[v] - mynu[v]);
+            const float divk = (mxk[v + 1] - mxk[v]) + (myk[v] - myku[v]);
+            const float Kn = divn - rn - fv[v];
+            const float Kk = divk - r0v[v] - fv[v];
+            ro[v] = rn;
+            ao[v] = in ? fmaf(t2, 2.f * Kn - Kk, a0v[v]) : 0.f;
+        }
+        st4(R1 + idx, ro[0], ro[1], ro[2], ro[3]);
+        st4(A1 + idx, ao[0], ao[1], ao[2], ao[3]);
     }
     __syncthreads();
-    // ---- iteration k+2, line 3: M'' on [1, RH-3] x [1, RW-3] (into MX0/MY0) ------------
-    for (int e = tid; e < (kRH - 3) * (kRW - 3); e += kT2Threads) {
-        const int jj = 1 + e / (kRW - 3), ii = 1 + e % (kRW - 3);
-        const int idx = jj * kRW + ii;
-        const int gi = gi0 + ii, gj = gj0 + jj;
-        const bool in = gi >= 0 && gi < nx && gj >= 0 && gj < ny;
-        const bool colx = in && gi < nx - 1, rowy = in && gj < ny - 1;
-        const float a = A1[idx];
-        const float gx = colx ? a - A1[idx + 1] : 0.f;
-        const float gy = rowy ? a - A1[idx + kRW] : 0.f;
-        const float qx = MX1[idx] - t1 * gx;                 // M' is 0 on pinned / outside
-        const float qy = MY1[idx] - t1 * gy;
-        const float n2 = qx * qx + qy * qy;
-        const float s = shrink_factor(n2, rsqrtf(n2), t1);
-        MX0[idx] = s * qx;
-        MY0[idx] = s * qy;
+    // ---- iteration k+2, line 3: M'' on rows [1, RH-3] (into MX0/MY0) --------------------
+    for (int e = threadIdx.x; e < (kRH - 3) * (kRW / 4); e += kT2Threads) {
+        const int rr = e / (kRW / 4), r = 1 + rr, c = 4 * (e - rr * (kRW / 4));
+        const int idx = r * kRW + c;
+        const float4 a4 = ld4(A1 + idx), ad4 = ld4(A1 + idx + kRW), mx4 = ld4(MX1 + idx), my4 = ld4(MY1 + idx);
+        const float a5 = A1[idx + 4];
+        const float av[5] = {a4.x, a4.y, a4.z, a4.w, a5}, adv[4] = {ad4.x, ad4.y, ad4.z, ad4.w};
+        const float mxv[4] = {mx4.x, mx4.y, mx4.z, mx4.w}, myv[4] = {my4.x, my4.y, my4.z, my4.w};
+        float ox[4], oy[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const float gx = colx(r, c + v) ? av[v] - av[v + 1] : 0.f;
+            const float gy = rowy(r, c + v) ? av[v] - adv[v] : 0.f;
+            const float qx = mxv[v] - t1 * gx;                // M' is 0 on pinned / outside
+            const float qy = myv[v] - t1 * gy;
+            const float n2 = qx * qx + qy * qy;
+            const float sf = shrink_factor(n2, rsqrtf(n2), t1);
+            ox[v] = sf * qx;
+            oy[v] = sf * qy;
+        }
+        st4(MX0 + idx, ox[0], ox[1], ox[2], ox[3]);
+        st4(MY0 + idx, oy[0], oy[1], oy[2], oy[3]);
     }
     __syncthreads();
-    // ---- iteration k+2, lines 5-7 on the interior; write M'', r'', a'' ----------------
+    // ---- iteration k+2, lines 5-7 on the interior rows [2, RH-3], cols [4, 67]: one
+    //      float4 (4 pixels) per thread, 128-bit SMEM reads and global stores -------------
     float s_tr = 0.f, s_gr = 0.f, s_k2 = 0.f, s_dz = 0.f, s_ub = 0.f;
-    for (int e = tid; e < kTH * kTW; e += kT2Threads) {
-        const int jj = kHalo + e / kTW, ii = kHalo + e % kTW;
-        const int gi = gi0 + ii, gj = gj0 + jj;
-        if (gi >= nx || gj >= ny) continue;
-        const int idx = jj * kRW + ii;
-        const float r1 = R1[idx], a1 = A1[idx], f = F[idx];
-        const float rn = r_update(fmaf(t1, a1, r1), A.r_mode, at1, A.r_scale);
-        const float mxn = MX0[idx], myn = MY0[idx];
-        const float divn = (mxn - MX0[idx - 1]) + (myn - MY0[idx - kRW]);
-        const float divk = (MX1[idx] - MX1[idx - 1]) + (MY1[idx] - MY1[idx - kRW]);
-        const float Kn = divn - rn - f;
-        const float Kk = divk - r1 - f;
-        const float an = fmaf(t2, 2.f * Kn - Kk, a1);
+    for (int e = threadIdx.x; e < kTH * (kTW / 4); e += kT2Threads) {
+        const int rr = e >> 4, r = kHalo + rr, c = kLW + 4 * (e & 15);
+        const int gi = gi0 + c, gj = gj0 + r;
+        if (EDGE && gj >= ny) continue;
+        const int idx = r * kRW + c;
+        const float4 R14 = *reinterpret_cast<const float4*>(R1 + idx);
+        const float4 A14 = *reinterpret_cast<const float4*>(A1 + idx);
+        const float4 F4 = *reinterpret_cast<const float4*>(F + idx);
+        const float4 MXn = *reinterpret_cast<const float4*>(MX0 + idx);
+        const float4 MYn = *reinterpret_cast<const float4*>(MY0 + idx);
+        const float4 MYnu = *reinterpret_cast<const float4*>(MY0 + idx - kRW);
+        const float4 MXk = *reinterpret_cast<const float4*>(MX1 + idx);
+        const float4 MYk = *reinterpret_cast<const float4*>(MY1 + idx);
+        const float4 MYku = *reinterpret_cast<const float4*>(MY1 + idx - kRW);
+        const float mxnl = MX0[idx - 1], mxkl = MX1[idx - 1];
+        const float r1v[4] = {R14.x, R14.y, R14.z, R14.w}, a1v[4] = {A14.x, A14.y, A14.z, A14.w};
+        const float fv[4] = {F4.x, F4.y, F4.z, F4.w};
+        const float mxn[4] = {MXn.x, MXn.y, MXn.z, MXn.w}, myn[4] = {MYn.x, MYn.y, MYn.z, MYn.w};
+        const float mynu[4] = {MYnu.x, MYnu.y, MYnu.z, MYnu.w};
+        const float mxk[4] = {MXk.x, MXk.y, MXk.z, MXk.w}, myk[4] = {MYk.x, MYk.y, MYk.z, MYk.w};
+        const float myku[4] = {MYku.x, MYku.y, MYku.z, MYku.w};
+        float rn[4], an[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            rn[v] = r_update(fmaf(t1, a1v[v], r1v[v]), A.r_mode, at1, A.r_scale);
+            const float divn = (mxn[v] - (v ? mxn[v - 1] : mxnl)) + (myn[v] - mynu[v]);
+            const float divk = (mxk[v] - (v ? mxk[v - 1] : mxkl)) + (myk[v] - myku[v]);
+            const float Kn = divn - rn[v] - fv[v];
+            const float Kk = divk - r1v[v] - fv[v];
+            an[v] = fmaf(t2, 2.f * Kn - Kk, a1v[v]);
+            if constexpr (RED) {
+                if (!EDGE || gi + v < nx) {
+                    const float dmx = mxn[v] - mxk[v], dmy = myn[v] - myk[v], dr = rn[v] - r1v[v];
+                    s_tr += sqrtf(mxn[v] * mxn[v] + myn[v] * myn[v]);
+                    s_gr += pw(rn[v], A.r_mode);
+                    s_k2 += Kn * Kn;
+                    s_dz += dmx * dmx + dmy * dmy + dr * dr;
+                    s_ub += pw(divn - fv[v], A.r_mode);
+                }
+            }
+        }
         const size_t g = po + (size_t)gj * nx + gi;
-        A.mx_out[g] = mxn;
-        A.my_out[g] = myn;
-        A.r_out[g] = rn;
-        A.a_out[g] = an;
-        if constexpr (RED) {
-            const float dmx = mxn - MX1[idx], dmy = myn - MY1[idx], dr = rn - r1;
-            s_tr += sqrtf(mxn * mxn + myn * myn);
-            s_gr += pw(rn, A.r_mode);
-            s_k2 += Kn * Kn;
-            s_dz += dmx * dmx + dmy * dmy + dr * dr;
-            s_ub += pw(divn - f, A.r_mode);
+        if (A.vec && (!EDGE || gi + 3 < nx)) {
+            *reinterpret_cast<float4*>(A.mx_out + g) = MXn;
+            *reinterpret_cast<float4*>(A.my_out + g) = MYn;
+            *reinterpret_cast<float4*>(A.r_out + g) = make_float4(rn[0], rn[1], rn[2], rn[3]);
+            *reinterpret_cast<float4*>(A.a_out + g) = make_float4(an[0], an[1], an[2], an[3]);
+        } else {
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                if (gi + v < nx) {
+                    A.mx_out[g + v] = mxn[v];
+                    A.my_out[g + v] = myn[v];
+                    A.r_out[g + v] = rn[v];
+                    A.a_out[g + v] = an[v];
+                }
         }
     }
     if constexpr (RED) {
-        // fixed-order block sums (warp butterfly, then warp 0 over the 8 warp sums)
+        // fixed-order block sums (warp butterfly, then the 8 warp sums in order)
         double v[5] = {s_tr, s_gr, s_k2, s_dz, s_ub};
-        const int w = tid >> 5, l = tid & 31;
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(kFull, v[q], o);
         }
-        if (l == 0)
+        if (lane == 0)
 #pragma unroll
-            for (int q = 0; q < 5; ++q) red_sh[q * 8 + w] = v[q];
+            for (int q = 0; q < 5; ++q) red_sh[q * NW + warp] = v[q];
         __syncthreads();
-        if (tid == 0) {
+        if (threadIdx.x == 0) {
+            const int tiles = A.tiles_x * A.tiles_y;
             double* P = A.partials + ((size_t)pair * tiles + tile) * kRec;
 #pragma unroll
             for (int q = 0; q < 5; ++q) {
                 double t = 0.0;
-                for (int k = 0; k < kT2Threads / 32; ++k) t += red_sh[q * 8 + k];
+                for (int k = 0; k < NW; ++k) t += red_sh[q * NW + k];
                 P[q] = t;
             }
             P[5] = 0.0; P[6] = 0.0; P[7] = 0.0;
         }
     }
+}
+
+template <int TH, bool RED>
+__global__ void __launch_bounds__(kT2Threads, T2<TH>::minb) k_iter2(const Iter2Args A) {
+    constexpr int kTH = TH, kRH = T2<TH>::RH;
+    extern __shared__ float4 sm4[];
+    __shared__ double red_sh[5 * (kT2Threads / 32)];
+    if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
+    const int tiles = A.tiles_x * A.tiles_y;
+    const int pair = blockIdx.x / tiles, tile = blockIdx.x - pair * tiles;
+    const int tx = tile % A.tiles_x, ty = tile / A.tiles_x;
+    const int gi0 = tx * kTW - kLW, gj0 = ty * kTH - kHalo;
+    // interior tile: every region pixel in the grid and off the pinned last row/column
+    const bool edge = gi0 < 0 || gj0 < 0 || gi0 + kRW > A.nx - 1 || gj0 + kRH > A.ny - 1;
+    float* sm = reinterpret_cast<float*>(sm4);
+    if (edge) iter2_tile<TH, RED, true>(A, sm, red_sh, pair, tile, gi0, gj0);
+    else iter2_tile<TH, RED, false>(A, sm, red_sh, pair, tile, gi0, gj0);
 }
 
 }  // namespace uotk
