@@ -475,7 +475,7 @@ size_t uot_scratch_doubles(const uot_params* p) {
     Geometry g1{1, (p->nx + 31) / 32, (p->ny + 3) / 4, 4, 0};
     size_t r1 = (size_t)G * g1.strips * g1.segs;
     if (r1 > recs) recs = r1;
-    const size_t r2 = (size_t)G * ((p->nx + kTW - 1) / kTW) * ((p->ny + 7) / 8);   // k_iter2 tiles (TH >= 8)
+    const size_t r2 = (size_t)G * ((p->nx + kTW - 1) / kTW) * ((p->ny + 15) / 16);   // k_iter2 tiles (TH >= 16)
     if (r2 > recs) recs = r2;
     return recs * kRec + 2 * (size_t)G * kRec + GL_N + 4 + persist_scratch_doubles();
 }
@@ -551,7 +551,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->iter = 0;
     c->launches = 0;
     c->t2h = env_int("UOT_T2_TH", kTH);
-    if (c->t2h != 8 && c->t2h != 32) c->t2h = 16;
+    if (c->t2h != 16 && c->t2h != 24 && c->t2h != 48) c->t2h = 32;
     c->t2x = (p.nx + kTW - 1) / kTW;
     c->t2y = (p.ny + c->t2h - 1) / c->t2h;
     size_t recs = part_records(c->geo, c->G, c->bpp);
@@ -572,7 +572,8 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->t2vec = (p.nx % 4 == 0) && al16(b.f) && al16(b.mx[0]) && al16(b.mx[1]) && al16(b.my[0]) && al16(b.my[1]) &&
                al16(b.a[0]) && al16(b.a[1]) && al16(b.r) && al16(b.r_alt);
     if (c->t2ok) {
-        const bool ok = c->t2h == 8 ? iter2_attr_t<8>() : (c->t2h == 32 ? iter2_attr_t<32>() : iter2_attr_t<16>());
+        const bool ok = c->t2h == 16 ? iter2_attr_t<16>()
+                        : (c->t2h == 24 ? iter2_attr_t<24>() : (c->t2h == 48 ? iter2_attr_t<48>() : iter2_attr_t<32>()));
         if (!ok) {
             cudaGetLastError();
             c->t2ok = false;
@@ -815,9 +816,10 @@ static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
         c->ev_used += 2;
     }
     switch (c->t2h) {
-        case 8: launch_iter2_t<8>(c, A, blocks, red); break;
-        case 32: launch_iter2_t<32>(c, A, blocks, red); break;
-        default: launch_iter2_t<16>(c, A, blocks, red); break;
+        case 16: launch_iter2_t<16>(c, A, blocks, red); break;
+        case 24: launch_iter2_t<24>(c, A, blocks, red); break;
+        case 48: launch_iter2_t<48>(c, A, blocks, red); break;
+        default: launch_iter2_t<32>(c, A, blocks, red); break;
     }
     if (e1) cudaEventRecord(e1, c->s);
     int rc = check_launch(c, "k_iter2");

@@ -21,11 +21,11 @@ constexpr int kTW = 64, kHalo = 2;
 constexpr int kLW = 4;                              // loaded columns left of the interior (16-B aligned)
 constexpr int kRW = kTW + 2 * kLW;                  // 72 loaded columns (18 float4), 2 extra unused
 constexpr int kT2Threads = 256;
-constexpr int kTH = 16;                             // default interior rows (tile 64 x kTH)
+constexpr int kTH = 32;                             // default interior rows (tile 64 x kTH)
 template <int TH> struct T2 {
     static constexpr int RH = TH + 2 * kHalo, RA = kRW * RH;
-    static constexpr size_t smem = 9 * (size_t)RA * sizeof(float);
-    static constexpr int minb = TH <= 8 ? 6 : (TH <= 16 ? 4 : 2);   // CTAs per SM the SMEM allows
+    static constexpr size_t smem = 7 * (size_t)RA * sizeof(float);
+    static constexpr int minb = TH <= 8 ? 6 : (TH <= 16 ? 4 : (TH <= 32 ? 3 : 2));   // CTAs/SM (SMEM-bound)
 };
 
 struct Iter2Args {
@@ -72,8 +72,8 @@ __device__ __forceinline__ void iter2_tile(const Iter2Args& A, float* sm, double
     float* F = A0 + kRA;
     float* MX1 = F + kRA;       // iteration k+1
     float* MY1 = MX1 + kRA;
-    float* R1 = MY1 + kRA;
-    float* A1 = R1 + kRA;
+    float* R1 = R0;             // r', a' overwrite r, a in place: the a'/r' phase reads r, a
+    float* A1 = A0;             // only at its own pixel, and nothing reads them afterwards
     const int nx = A.nx, ny = A.ny;
     const size_t po = (size_t)pair * (size_t)A.N;
     const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1;
