@@ -324,17 +324,47 @@ def main():
     pxit_total = sum_over_ranks(float(G) * N * iters_done)
     value = pxit_total / (ms_max / 1e3)
 
-    # ---- roofline of the dominant kernel (fused iteration), per iteration (1 launch, or
-    #      interior + boundary launches in overlapped chain-prox shards)
+    # ---- roofline of the dominant kernel.  Fixed marginals: one launch = one HBM pass of the
+    #      state (k_iter2: two fused iterations; k_iter: one), algorithmic 36 B per pair-pixel
+    #      per pass.  Chain prox: per iteration (1 launch, or interior + boundary launches).
     peak, peak_src = load_peaks()
     alg_bytes_launch = bytes_iter
-    avg_launch_s = (kern_ms / max(iters_done, 1)) / 1e3
+    if prox:
+        avg_launch_s = (kern_ms / max(iters_done, 1)) / 1e3
+    else:
+        avg_launch_s = (kern_ms / max(kern_n, 1)) / 1e3
     achieved = alg_bytes_launch / avg_launch_s / 1e9
+    temporal = (not prox) and kern_n < iters_done
+    kernel_name = ("k_iter2 (two fused Alg.1 iterations per HBM pass, SMEM tiles)" if temporal
+                   else f"k_iter<{'prox' if prox else 'fixed'}> (fused Alg.1 iteration)")
+
+    # ---- the one-pass kernel (one iteration per HBM pass) on the same state, for reference
+    one_pass = None
+    if temporal:
+        n1 = 20
+        prob.set_temporal(False)
+        prob.set_timing(True)
+        prob.get_timing()
+        barrier()
+        o0, o1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        o0.record(stream)
+        prob.step(n1)
+        o1.record(stream)
+        barrier()
+        k1_ms, k1_n = prob.get_timing()
+        prob.set_timing(False)
+        prob.set_temporal(True)
+        ms1 = max_over_ranks(o0.elapsed_time(o1))
+        a1 = bytes_iter / ((k1_ms / max(k1_n, 1)) / 1e3) / 1e9
+        one_pass = {"kernel": "k_iter<fixed> (one Alg.1 iteration per HBM pass)", "achieved": a1, "peak": peak,
+                    "unit": "GB/s", "frac": a1 / peak, "px_it_per_s": sum_over_ranks(float(G) * N * n1) / (ms1 / 1e3),
+                    "iterations": n1}
     traffic = None
     prof_sum = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof_sum):
         try:
-            d = json.load(open(prof_sum)).get(cfg.name if not prox else cfg.name + "-prox")
+            key = cfg.name + ("-prox" if prox else ("-k_iter2" if temporal else ""))
+            d = json.load(open(prof_sum)).get(key)
             if d:
                 traffic = d.get("dram_bytes_per_launch")
         except Exception:
@@ -386,9 +416,11 @@ def main():
             "config": config_dict(cfg, world, args.mode),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": f"k_iter<{'prox' if prox else 'fixed'}> (fused Alg.1 iteration)",
+                         "kernel": kernel_name,
+                         "iterations_per_launch": (iters_done / max(kern_n, 1)) if not prox else 1,
                          "alg_bytes_per_launch": alg_bytes_launch, "avg_launch_ms": avg_launch_s * 1e3,
                          "launches_timed": kern_n, "peak_source": peak_src},
+            "one_pass_kernel": one_pass,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -194,6 +194,10 @@ int uot_get_timing(uot_ctx* ctx, double* ms_total, int64_t* n_launches);
 int uot_state_slot(const uot_ctx* ctx);
 /* Which r buffer holds the current r: 0 = buffers.r, 1 = buffers.r_alt. */
 int uot_r_slot(const uot_ctx* ctx);
+/* Fixed marginals with buffers.r_alt: enable (1, the default) or disable (0) the two-iterations-
+ * per-pass kernel k_iter2; disabled, every iteration is one pass of k_iter (for A/B timing).
+ * Returns UOT_E_INVALID if k_iter2 is unavailable and enable != 0. */
+int uot_set_temporal(uot_ctx* ctx, int enable);
 
 /* CUDA kernels launched by this context since creation (for accounting). */
 int64_t uot_launch_count(const uot_ctx* ctx);

@@ -316,6 +316,7 @@ struct uot_ctx {
     int slot;            // ping-pong slot of mx/my/a(/x) holding the current iterate
     int rcur;            // 0: r holds the current r, 1: r_alt (after an odd number of k_iter2 passes)
     bool t2ok;           // temporally blocked fixed-marginal kernel available (r_alt given)
+    bool t2on;           // ... and enabled (uot_set_temporal)
     int t2vec;           // its 16-byte loads (nx % 4 == 0, aligned planes)
     int t2x, t2y;        // its tiles per pair
     int t2h;             // its interior tile rows (8, 16, 32)
@@ -569,6 +570,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->slot = 0;
     c->rcur = 0;
     c->t2ok = !prox && b.r_alt != nullptr && env_int("UOT_TEMPORAL", 1) != 0;
+    c->t2on = true;
     c->t2vec = (p.nx % 4 == 0) && al16(b.f) && al16(b.mx[0]) && al16(b.mx[1]) && al16(b.my[0]) && al16(b.my[1]) &&
                al16(b.a[0]) && al16(b.a[1]) && al16(b.r) && al16(b.r_alt);
     if (c->t2ok) {
@@ -859,7 +861,7 @@ static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, c
             }
         }
         int rc;
-        if (c->t2ok && n - k >= 2 && !need_red(k)) {   // two iterations per pass (reductions of the 2nd)
+        if (c->t2ok && c->t2on && n - k >= 2 && !need_red(k)) {   // two iterations per pass (reductions of the 2nd)
             rc = launch_pass(c, need_red(k + 1), stop, tol);
             k += 2;
         } else {
@@ -1065,6 +1067,13 @@ int uot_get_timing(uot_ctx* c, double* ms_total, int64_t* n) {
 
 int uot_state_slot(const uot_ctx* c) { return c ? c->slot : -1; }
 int uot_r_slot(const uot_ctx* c) { return c ? c->rcur : -1; }
+
+int uot_set_temporal(uot_ctx* c, int enable) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    if (enable && !c->t2ok) return fail(c, UOT_E_INVALID, "k_iter2 unavailable (prox mode, no r_alt, or UOT_TEMPORAL=0)");
+    c->t2on = enable != 0;
+    return UOT_OK;
+}
 
 int64_t uot_launch_count(const uot_ctx* c) { return c ? c->launches : -1; }
 

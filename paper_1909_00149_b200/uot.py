@@ -190,6 +190,10 @@ class Problem:
     def slot(self) -> int:
         return int(lib().uot_state_slot(self._ctx))
 
+    def set_temporal(self, enable: bool = True):
+        """Fixed marginals: two iterations per HBM pass (k_iter2, default) or one (k_iter)."""
+        check(lib().uot_set_temporal(self._ctx, int(bool(enable))), self._ctx)
+
     @property
     def launches(self) -> int:
         return int(lib().uot_launch_count(self._ctx))
