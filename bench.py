@@ -334,9 +334,14 @@ def main():
     else:
         avg_launch_s = (kern_ms / max(kern_n, 1)) / 1e3
     achieved = alg_bytes_launch / avg_launch_s / 1e9
-    temporal = (not prox) and kern_n < iters_done
-    kernel_name = ("k_iter2 (two fused Alg.1 iterations per HBM pass, SMEM tiles)" if temporal
-                   else f"k_iter<{'prox' if prox else 'fixed'}> (fused Alg.1 iteration)")
+    path = prob.kernel_path
+    temporal = path == "k_iter2"
+    kernel_name = {"k_iter2": "k_iter2 (two fused Alg.1 iterations per HBM pass, SMEM tiles)",
+                   "k_persist": "k_persist (all iterations in one cooperative launch, SMEM-resident)"}.get(
+        path, f"k_iter<{'prox' if prox else 'fixed'}> (fused Alg.1 iteration)")
+    if path == "k_persist":            # one launch per step: time per iteration
+        avg_launch_s = (kern_ms / max(iters_done, 1)) / 1e3
+        achieved = alg_bytes_launch / avg_launch_s / 1e9
 
     # ---- the one-pass kernel (one iteration per HBM pass) on the same state, for reference
     one_pass = None
@@ -417,7 +422,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": kernel_name,
-                         "iterations_per_launch": (iters_done / max(kern_n, 1)) if not prox else 1,
+                         "iterations_per_launch": (iters_done / max(kern_n, 1)) if path != "k_persist" else 1,
                          "alg_bytes_per_launch": alg_bytes_launch, "avg_launch_ms": avg_launch_s * 1e3,
                          "launches_timed": kern_n, "peak_source": peak_src},
             "one_pass_kernel": one_pass,

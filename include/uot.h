@@ -198,6 +198,10 @@ int uot_r_slot(const uot_ctx* ctx);
  * per-pass kernel k_iter2; disabled, every iteration is one pass of k_iter (for A/B timing).
  * Returns UOT_E_INVALID if k_iter2 is unavailable and enable != 0. */
 int uot_set_temporal(uot_ctx* ctx, int enable);
+/* Kernel that runs the iterations of this context: 0 = k_iter (one pass per iteration),
+ * 1 = k_iter2 (two iterations per pass, fixed marginals), 2 = k_persist (all iterations of
+ * a call in one cooperative launch, small grids). */
+int uot_kernel_path(const uot_ctx* ctx);
 
 /* CUDA kernels launched by this context since creation (for accounting). */
 int64_t uot_launch_count(const uot_ctx* ctx);

@@ -322,6 +322,7 @@ struct uot_ctx {
     int t2h;             // its interior tile rows (8, 16, 32)
     struct LogE { int64_t iter; int slot, rcur; };
     std::vector<LogE> log;           // launches since the stop was armed (device-stop correction)
+    std::vector<LogE> persist_base;  // state at the start of each persistent launch since arming
     std::vector<cudaEvent_t> ev;     // event pool, pairs (start, stop)
     size_t ev_used;
     char err[512];
@@ -620,6 +621,7 @@ int uot_reset(uot_ctx* c, uint32_t flags) {
     c->slot = 0;
     c->rcur = 0;
     c->log.clear();
+    c->persist_base.clear();
     int rc = check_launch(c, "memset", false);
     if (rc) return rc;
     k_init_glob<<<1, 32, 0, c->s>>>(c->glob, c->stop, c->counter, 1);
@@ -744,7 +746,7 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
     A.nx = c->nx; A.ny = c->ny; A.G = c->G; A.T = c->T; A.P = c->P; A.N = c->N;
     A.TW = c->pg.TW; A.TH = c->pg.TH; A.tiles_x = c->pg.tx; A.tiles_y = c->pg.ty;
     A.n_iters = n; A.red_every = reduce_every; A.red_last = reduce_last ? 1 : 0;
-    A.iter0 = c->iter; A.prox = c->prox;
+    A.iter0 = c->iter; A.slot0 = c->slot; A.prox = c->prox;
     A.f = c->b.f;
     for (int q = 0; q < 2; ++q) {
         A.mxb[q] = c->b.mx[q]; A.myb[q] = c->b.my[q]; A.ab[q] = c->b.a[q]; A.xb[q] = c->b.x[q];
@@ -777,7 +779,9 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
     if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "k_persist launch: %s", cudaGetErrorString(e));
     int rc = check_launch(c, "k_persist");
     if (rc) return rc;
-    c->slot = (int)((c->iter + n) & 1);   // the kernel writes iterate iter0 + done to slot (iter0 + done) & 1
+    const int slot0 = c->slot;
+    c->slot = slot0 ^ (n & 1);            // the kernel writes iterate iter0 + done to slot slot0 ^ (done & 1)
+    if (c->stop_armed) c->persist_base.push_back({c->iter, slot0, c->rcur});   // (device-stop correction)
     c->iter += n;            // uot_get_report corrects it if the device stopped early
     c->persist_launches++;
     return UOT_OK;
@@ -843,8 +847,17 @@ static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
     return UOT_OK;
 }
 
+// Small grids: the SMEM-resident persistent kernel, unless k_iter2 serves the fixed-
+// marginal problem and it has more than kPersistMaxPx pair-pixels (measured: C2, 512^2,
+// 5.5 us/iteration with k_iter2 vs 8.8 with k_persist; C1, 64^2: k_persist 2x faster).
+static const long long kPersistMaxPx = 65536;
+static bool use_persist(const uot_ctx* c) {
+    if (!c->pg.ok) return false;
+    return !(c->t2ok && c->t2on && (long long)c->G * c->N > kPersistMaxPx);
+}
+
 static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
-    if (c->pg.ok && n >= 2) return launch_persist(c, n, reduce_every, reduce_last, stop, tol);
+    if (use_persist(c) && n >= 2) return launch_persist(c, n, reduce_every, reduce_last, stop, tol);
     const bool poll = stop != nullptr && n > 2 * kPollChunk && c->poll.init();
     if (poll) c->poll.begin();
     auto need_red = [&](int k) {
@@ -909,6 +922,7 @@ int uot_iterate(uot_ctx* c, int32_t n, int32_t check_every, double tol) {
         stop = c->stop;
         c->stop_armed = true;
         c->log.clear();
+        c->persist_base.clear();
         c->log.push_back({c->iter, c->slot, c->rcur});
     }
     return launch_iters(c, n, check_every, n > 0, stop, tol);
@@ -936,10 +950,13 @@ int uot_get_report(uot_ctx* c, uot_report* out) {
             bool found = false;
             for (const auto& e : c->log)
                 if (e.iter == c->iter) { c->slot = e.slot; c->rcur = e.rcur; found = true; break; }
-            if (!found) c->slot = (int)(c->iter & 1);                     // persistent / one-iteration launches
+            if (!found)                                                   // stopped inside a persistent launch
+                for (const auto& e : c->persist_base)
+                    if (e.iter <= c->iter) { c->slot = e.slot ^ (int)((c->iter - e.iter) & 1); c->rcur = e.rcur; }
         }
         c->stop_armed = false;
         c->log.clear();
+        c->persist_base.clear();
     }
     uot_report rep;
     fill_report(c, h, &rep);
@@ -965,6 +982,7 @@ int uot_solve(uot_ctx* c, int32_t max_iters, double tol, int32_t check_every, uo
     if (rc) return rc;
     c->stop_armed = true;
     c->log.clear();
+    c->persist_base.clear();
     c->log.push_back({c->iter, c->slot, c->rcur});
     rc = launch_iters(c, max_iters, check_every, max_iters > 0, c->stop, tol);
     if (rc) return rc;
@@ -1067,6 +1085,12 @@ int uot_get_timing(uot_ctx* c, double* ms_total, int64_t* n) {
 
 int uot_state_slot(const uot_ctx* c) { return c ? c->slot : -1; }
 int uot_r_slot(const uot_ctx* c) { return c ? c->rcur : -1; }
+
+int uot_kernel_path(const uot_ctx* c) {
+    if (!c) return -1;
+    if (use_persist(c)) return 2;
+    return (c->t2ok && c->t2on) ? 1 : 0;
+}
 
 int uot_set_temporal(uot_ctx* c, int enable) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");

@@ -36,9 +36,10 @@ struct PersistArgs {
     int red_every;                    // reductions every red_every-th iteration (0: none) ...
     int red_last;                     // ... and on the last one
     long long iter0;                  // iteration count before the launch
+    int slot0;                        // ping-pong slot holding iterate iter0
     int prox;                         // T == 2 prox mode
     const float* f;
-    float* mxb[2]; float* myb[2]; float* ab[2];   // ping-pong slots; input = slot iter0&1
+    float* mxb[2]; float* myb[2]; float* ab[2];   // ping-pong slots; input = slot slot0
     float* r;
     float* xb[2]; const float* p;
     float tau1, tau2, atau1, c1, c2, c3;
@@ -116,7 +117,7 @@ k_persist(const PersistArgs A) {
     const size_t f0 = PROX ? ((size_t)(pair / A.P) * A.T + (pair % A.P)) * (size_t)A.N : 0;
 
     // ---- initial load from global (iteration iter0); halos straight from neighbours' regions
-    const int in = (int)(A.iter0 & 1);
+    const int in = A.slot0;
     const float* gmx = A.mxb[in] + po; const float* gmy = A.myb[in] + po; const float* ga = A.ab[in] + po;
     auto gidx_ok = [&](int gj, int gi) { return gj >= 0 && gj < ny && gi >= 0 && gi < nx; };
     // the (-1,-1) and (TH,TW) corners are never used: not loaded (their owners are not
@@ -369,7 +370,7 @@ k_persist(const PersistArgs A) {
     }
 
     // ---- write the final iterate (iteration iter0 + done) to its ping-pong slot
-    const int o = (int)((A.iter0 + done) & 1);
+    const int o = A.slot0 ^ (int)(done & 1);
     const float* MXc = sMX[cur]; const float* MYc = sMY[cur];
     for (int e = tid; e < TH * TW; e += nth) {
         const int jj = e / TW, ii = e % TW;

@@ -190,6 +190,11 @@ class Problem:
     def slot(self) -> int:
         return int(lib().uot_state_slot(self._ctx))
 
+    @property
+    def kernel_path(self) -> str:
+        """'k_iter' (one pass per iteration), 'k_iter2' (two per pass) or 'k_persist'."""
+        return {0: "k_iter", 1: "k_iter2", 2: "k_persist"}[int(lib().uot_kernel_path(self._ctx))]
+
     def set_temporal(self, enable: bool = True):
         """Fixed marginals: two iterations per HBM pass (k_iter2, default) or one (k_iter)."""
         check(lib().uot_set_temporal(self._ctx, int(bool(enable))), self._ctx)

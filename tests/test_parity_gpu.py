@@ -359,3 +359,30 @@ def test_temporal_device_stop_replays_slots(check):
     prob.step(9)
     ref2, _ = oracle.iterate(fr, 0.8, math.inf, tau, tau, kc + 9)
     compare(fr, {k: v.double().cpu().numpy() for k, v in prob.state().items()}, ref2)
+
+
+def test_path_switching_keeps_the_iterate():
+    """Mixing k_iter2 passes, one-pass launches and (small grid) the persistent kernel in one
+    context: the ping-pong slot / r buffer bookkeeping keeps the iterate the oracle's."""
+    fr = inputs.gen_random(1, 2, 100, 120, seed=95, kind="sparse")
+    tau = tau_for(100, 120)
+    old = os.environ.get("UOT_PERSIST")
+    os.environ["UOT_PERSIST"] = "1"
+    try:
+        prob = Problem(torch.from_numpy(fr).cuda(), 1.2, tau1=tau, tau2=tau)
+    finally:
+        if old is None:
+            os.environ.pop("UOT_PERSIST", None)
+        else:
+            os.environ["UOT_PERSIST"] = old
+    assert prob.kernel_path in ("k_iter2", "k_persist")
+    prob.step(7)                       # passes + an odd tail
+    prob.set_temporal(False)
+    path_off = prob.kernel_path
+    prob.step(6)                       # persistent (the grid fits) or one-pass launches
+    prob.set_temporal(True)
+    prob.step(9)
+    ref, _ = oracle.iterate(fr, 1.2, math.inf, tau, tau, 22)
+    st = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
+    compare(fr, st, ref)
+    assert path_off in ("k_iter", "k_persist")
