@@ -553,7 +553,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->iter = 0;
     c->launches = 0;
     c->t2h = env_int("UOT_T2_TH", kTH);
-    if (c->t2h != 16 && c->t2h != 24 && c->t2h != 48) c->t2h = 32;
+    if (c->t2h != 16 && c->t2h != 20 && c->t2h != 24 && c->t2h != 48) c->t2h = 32;
     c->t2x = (p.nx + kTW - 1) / kTW;
     c->t2y = (p.ny + c->t2h - 1) / c->t2h;
     size_t recs = part_records(c->geo, c->G, c->bpp);
@@ -576,7 +576,8 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
                al16(b.a[0]) && al16(b.a[1]) && al16(b.r) && al16(b.r_alt);
     if (c->t2ok) {
         const bool ok = c->t2h == 16 ? iter2_attr_t<16>()
-                        : (c->t2h == 24 ? iter2_attr_t<24>() : (c->t2h == 48 ? iter2_attr_t<48>() : iter2_attr_t<32>()));
+                        : (c->t2h == 20 ? iter2_attr_t<20>()
+                        : (c->t2h == 24 ? iter2_attr_t<24>() : (c->t2h == 48 ? iter2_attr_t<48>() : iter2_attr_t<32>())));
         if (!ok) {
             cudaGetLastError();
             c->t2ok = false;
@@ -823,6 +824,7 @@ static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
     }
     switch (c->t2h) {
         case 16: launch_iter2_t<16>(c, A, blocks, red); break;
+        case 20: launch_iter2_t<20>(c, A, blocks, red); break;
         case 24: launch_iter2_t<24>(c, A, blocks, red); break;
         case 48: launch_iter2_t<48>(c, A, blocks, red); break;
         default: launch_iter2_t<32>(c, A, blocks, red); break;

@@ -25,7 +25,7 @@ constexpr int kTH = 32;                             // default interior rows (ti
 template <int TH> struct T2 {
     static constexpr int RH = TH + 2 * kHalo, RA = kRW * RH;
     static constexpr size_t smem = 7 * (size_t)RA * sizeof(float);
-    static constexpr int minb = TH <= 8 ? 6 : (TH <= 16 ? 4 : (TH <= 32 ? 3 : 2));   // CTAs/SM (SMEM-bound)
+    static constexpr int minb = TH <= 8 ? 6 : (TH <= 20 ? 4 : (TH <= 32 ? 3 : 2));   // CTAs/SM (SMEM-bound)
 };
 
 struct Iter2Args {
