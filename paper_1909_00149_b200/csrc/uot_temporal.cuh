@@ -20,7 +20,7 @@ namespace uotk {
 constexpr int kTW = 64, kHalo = 2;
 constexpr int kLW = 4;                              // loaded columns left of the interior (16-B aligned)
 constexpr int kRW = kTW + 2 * kLW;                  // 72 loaded columns (18 float4), 2 extra unused
-constexpr int kT2Threads = 256;
+constexpr int kT2Threads = 320;             // 10 warps: 2 quads per thread in every phase at TH = 32
 constexpr int kTH = 32;                             // default interior rows (tile 64 x kTH)
 template <int TH> struct T2 {
     static constexpr int RH = TH + 2 * kHalo, RA = kRW * RH;
@@ -65,13 +65,13 @@ template <int TH, bool RED, bool EDGE>
 __device__ __forceinline__ void iter2_tile(const Iter2Args& A, float* sm, double* red_sh, int pair, int tile,
                                            int gi0, int gj0) {
     constexpr int kRH = T2<TH>::RH, kRA = T2<TH>::RA, kTH = TH;
-    float* MX0 = sm;            // iteration k (masked: pinned / outside = 0), later M^{k+2}
-    float* MY0 = MX0 + kRA;
-    float* R0 = MY0 + kRA;
-    float* A0 = R0 + kRA;
-    float* F = A0 + kRA;
-    float* MX1 = F + kRA;       // iteration k+1
-    float* MY1 = MX1 + kRA;
+    float* __restrict__ MX0 = sm;   // iteration k (masked: pinned / outside = 0), later M^{k+2}
+    float* __restrict__ MY0 = sm + kRA;
+    float* R0 = sm + 2 * kRA;
+    float* A0 = sm + 3 * kRA;
+    float* __restrict__ F = sm + 4 * kRA;
+    float* __restrict__ MX1 = sm + 5 * kRA;   // iteration k+1
+    float* __restrict__ MY1 = sm + 6 * kRA;
     float* R1 = R0;             // r', a' overwrite r, a in place: the a'/r' phase reads r, a
     float* A1 = A0;             // only at its own pixel, and nothing reads them afterwards
     const int nx = A.nx, ny = A.ny;
@@ -140,6 +140,7 @@ __device__ __forceinline__ void iter2_tile(const Iter2Args& A, float* sm, double
     auto ld4 = [](const float* p) { return *reinterpret_cast<const float4*>(p); };
     auto st4 = [](float* p, float a, float b, float c, float d) { *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d); };
     // ---- iteration k+1, line 3: M' on rows [0, RH-2] (needs a at +i, +j) ----------------
+#pragma unroll 2
     for (int e = threadIdx.x; e < (kRH - 1) * (kRW / 4); e += kT2Threads) {
         const int r = e / (kRW / 4), c = 4 * (e - r * (kRW / 4));
         const int idx = r * kRW + c;
@@ -164,6 +165,7 @@ __device__ __forceinline__ void iter2_tile(const Iter2Args& A, float* sm, double
     }
     __syncthreads();
     // ---- iteration k+1, lines 5-7: r', a' on rows [1, RH-2] ----------------------------
+#pragma unroll 2
     for (int e = threadIdx.x; e < (kRH - 2) * (kRW / 4); e += kT2Threads) {
         const int rr = e / (kRW / 4), r = 1 + rr, c = 4 * (e - rr * (kRW / 4));
         const int idx = r * kRW + c;
@@ -194,6 +196,7 @@ __device__ __forceinline__ void iter2_tile(const Iter2Args& A, float* sm, double
     }
     __syncthreads();
     // ---- iteration k+2, line 3: M'' on rows [1, RH-3] (into MX0/MY0) --------------------
+#pragma unroll 2
     for (int e = threadIdx.x; e < (kRH - 3) * (kRW / 4); e += kT2Threads) {
         const int rr = e / (kRW / 4), r = 1 + rr, c = 4 * (e - rr * (kRW / 4));
         const int idx = r * kRW + c;
