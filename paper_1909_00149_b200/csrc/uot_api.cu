@@ -22,6 +22,37 @@
 
 using namespace uotk;
 
+// TMA descriptor of a [G][ny][nx] fp32 plane stack, box kRW x rows x 1, zero fill out of bounds
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+static bool encode_plane_map(CUtensorMap* m, const float* base, int nx, int ny, int G, int box_rows) {
+    EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn || !base) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)G};
+    const cuuint64_t strides[2] = {(cuuint64_t)nx * 4, (cuuint64_t)nx * ny * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)kRW, (cuuint32_t)box_rows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int TH>
 static bool iter2_attr_t() {
     return cudaFuncSetAttribute((const void*)k_iter2<TH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -320,6 +351,8 @@ struct uot_ctx {
     int t2vec;           // its 16-byte loads (nx % 4 == 0, aligned planes)
     int t2x, t2y;        // its tiles per pair
     int t2h;             // its interior tile rows (8, 16, 32)
+    bool t2tma;          // its tile loads by TMA (tensor maps below)
+    CUtensorMap tm_mx[2], tm_my[2], tm_a[2], tm_r[2], tm_f;   // [G][ny][nx] views, box 72 x (t2h+4)
     struct LogE { int64_t iter; int slot, rcur; };
     std::vector<LogE> log;           // launches since the stop was armed (device-stop correction)
     std::vector<LogE> persist_base;  // state at the start of each persistent launch since arming
@@ -574,6 +607,20 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->t2on = true;
     c->t2vec = (p.nx % 4 == 0) && al16(b.f) && al16(b.mx[0]) && al16(b.mx[1]) && al16(b.my[0]) && al16(b.my[1]) &&
                al16(b.a[0]) && al16(b.a[1]) && al16(b.r) && al16(b.r_alt);
+    c->t2tma = false;
+    if (c->t2ok && c->t2vec && env_int("UOT_T2_TMA", 1) != 0) {
+        const int rows = c->t2h + 2 * kHalo;
+        bool ok = true;
+        for (int k = 0; k < 2; ++k) {
+            ok = ok && encode_plane_map(&c->tm_mx[k], b.mx[k], p.nx, p.ny, c->G, rows);
+            ok = ok && encode_plane_map(&c->tm_my[k], b.my[k], p.nx, p.ny, c->G, rows);
+            ok = ok && encode_plane_map(&c->tm_a[k], b.a[k], p.nx, p.ny, c->G, rows);
+        }
+        ok = ok && encode_plane_map(&c->tm_r[0], b.r, p.nx, p.ny, c->G, rows);
+        ok = ok && encode_plane_map(&c->tm_r[1], b.r_alt, p.nx, p.ny, c->G, rows);
+        ok = ok && encode_plane_map(&c->tm_f, b.f, p.nx, p.ny, c->G, rows);
+        c->t2tma = ok;
+    }
     if (c->t2ok) {
         const bool ok = c->t2h == 16 ? iter2_attr_t<16>()
                         : (c->t2h == 20 ? iter2_attr_t<20>()
@@ -790,9 +837,9 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
 
 extern "C++" {
 template <int TH>
-static void launch_iter2_t(uot_ctx* c, const Iter2Args& A, unsigned blocks, bool red) {
-    if (red) k_iter2<TH, true><<<blocks, kT2Threads, T2<TH>::smem, c->s>>>(A);
-    else k_iter2<TH, false><<<blocks, kT2Threads, T2<TH>::smem, c->s>>>(A);
+static void launch_iter2_t(uot_ctx* c, const Iter2Args& A, const Iter2Maps& M, unsigned blocks, bool red) {
+    if (red) k_iter2<TH, true><<<blocks, kT2Threads, T2<TH>::smem, c->s>>>(A, M);
+    else k_iter2<TH, false><<<blocks, kT2Threads, T2<TH>::smem, c->s>>>(A, M);
 }
 }
 
@@ -809,6 +856,13 @@ static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
     A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
     A.r_mode = c->r_mode; A.r_scale = c->r_scale;
     A.vec = c->t2vec;
+    A.tma = c->t2tma ? 1 : 0;
+    Iter2Maps Mp;
+    memset(&Mp, 0, sizeof(Mp));
+    if (c->t2tma) {
+        Mp.tmap[0] = c->tm_mx[in]; Mp.tmap[1] = c->tm_my[in]; Mp.tmap[2] = c->tm_r[c->rcur];
+        Mp.tmap[3] = c->tm_a[in]; Mp.tmap[4] = c->tm_f;
+    }
     A.partials = c->part; A.stop = stop;
     const unsigned blocks = (unsigned)c->G * c->t2x * c->t2y;
     cudaEvent_t e1 = nullptr;
@@ -823,11 +877,11 @@ static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
         c->ev_used += 2;
     }
     switch (c->t2h) {
-        case 16: launch_iter2_t<16>(c, A, blocks, red); break;
-        case 20: launch_iter2_t<20>(c, A, blocks, red); break;
-        case 24: launch_iter2_t<24>(c, A, blocks, red); break;
-        case 48: launch_iter2_t<48>(c, A, blocks, red); break;
-        default: launch_iter2_t<32>(c, A, blocks, red); break;
+        case 16: launch_iter2_t<16>(c, A, Mp, blocks, red); break;
+        case 20: launch_iter2_t<20>(c, A, Mp, blocks, red); break;
+        case 24: launch_iter2_t<24>(c, A, Mp, blocks, red); break;
+        case 48: launch_iter2_t<48>(c, A, Mp, blocks, red); break;
+        default: launch_iter2_t<32>(c, A, Mp, blocks, red); break;
     }
     if (e1) cudaEventRecord(e1, c->s);
     int rc = check_launch(c, "k_iter2");

@@ -13,6 +13,7 @@
 // Because neighbouring tiles read this tile's iteration-k values as their halo, the
 // outputs go to the other ping-pong slot for M, a AND to a second r buffer (r_alt).
 #pragma once
+#include <cuda.h>                   // CUtensorMap (TMA descriptors; encoded on the host)
 #include "uot_kernels.cuh"
 
 namespace uotk {
@@ -38,9 +39,43 @@ struct Iter2Args {
     int r_mode;
     float r_scale;
     int vec;                    // 16-byte loads (nx % 4 == 0, aligned planes)
+    int tma;                    // tile loads by TMA (Iter2Maps valid)
     double* partials;           // [G * tiles][kRec] when reducing
     const int* stop;
 };
+struct Iter2Maps {
+    CUtensorMap tmap[5];        // [G][ny][nx] fp32 views of Mx, My, r, a, f (inputs of this pass);
+                                // box 72 x RH x 1, out-of-bounds elements read as 0
+};
+
+// TMA: one thread arms an mbarrier with the tile's byte count and issues one 3-D bulk
+// tensor copy per plane (coordinates may be negative: out-of-grid elements are zero-filled).
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, int x, int y, int z,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+        ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(reinterpret_cast<unsigned long long>(map)),
+          "r"(x), "r"(y), "r"(z), "r"((unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
+}
 
 // async global -> shared copies; zero-fill when !valid (src-size 0)
 __device__ __forceinline__ void cp_async4(float* s, const float* g, bool valid) {
@@ -96,7 +131,9 @@ __device__ __forceinline__ void iter2_tile(const Iter2Args& A, float* sm, double
     };
 
     // ---- load the tile + halo (iteration k) -------------------------------------------
-    if (A.vec) {
+    if (A.tma) {
+        // loaded by the kernel (TMA): complete and visible
+    } else if (A.vec) {
         for (int e = threadIdx.x; e < kRH * (kRW / 4); e += kT2Threads) {
             const int r = e / (kRW / 4), c = 4 * (e - r * (kRW / 4));
             const int gi = gi0 + c, gj = gj0 + r;
@@ -122,7 +159,7 @@ __device__ __forceinline__ void iter2_tile(const Iter2Args& A, float* sm, double
             cp_async4(F + e, A.f + g, ok);
         }
     }
-    cp_async_wait_all();
+    if (!A.tma) cp_async_wait_all();
     if (EDGE) {                                      // pinned flux components read as 0 (L3)
         __syncthreads();
         for (int e = threadIdx.x; e < kRA; e += kT2Threads) {
@@ -308,9 +345,10 @@ __device__ __forceinline__ void iter2_tile(const Iter2Args& A, float* sm, double
 }
 
 template <int TH, bool RED>
-__global__ void __launch_bounds__(kT2Threads, T2<TH>::minb) k_iter2(const Iter2Args A) {
+__global__ void __launch_bounds__(kT2Threads, T2<TH>::minb) k_iter2(const Iter2Args A,
+                                                                    const __grid_constant__ Iter2Maps M) {
     constexpr int kTH = TH, kRH = T2<TH>::RH;
-    extern __shared__ float4 sm4[];
+    extern __shared__ __align__(128) float4 sm4[];
     __shared__ double red_sh[5 * (kT2Threads / 32)];
     if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
     const int tiles = A.tiles_x * A.tiles_y;
@@ -320,6 +358,19 @@ __global__ void __launch_bounds__(kT2Threads, T2<TH>::minb) k_iter2(const Iter2A
     // interior tile: every region pixel in the grid and off the pinned last row/column
     const bool edge = gi0 < 0 || gj0 < 0 || gi0 + kRW > A.nx - 1 || gj0 + kRH > A.ny - 1;
     float* sm = reinterpret_cast<float*>(sm4);
+    if (A.tma) {                                     // one thread: 5 TMA tile copies on one mbarrier
+        __shared__ alignas(8) unsigned long long tbar;
+        constexpr int kRA = T2<TH>::RA;
+        if (threadIdx.x == 0) {
+            mbar_init(&tbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            mbar_expect_tx(&tbar, 5u * kRA * (unsigned)sizeof(float));
+#pragma unroll
+            for (int q = 0; q < 5; ++q) tma_load_3d(sm + q * kRA, &M.tmap[q], gi0, gj0, pair, &tbar);
+        }
+        __syncthreads();                             // barrier initialised before anyone waits
+        mbar_wait(&tbar, 0);
+    }
     if (edge) iter2_tile<TH, RED, true>(A, sm, red_sh, pair, tile, gi0, gj0);
     else iter2_tile<TH, RED, false>(A, sm, red_sh, pair, tile, gi0, gj0);
 }
