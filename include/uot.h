@@ -189,6 +189,11 @@ int uot_objective(uot_ctx* ctx, double* per_pair, uot_report* out);
  * number of timed launches since the last call, and clears the record. */
 int uot_set_timing(uot_ctx* ctx, int enable);
 int uot_get_timing(uot_ctx* ctx, double* ms_total, int64_t* n_launches);
+/* As uot_get_timing, split by kernel: ms[k], n[k] for k = uot_kernel_path codes (0 k_iter,
+ * 1 two-iteration k_iter2 pass, 2 k_persist, 3 four-iteration pass) and 4 = the UOT-DF
+ * ADMM kernel; both arrays hold UOT_N_PATHS entries.  Clears the record. */
+#define UOT_N_PATHS 5
+int uot_get_timing_paths(uot_ctx* ctx, double* ms, int64_t* n);
 
 /* Which ping-pong slot (0/1) of mx/my/a/x holds the current iterate. */
 int uot_state_slot(const uot_ctx* ctx);
@@ -200,7 +205,8 @@ int uot_r_slot(const uot_ctx* ctx);
 int uot_set_temporal(uot_ctx* ctx, int enable);
 /* Kernel that runs the iterations of this context: 0 = k_iter (one pass per iteration),
  * 1 = k_iter2 (two iterations per pass, fixed marginals), 2 = k_persist (all iterations of
- * a call in one cooperative launch, small grids). */
+ * a call in one cooperative launch, small grids), 3 = k_iter2 with four-iteration passes
+ * (two-iteration passes / k_iter where a reduction falls inside four). */
 int uot_kernel_path(const uot_ctx* ctx);
 
 /* CUDA kernels launched by this context since creation (for accounting). */

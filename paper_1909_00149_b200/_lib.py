@@ -25,6 +25,7 @@ UOT_PART_ALL, UOT_PART_INTERIOR, UOT_PART_BOUNDARY = 0, 1, 2
 
 EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset", "uot_load_frames",
             "uot_iterate", "uot_iterate_part", "uot_get_report", "uot_prox_step", "uot_solve", "uot_objective", "uot_set_timing", "uot_get_timing",
+            "uot_get_timing_paths",
             "uot_state_slot", "uot_r_slot", "uot_set_temporal", "uot_kernel_path", "uot_launch_count",
             "uot_destroy", "uot_last_error",
             "uot_df_scratch_doubles", "uot_df_create", "uot_df_reset", "uot_df_solve", "uot_df_set_timing",
@@ -32,6 +33,7 @@ EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset
             "uot_rpca_scratch_doubles", "uot_rpca_create", "uot_rpca_reset", "uot_rpca_solve",
             "uot_rpca_set_timing", "uot_rpca_get_timing", "uot_rpca_state_slot", "uot_rpca_launch_count",
             "uot_rpca_destroy", "uot_rpca_last_error")
+UOT_N_PATHS = 5
 UOT_RPCA_MAX_T = 128
 UOT_RPCA_SIGNED = 8
 
@@ -145,6 +147,8 @@ def lib():
     L.uot_set_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]; L.uot_set_timing.restype = ctypes.c_int
     L.uot_get_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
     L.uot_get_timing.restype = ctypes.c_int
+    L.uot_get_timing_paths.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+    L.uot_get_timing_paths.restype = ctypes.c_int
     L.uot_state_slot.argtypes = [ctypes.c_void_p]; L.uot_state_slot.restype = ctypes.c_int
     L.uot_r_slot.argtypes = [ctypes.c_void_p]; L.uot_r_slot.restype = ctypes.c_int
     L.uot_set_temporal.argtypes = [ctypes.c_void_p, ctypes.c_int]; L.uot_set_temporal.restype = ctypes.c_int

@@ -53,12 +53,38 @@ static bool encode_plane_map(CUtensorMap* m, const float* base, int nx, int ny, 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int TH>
-static bool iter2_attr_t() {
-    return cudaFuncSetAttribute((const void*)k_iter2<TH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)T2<TH>::smem) == cudaSuccess &&
-           cudaFuncSetAttribute((const void*)k_iter2<TH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)T2<TH>::smem) == cudaSuccess;
+// One temporally blocked variant (S fused iterations per pass, TH interior rows per tile):
+// its kernels (without / with reductions), launch shape and TMA tensor maps.
+struct TVar {
+    int S, th, tx, ty, rows, threads;
+    size_t smem;
+    bool ok, tma;
+    const void* fn[2];
+    CUtensorMap mx[2], my[2], a[2], r[2], f;   // [G][ny][nx] views, box 72 x rows
+};
+
+template <int TH, int S, int RM>
+static bool tvar_fill(TVar& v, bool wide) {
+    using namespace uotk;
+    v.S = S; v.th = TH; v.rows = TB<TH, S>::RH; v.smem = TB<TH, S>::smem;
+    v.threads = wide ? kT2Wide : kT2Threads;
+    v.fn[0] = wide ? (const void*)k_iter2<TH, S, false, kT2Wide, RM> : (const void*)k_iter2<TH, S, false, kT2Threads, RM>;
+    v.fn[1] = wide ? (const void*)k_iter2<TH, S, true, kT2Wide, RM> : (const void*)k_iter2<TH, S, true, kT2Threads, RM>;
+    bool ok = true;
+    for (const void* f : v.fn)
+        ok = ok && cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem) == cudaSuccess;
+    return ok;
+}
+
+template <int TH, int S>
+static bool tvar_fill_m(TVar& v, bool wide, int rm) {
+    return rm == 1 ? tvar_fill<TH, S, 1>(v, wide) : (rm == 2 ? tvar_fill<TH, S, 2>(v, wide) : tvar_fill<TH, S, 0>(v, wide));
+}
+
+// Supported (S, TH): S = 2 with TH = 32; S = 4 with TH in {32, 36}.
+static bool tvar_select(TVar& v, int S, int th, bool wide, int rm) {
+    if (S == 4) return th == 32 ? tvar_fill_m<32, 4>(v, wide, rm) : tvar_fill_m<36, 4>(v, wide, rm);
+    return tvar_fill_m<32, 2>(v, wide, rm);
 }
 
 // ============================================================================ kernels
@@ -349,15 +375,14 @@ struct uot_ctx {
     bool t2ok;           // temporally blocked fixed-marginal kernel available (r_alt given)
     bool t2on;           // ... and enabled (uot_set_temporal)
     int t2vec;           // its 16-byte loads (nx % 4 == 0, aligned planes)
-    int t2x, t2y;        // its tiles per pair
-    int t2h;             // its interior tile rows (8, 16, 32)
-    bool t2tma;          // its tile loads by TMA (tensor maps below)
-    CUtensorMap tm_mx[2], tm_my[2], tm_a[2], tm_r[2], tm_f;   // [G][ny][nx] views, box 72 x (t2h+4)
+    TVar tv[2];          // its variants: [0] two iterations per pass, [1] four
+    bool t4on;           // four-iteration passes enabled (UOT_T4)
     struct LogE { int64_t iter; int slot, rcur; };
     std::vector<LogE> log;           // launches since the stop was armed (device-stop correction)
     std::vector<LogE> persist_base;  // state at the start of each persistent launch since arming
     std::vector<cudaEvent_t> ev;     // event pool, pairs (start, stop)
     size_t ev_used;
+    std::vector<int> ev_kind;        // per timed launch: uot_kernel_path code (4: UOT-DF kernel)
     char err[512];
 };
 
@@ -585,12 +610,16 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->tau1f = (float)p.tau1; c->tau2f = (float)p.tau2;
     c->iter = 0;
     c->launches = 0;
-    c->t2h = env_int("UOT_T2_TH", kTH);
-    if (c->t2h != 16 && c->t2h != 20 && c->t2h != 24 && c->t2h != 48) c->t2h = 32;
-    c->t2x = (p.nx + kTW - 1) / kTW;
-    c->t2y = (p.ny + c->t2h - 1) / c->t2h;
+    memset(c->tv, 0, sizeof(c->tv));
+    c->tv[0].th = 32;
+    c->tv[1].th = env_int("UOT_T4_TH", 36) == 32 ? 32 : 36;   // 36: measured best on C4 (3 CTAs / SM)
+    for (TVar& v : c->tv) {
+        v.tx = (p.nx + kTW - 1) / kTW;
+        v.ty = (p.ny + v.th - 1) / v.th;
+    }
     size_t recs = part_records(c->geo, c->G, c->bpp);
-    if ((size_t)c->G * c->t2x * c->t2y > recs) recs = (size_t)c->G * c->t2x * c->t2y;
+    for (const TVar& v : c->tv)
+        if ((size_t)c->G * v.tx * v.ty > recs) recs = (size_t)c->G * v.tx * v.ty;
     c->part = b.scratch;
     c->pair_it = c->part + recs * kRec;
     c->pair_obj = c->pair_it + (size_t)c->G * kRec;
@@ -607,28 +636,32 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->t2on = true;
     c->t2vec = (p.nx % 4 == 0) && al16(b.f) && al16(b.mx[0]) && al16(b.mx[1]) && al16(b.my[0]) && al16(b.my[1]) &&
                al16(b.a[0]) && al16(b.a[1]) && al16(b.r) && al16(b.r_alt);
-    c->t2tma = false;
-    if (c->t2ok && c->t2vec && env_int("UOT_T2_TMA", 1) != 0) {
-        const int rows = c->t2h + 2 * kHalo;
-        bool ok = true;
-        for (int k = 0; k < 2; ++k) {
-            ok = ok && encode_plane_map(&c->tm_mx[k], b.mx[k], p.nx, p.ny, c->G, rows);
-            ok = ok && encode_plane_map(&c->tm_my[k], b.my[k], p.nx, p.ny, c->G, rows);
-            ok = ok && encode_plane_map(&c->tm_a[k], b.a[k], p.nx, p.ny, c->G, rows);
-        }
-        ok = ok && encode_plane_map(&c->tm_r[0], b.r, p.nx, p.ny, c->G, rows);
-        ok = ok && encode_plane_map(&c->tm_r[1], b.r_alt, p.nx, p.ny, c->G, rows);
-        ok = ok && encode_plane_map(&c->tm_f, b.f, p.nx, p.ny, c->G, rows);
-        c->t2tma = ok;
-    }
+    c->t4on = env_int("UOT_T4", 1) != 0;
     if (c->t2ok) {
-        const bool ok = c->t2h == 16 ? iter2_attr_t<16>()
-                        : (c->t2h == 20 ? iter2_attr_t<20>()
-                        : (c->t2h == 24 ? iter2_attr_t<24>() : (c->t2h == 48 ? iter2_attr_t<48>() : iter2_attr_t<32>())));
-        if (!ok) {
-            cudaGetLastError();
-            c->t2ok = false;
+        const int wenv = env_int("UOT_T2_WIDE", -1);
+        for (int k = 0; k < 2; ++k) {
+            TVar& v = c->tv[k];
+            const bool wide = wenv >= 0 ? (wenv != 0) : ((long long)c->G * v.tx * v.ty <= kSMs);
+            v.ok = tvar_select(v, k ? 4 : 2, v.th, wide, c->r_mode);
+            if (!v.ok) {
+                cudaGetLastError();
+                continue;
+            }
+            v.tma = false;
+            if (c->t2vec && env_int("UOT_T2_TMA", 1) != 0) {
+                bool ok = true;
+                for (int q = 0; q < 2; ++q) {
+                    ok = ok && encode_plane_map(&v.mx[q], b.mx[q], p.nx, p.ny, c->G, v.rows);
+                    ok = ok && encode_plane_map(&v.my[q], b.my[q], p.nx, p.ny, c->G, v.rows);
+                    ok = ok && encode_plane_map(&v.a[q], b.a[q], p.nx, p.ny, c->G, v.rows);
+                }
+                ok = ok && encode_plane_map(&v.r[0], b.r, p.nx, p.ny, c->G, v.rows);
+                ok = ok && encode_plane_map(&v.r[1], b.r_alt, p.nx, p.ny, c->G, v.rows);
+                ok = ok && encode_plane_map(&v.f, b.f, p.nx, p.ny, c->G, v.rows);
+                v.tma = ok;
+            }
         }
+        if (!c->tv[0].ok) c->t2ok = false;
     }
     c->err[0] = 0;
     c->timing = false;
@@ -762,6 +795,7 @@ static int launch_one(uot_ctx* c, int part, bool red, const int* stop, double to
             cudaEventRecord(c->ev[c->ev_used], c->s);
             e1 = c->ev[c->ev_used + 1];
             c->ev_used += 2;
+            c->ev_kind.push_back(0);
         }
         if (c->geo.vec == 4) launch_iter_v<4>(c, A, red, c->prox);
         else if (c->geo.vec == 2) launch_iter_v<2>(c, A, red, c->prox);
@@ -820,6 +854,7 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
         cudaEventRecord(c->ev[c->ev_used], c->s);
         e1 = c->ev[c->ev_used + 1];
         c->ev_used += 2;
+        c->ev_kind.push_back(2);
     }
     const void* fn = c->prox ? (const void*)k_persist<true> : (const void*)k_persist<false>;
     e = cudaLaunchCooperativeKernel(fn, dim3(c->pg.ctas), dim3(c->pg.threads), args, c->pg.smem, c->s);
@@ -835,20 +870,13 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
     return UOT_OK;
 }
 
-extern "C++" {
-template <int TH>
-static void launch_iter2_t(uot_ctx* c, const Iter2Args& A, const Iter2Maps& M, unsigned blocks, bool red) {
-    if (red) k_iter2<TH, true><<<blocks, kT2Threads, T2<TH>::smem, c->s>>>(A, M);
-    else k_iter2<TH, false><<<blocks, kT2Threads, T2<TH>::smem, c->s>>>(A, M);
-}
-}
-
-// Two fixed-marginal iterations in one HBM pass (k_iter2, uot_temporal.cuh): iterations
-// iter+1, iter+2; reductions (red) for iteration iter+2.
-static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
+// S fixed-marginal iterations in one HBM pass (k_iter2<TH, S>, uot_temporal.cuh): iterations
+// iter+1 .. iter+S; reductions (red) for iteration iter+S.
+static int launch_pass(uot_ctx* c, int vi, bool red, const int* stop, double tol) {
+    const TVar& v = c->tv[vi];
     const int in = c->slot, o = in ^ 1;
     Iter2Args A{};
-    A.nx = c->nx; A.ny = c->ny; A.tiles_x = c->t2x; A.tiles_y = c->t2y; A.N = c->N;
+    A.nx = c->nx; A.ny = c->ny; A.tiles_x = v.tx; A.tiles_y = v.ty; A.N = c->N;
     A.f = c->b.f;
     A.mx_in = c->b.mx[in]; A.my_in = c->b.my[in]; A.a_in = c->b.a[in]; A.r_in = rbuf(c);
     A.mx_out = c->b.mx[o]; A.my_out = c->b.my[o]; A.a_out = c->b.a[o];
@@ -856,15 +884,15 @@ static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
     A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
     A.r_mode = c->r_mode; A.r_scale = c->r_scale;
     A.vec = c->t2vec;
-    A.tma = c->t2tma ? 1 : 0;
+    A.tma = v.tma ? 1 : 0;
     Iter2Maps Mp;
     memset(&Mp, 0, sizeof(Mp));
-    if (c->t2tma) {
-        Mp.tmap[0] = c->tm_mx[in]; Mp.tmap[1] = c->tm_my[in]; Mp.tmap[2] = c->tm_r[c->rcur];
-        Mp.tmap[3] = c->tm_a[in]; Mp.tmap[4] = c->tm_f;
+    if (v.tma) {
+        Mp.tmap[0] = v.mx[in]; Mp.tmap[1] = v.my[in]; Mp.tmap[2] = v.r[c->rcur];
+        Mp.tmap[3] = v.a[in]; Mp.tmap[4] = v.f;
     }
     A.partials = c->part; A.stop = stop;
-    const unsigned blocks = (unsigned)c->G * c->t2x * c->t2y;
+    const unsigned blocks = (unsigned)c->G * v.tx * v.ty;
     cudaEvent_t e1 = nullptr;
     if (c->timing) {
         while (c->ev_used + 2 > c->ev.size()) {
@@ -875,24 +903,22 @@ static int launch_pass(uot_ctx* c, bool red, const int* stop, double tol) {
         cudaEventRecord(c->ev[c->ev_used], c->s);
         e1 = c->ev[c->ev_used + 1];
         c->ev_used += 2;
+        c->ev_kind.push_back((v.S == 4 ? 3 : 1));
     }
-    switch (c->t2h) {
-        case 16: launch_iter2_t<16>(c, A, Mp, blocks, red); break;
-        case 20: launch_iter2_t<20>(c, A, Mp, blocks, red); break;
-        case 24: launch_iter2_t<24>(c, A, Mp, blocks, red); break;
-        case 48: launch_iter2_t<48>(c, A, Mp, blocks, red); break;
-        default: launch_iter2_t<32>(c, A, Mp, blocks, red); break;
+    {
+        void* kargs[2] = {(void*)&A, (void*)&Mp};
+        cudaLaunchKernel(v.fn[red ? 1 : 0], dim3(blocks), dim3(v.threads), kargs, v.smem, c->s);
     }
     if (e1) cudaEventRecord(e1, c->s);
     int rc = check_launch(c, "k_iter2");
     if (rc) return rc;
-    c->iter += 2;
+    c->iter += v.S;
     c->slot ^= 1;
     c->rcur ^= 1;
     log_launch(c);
     if (red) {
         ReduceArgs R{};
-        R.partials = c->part; R.recs_per_pair = c->t2x * c->t2y; R.G = c->G;
+        R.partials = c->part; R.recs_per_pair = v.tx * v.ty; R.G = c->G;
         R.pair_out = c->pair_it; R.glob = c->glob; R.counter = c->counter;
         R.stop = const_cast<int*>(stop); R.max_mask = 0u; R.is_iteration = 1; R.is_setup = 0;
         R.iteration = c->iter; R.tol = tol; R.tau1 = c->tau1;
@@ -930,8 +956,12 @@ static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, c
             }
         }
         int rc;
-        if (c->t2ok && c->t2on && n - k >= 2 && !need_red(k)) {   // two iterations per pass (reductions of the 2nd)
-            rc = launch_pass(c, need_red(k + 1), stop, tol);
+        if (c->t2ok && c->t2on && c->t4on && c->tv[1].ok && n - k >= 4 && !need_red(k) && !need_red(k + 1) &&
+            !need_red(k + 2)) {                 // four iterations per pass (reductions of the 4th)
+            rc = launch_pass(c, 1, need_red(k + 3), stop, tol);
+            k += 4;
+        } else if (c->t2ok && c->t2on && n - k >= 2 && !need_red(k)) {   // two iterations per pass
+            rc = launch_pass(c, 0, need_red(k + 1), stop, tol);
             k += 2;
         } else {
             rc = launch_one(c, UOT_PART_ALL, need_red(k), stop, tol);
@@ -1136,6 +1166,26 @@ int uot_get_timing(uot_ctx* c, double* ms_total, int64_t* n) {
     if (ms_total) *ms_total = tot;
     if (n) *n = (int64_t)(c->ev_used / 2);
     c->ev_used = 0;
+    c->ev_kind.clear();
+    return UOT_OK;
+}
+
+int uot_get_timing_paths(uot_ctx* c, double* ms, int64_t* n) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    if (!ms || !n) return fail(c, UOT_E_INVALID, "ms and n must be non-NULL");
+    cudaError_t e = cudaStreamSynchronize(c->s);
+    if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "sync: %s", cudaGetErrorString(e));
+    for (int k = 0; k < UOT_N_PATHS; ++k) { ms[k] = 0.0; n[k] = 0; }
+    for (size_t q = 0; q + 1 < c->ev_used; q += 2) {
+        float t = 0.f;
+        e = cudaEventElapsedTime(&t, c->ev[q], c->ev[q + 1]);
+        if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "cudaEventElapsedTime: %s", cudaGetErrorString(e));
+        const int k = q / 2 < c->ev_kind.size() ? c->ev_kind[q / 2] : 0;
+        ms[k] += t;
+        n[k] += 1;
+    }
+    c->ev_used = 0;
+    c->ev_kind.clear();
     return UOT_OK;
 }
 
@@ -1145,7 +1195,8 @@ int uot_r_slot(const uot_ctx* c) { return c ? c->rcur : -1; }
 int uot_kernel_path(const uot_ctx* c) {
     if (!c) return -1;
     if (use_persist(c)) return 2;
-    return (c->t2ok && c->t2on) ? 1 : 0;
+    if (!(c->t2ok && c->t2on)) return 0;
+    return (c->t4on && c->tv[1].ok) ? 3 : 1;
 }
 
 int uot_set_temporal(uot_ctx* c, int enable) {

@@ -186,6 +186,17 @@ class Problem:
         check(lib().uot_get_timing(self._ctx, ctypes.byref(ms), ctypes.byref(n)), self._ctx)
         return ms.value, n.value
 
+    PATH_NAMES = ("k_iter", "k_iter2", "k_persist", "k_iter4", "k_df")
+
+    def get_timing_paths(self):
+        """{kernel: (summed device ms, launches)} of the timed launches, split by kernel
+        (k_iter2 = two-iteration passes, k_iter4 = four-iteration passes); clears."""
+        from ._lib import UOT_N_PATHS
+        ms = (ctypes.c_double * UOT_N_PATHS)()
+        n = (ctypes.c_int64 * UOT_N_PATHS)()
+        check(lib().uot_get_timing_paths(self._ctx, ms, n), self._ctx)
+        return {self.PATH_NAMES[k]: (ms[k], n[k]) for k in range(UOT_N_PATHS) if n[k]}
+
     @property
     def slot(self) -> int:
         return int(lib().uot_state_slot(self._ctx))
@@ -193,7 +204,7 @@ class Problem:
     @property
     def kernel_path(self) -> str:
         """'k_iter' (one pass per iteration), 'k_iter2' (two per pass) or 'k_persist'."""
-        return {0: "k_iter", 1: "k_iter2", 2: "k_persist"}[int(lib().uot_kernel_path(self._ctx))]
+        return {0: "k_iter", 1: "k_iter2", 2: "k_persist", 3: "k_iter4"}[int(lib().uot_kernel_path(self._ctx))]
 
     def set_temporal(self, enable: bool = True):
         """Fixed marginals: two iterations per HBM pass (k_iter2, default) or one (k_iter)."""

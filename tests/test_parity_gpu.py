@@ -95,7 +95,8 @@ PATHS = [dict(UOT_VEC=1, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
          dict(UOT_VEC=4, UOT_SEG_H=7, UOT_PERSIST=0, UOT_TEMPORAL=0),
          dict(UOT_VEC=4, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
          dict(UOT_VEC=2, UOT_SEG_H=5, UOT_PERSIST=0, UOT_TEMPORAL=0),
-         dict(UOT_PERSIST=0, UOT_TEMPORAL=1), dict(UOT_PERSIST=1)]
+         dict(UOT_PERSIST=0, UOT_TEMPORAL=1), dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_T4=0),
+         dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_T4_TH=32, UOT_T2_WIDE=0), dict(UOT_PERSIST=1)]
 
 
 @pytest.mark.parametrize("env", PATHS, ids=lambda e: "-".join(f"{k[4:]}{v}" for k, v in e.items()))
@@ -310,16 +311,26 @@ def test_persistent_solve_stops_on_device():
 
 
 # ------------------------------------------------------------------------- temporal blocking (k_iter2)
-@pytest.mark.parametrize("n,check", [(40, 10), (41, 10), (35, 7), (12, 0)])
-def test_temporal_matches_streaming_and_oracle(n, check):
-    """Two iterations per HBM pass (k_iter2) give the one-iteration kernel's iterates (to
-    fp32 rounding; same arithmetic per iteration) and the oracle's, with reductions on
-    aligned (every 10) and misaligned (every 7: single launches fill in) iterations and
-    an odd tail; tiles ragged in both directions (150 x 200 = 2.3 x 4.7 tiles)."""
+# temporal variants: four-iteration passes (tile rows 36 / 32), two-iteration passes only,
+# 320- or 640-thread CTAs
+TVARS = [dict(UOT_T4=1), dict(UOT_T4=1, UOT_T4_TH=32, UOT_T2_WIDE=0), dict(UOT_T4=1, UOT_T2_WIDE=1),
+         dict(UOT_T4=0), dict(UOT_T4=0, UOT_T2_WIDE=0)]
+
+
+@pytest.mark.parametrize("tvar", TVARS, ids=lambda e: "-".join(f"{k[4:]}{v}" for k, v in e.items()))
+@pytest.mark.parametrize("n,check", [(40, 10), (41, 10), (35, 7), (12, 0), (23, 12)])
+def test_temporal_matches_streaming_and_oracle(n, check, tvar):
+    """S iterations per HBM pass (k_iter2<TH, S>, S = 4 and 2) give the one-iteration
+    kernel's iterates (to fp32 rounding; same arithmetic per iteration) and the oracle's,
+    with reductions on aligned (every 10: 4 + 4 + 2) and misaligned (every 7: two-iteration
+    passes and single launches fill in) iterations and odd tails; tiles ragged in both
+    directions (150 x 200 = 2.3 x 4.7 .. 12.5 tiles)."""
     fr = inputs.gen_random(2, 3, 150, 200, seed=91, kind="sparse")
     tau = tau_for(150, 200)
     _, st_s, rep_s = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 0}, check_every=check)
-    prob, st_t, rep_t = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 1}, check_every=check)
+    prob, st_t, rep_t = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 1, **tvar},
+                                check_every=check)
+    assert prob.kernel_path == ("k_iter4" if tvar["UOT_T4"] else "k_iter2")
     for k in ("mx", "my", "r", "a"):
         scale = max(np.abs(st_s[k]).max(), 1e-30)
         assert np.abs(st_t[k] - st_s[k]).max() <= 1e-5 * scale, k
@@ -332,7 +343,7 @@ def test_temporal_matches_streaming_and_oracle(n, check):
     assert np.all(st_t["mx"][..., -1] == 0) and np.all(st_t["my"][..., -1, :] == 0)
 
 
-@pytest.mark.parametrize("check", [10, 7])
+@pytest.mark.parametrize("check", [10, 7, 12])
 def test_temporal_device_stop_replays_slots(check):
     """A device-side stop inside a run of k_iter2 passes: the returned state is iterate
     k_c (the r buffer and ping-pong slot are recovered from the launch log)."""
@@ -375,7 +386,7 @@ def test_path_switching_keeps_the_iterate():
             os.environ.pop("UOT_PERSIST", None)
         else:
             os.environ["UOT_PERSIST"] = old
-    assert prob.kernel_path in ("k_iter2", "k_persist")
+    assert prob.kernel_path in ("k_iter2", "k_iter4", "k_persist")
     prob.step(7)                       # passes + an odd tail
     prob.set_temporal(False)
     path_off = prob.kernel_path
