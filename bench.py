@@ -345,8 +345,10 @@ def main():
         avg_launch_s = (dom_ms / max(dom_n, 1)) / 1e3
     achieved = alg_bytes_launch / avg_launch_s / 1e9
     path = prob.kernel_path
-    temporal = path in ("k_iter2", "k_iter4")
-    kernel_name = {"k_iter4": "k_iter2<36, S=4> (four fused Alg.1 iterations per HBM pass, SMEM tiles)",
+    temporal = path in ("k_iter2", "k_iter4", "k_wave2", "k_wave4")
+    kernel_name = {"k_wave4": "k_wave<S=4> (four fused Alg.1 iterations per HBM pass, register wavefront)",
+                   "k_wave2": "k_wave<S=2> (two fused Alg.1 iterations per HBM pass, register wavefront)",
+                   "k_iter4": "k_iter2<36, S=4> (four fused Alg.1 iterations per HBM pass, SMEM tiles)",
                    "k_iter2": "k_iter2<32, S=2> (two fused Alg.1 iterations per HBM pass, SMEM tiles)",
                    "k_persist": "k_persist (all iterations in one cooperative launch, SMEM-resident)"}.get(
         dom, f"k_iter<{'prox' if prox else 'fixed'}> (fused Alg.1 iteration)")

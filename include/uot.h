@@ -190,9 +190,10 @@ int uot_objective(uot_ctx* ctx, double* per_pair, uot_report* out);
 int uot_set_timing(uot_ctx* ctx, int enable);
 int uot_get_timing(uot_ctx* ctx, double* ms_total, int64_t* n_launches);
 /* As uot_get_timing, split by kernel: ms[k], n[k] for k = uot_kernel_path codes (0 k_iter,
- * 1 two-iteration k_iter2 pass, 2 k_persist, 3 four-iteration pass) and 4 = the UOT-DF
- * ADMM kernel; both arrays hold UOT_N_PATHS entries.  Clears the record. */
-#define UOT_N_PATHS 5
+ * 1 / 3 two- / four-iteration k_iter2 pass, 2 k_persist, 5 / 6 two- / four-iteration k_wave
+ * pass) and 4 = the UOT-DF ADMM kernel; both arrays hold UOT_N_PATHS entries.  Clears the
+ * record. */
+#define UOT_N_PATHS 7
 int uot_get_timing_paths(uot_ctx* ctx, double* ms, int64_t* n);
 
 /* Which ping-pong slot (0/1) of mx/my/a/x holds the current iterate. */
@@ -204,9 +205,11 @@ int uot_r_slot(const uot_ctx* ctx);
  * Returns UOT_E_INVALID if k_iter2 is unavailable and enable != 0. */
 int uot_set_temporal(uot_ctx* ctx, int enable);
 /* Kernel that runs the iterations of this context: 0 = k_iter (one pass per iteration),
- * 1 = k_iter2 (two iterations per pass, fixed marginals), 2 = k_persist (all iterations of
- * a call in one cooperative launch, small grids), 3 = k_iter2 with four-iteration passes
- * (two-iteration passes / k_iter where a reduction falls inside four). */
+ * 1 = k_iter2 (SMEM tiles, two iterations per pass, fixed marginals), 2 = k_persist (all
+ * iterations of a call in one cooperative launch, small grids), 3 = k_iter2 with
+ * four-iteration passes, 5 / 6 = k_wave (register wavefront, 16-byte-aligned planes with
+ * nx % 4 == 0) with two / four iterations per pass.  Four-iteration contexts fill in with
+ * two-iteration passes / k_iter where a reduction falls inside four iterations. */
 int uot_kernel_path(const uot_ctx* ctx);
 
 /* CUDA kernels launched by this context since creation (for accounting). */

@@ -19,6 +19,7 @@
 #include "uot_kernels.cuh"
 #include "uot_persist.cuh"
 #include "uot_temporal.cuh"
+#include "uot_wave.cuh"
 
 using namespace uotk;
 
@@ -59,6 +60,7 @@ struct TVar {
     int S, th, tx, ty, rows, threads;
     size_t smem;
     bool ok, tma;
+    bool wave;                                 // register wavefront k_wave (tx strips x ty segments of th rows)
     const void* fn[2];
     CUtensorMap mx[2], my[2], a[2], r[2], f;   // [G][ny][nx] views, box 72 x rows
 };
@@ -74,6 +76,23 @@ static bool tvar_fill(TVar& v, bool wide) {
     for (const void* f : v.fn)
         ok = ok && cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem) == cudaSuccess;
     return ok;
+}
+
+template <int S, int RM>
+static bool wvar_fill(TVar& v) {
+    using namespace uotk;
+    v.S = S; v.wave = true; v.tma = false; v.threads = kWaveWarps * 32; v.smem = kWaveSmem;
+    v.fn[0] = (const void*)k_wave<S, RM, false>;
+    v.fn[1] = (const void*)k_wave<S, RM, true>;
+    bool ok = true;
+    for (const void* f : v.fn)
+        ok = ok && cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem) == cudaSuccess;
+    return ok;
+}
+
+static bool wvar_select(TVar& v, int S, int rm) {
+    if (S == 4) return rm == 1 ? wvar_fill<4, 1>(v) : (rm == 2 ? wvar_fill<4, 2>(v) : wvar_fill<4, 0>(v));
+    return rm == 1 ? wvar_fill<2, 1>(v) : (rm == 2 ? wvar_fill<2, 2>(v) : wvar_fill<2, 0>(v));
 }
 
 template <int TH, int S>
@@ -613,8 +632,17 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     memset(c->tv, 0, sizeof(c->tv));
     c->tv[0].th = 32;
     c->tv[1].th = env_int("UOT_T4_TH", 36) == 32 ? 32 : 36;   // 36: measured best on C4 (3 CTAs / SM)
+    // register wavefront (k_wave) for 16-byte-aligned planes with nx % 4 == 0 (UOT_WAVE=0: SMEM tiles)
+    const bool wave = env_int("UOT_WAVE", 1) != 0 && (p.nx % 4 == 0);
+    const int wave_h = std::max(16, env_int("UOT_WAVE_H", 128));   // >= 16: records within uot_scratch_doubles
     for (TVar& v : c->tv) {
-        v.tx = (p.nx + kTW - 1) / kTW;
+        v.wave = wave;
+        if (wave) {
+            v.th = wave_h;
+            v.tx = (p.nx + kWaveOut - 1) / kWaveOut;
+        } else {
+            v.tx = (p.nx + kTW - 1) / kTW;
+        }
         v.ty = (p.ny + v.th - 1) / v.th;
     }
     size_t recs = part_records(c->geo, c->G, c->bpp);
@@ -642,13 +670,19 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
         for (int k = 0; k < 2; ++k) {
             TVar& v = c->tv[k];
             const bool wide = wenv >= 0 ? (wenv != 0) : ((long long)c->G * v.tx * v.ty <= kSMs);
-            v.ok = tvar_select(v, k ? 4 : 2, v.th, wide, c->r_mode);
+            if (v.wave && !c->t2vec) {          // unaligned planes: SMEM tiles
+                v.wave = false;
+                v.th = k ? (env_int("UOT_T4_TH", 36) == 32 ? 32 : 36) : 32;
+                v.tx = (p.nx + kTW - 1) / kTW;
+                v.ty = (p.ny + v.th - 1) / v.th;
+            }
+            v.ok = v.wave ? wvar_select(v, k ? 4 : 2, c->r_mode) : tvar_select(v, k ? 4 : 2, v.th, wide, c->r_mode);
             if (!v.ok) {
                 cudaGetLastError();
                 continue;
             }
             v.tma = false;
-            if (c->t2vec && env_int("UOT_T2_TMA", 1) != 0) {
+            if (!v.wave && c->t2vec && env_int("UOT_T2_TMA", 1) != 0) {
                 bool ok = true;
                 for (int q = 0; q < 2; ++q) {
                     ok = ok && encode_plane_map(&v.mx[q], b.mx[q], p.nx, p.ny, c->G, v.rows);
@@ -892,7 +926,16 @@ static int launch_pass(uot_ctx* c, int vi, bool red, const int* stop, double tol
         Mp.tmap[3] = v.a[in]; Mp.tmap[4] = v.f;
     }
     A.partials = c->part; A.stop = stop;
-    const unsigned blocks = (unsigned)c->G * v.tx * v.ty;
+    WaveArgs W{};
+    if (v.wave) {
+        W.nx = c->nx; W.ny = c->ny; W.strips = v.tx; W.segs = v.ty; W.H = v.th; W.G = c->G; W.N = c->N;
+        W.f = A.f; W.mx_in = A.mx_in; W.my_in = A.my_in; W.a_in = A.a_in; W.r_in = A.r_in;
+        W.mx_out = A.mx_out; W.my_out = A.my_out; W.a_out = A.a_out; W.r_out = A.r_out;
+        W.tau1 = A.tau1; W.tau2 = A.tau2; W.atau1 = A.atau1; W.r_scale = A.r_scale;
+        W.partials = c->part; W.stop = stop;
+    }
+    const long long units = (long long)c->G * v.tx * v.ty;
+    const unsigned blocks = (unsigned)(v.wave ? (units + kWaveWarps - 1) / kWaveWarps : units);
     cudaEvent_t e1 = nullptr;
     if (c->timing) {
         while (c->ev_used + 2 > c->ev.size()) {
@@ -903,9 +946,12 @@ static int launch_pass(uot_ctx* c, int vi, bool red, const int* stop, double tol
         cudaEventRecord(c->ev[c->ev_used], c->s);
         e1 = c->ev[c->ev_used + 1];
         c->ev_used += 2;
-        c->ev_kind.push_back((v.S == 4 ? 3 : 1));
+        c->ev_kind.push_back(v.wave ? (v.S == 4 ? 6 : 5) : (v.S == 4 ? 3 : 1));
     }
-    {
+    if (v.wave) {
+        void* kargs[1] = {(void*)&W};
+        cudaLaunchKernel(v.fn[red ? 1 : 0], dim3(blocks), dim3(v.threads), kargs, v.smem, c->s);
+    } else {
         void* kargs[2] = {(void*)&A, (void*)&Mp};
         cudaLaunchKernel(v.fn[red ? 1 : 0], dim3(blocks), dim3(v.threads), kargs, v.smem, c->s);
     }
@@ -1196,7 +1242,9 @@ int uot_kernel_path(const uot_ctx* c) {
     if (!c) return -1;
     if (use_persist(c)) return 2;
     if (!(c->t2ok && c->t2on)) return 0;
-    return (c->t4on && c->tv[1].ok) ? 3 : 1;
+    const bool four = c->t4on && c->tv[1].ok;
+    const TVar& v = c->tv[four ? 1 : 0];
+    return v.wave ? (four ? 6 : 5) : (four ? 3 : 1);
 }
 
 int uot_set_temporal(uot_ctx* c, int enable) {

@@ -1,0 +1,190 @@
+// uot_wave.cuh -- S fixed-marginal Algorithm-1 iterations per HBM pass as a register
+// wavefront (arXiv 1909.00149, Alg. 1 lines 3, 5-7; rho = inf).
+//
+// One warp owns a strip of 128 columns (32 lanes x one float4 quad) and marches down H + 2S
+// rows of one pair.  At step t it receives row t of the iterate (M, r, a, f; cp.async into a
+// per-warp SMEM ring, 3..5 rows ahead) and advances every level j = 1..S by one row: level
+// j updates row t - j from level j-1's rows t - j (carried in registers) and t - j + 1 (just
+// produced), so the S iterations run as a wavefront with no block barrier and no SMEM
+// traffic beyond the ring.  Horizontal neighbours (a at i+1 for div^*, M_x at i-1 for div)
+// come from the adjacent lane by shuffle; vertical ones are the carried rows.  Each
+// iteration invalidates one more column at each strip side, so lanes 0 and 31 (4 columns
+// each) are halo and the warp writes the 120 columns of lanes 1..30 (S <= 4); the S rows
+// above / below the H output rows are halo likewise (re-read from L2 by the neighbours).
+// K^{j-1} (line 7's previous K) is carried with the level, so div M is evaluated once per
+// pixel and iteration.  The arithmetic per pixel is k_iter's, in the same order.
+// HBM traffic: 36 B per pair-pixel per S iterations (+ 6.7% column and 2S/H row halo, L2).
+#pragma once
+#include "uot_temporal.cuh"
+
+namespace uotk {
+
+constexpr int kWaveOut = 120;                   // columns written per warp strip (lanes 1..30)
+constexpr int kWaveRing = 8;                    // rows per warp in the SMEM ring
+constexpr int kWaveWarps = 2;                   // warps (independent strips) per CTA
+constexpr int kWaveMinBlocks = 5;               // 10 warps / SM (registers: <= 204 per thread)
+constexpr size_t kWaveSmem = (size_t)kWaveWarps * kWaveRing * 5 * 32 * sizeof(float4);   // 40 KB
+
+struct WaveArgs {
+    int nx, ny;                 // nx % 4 == 0, 16-byte aligned planes
+    int strips, segs, H;        // units per pair: strips x segs (segment = H output rows)
+    int G;
+    long long N;
+    const float* f;
+    const float* mx_in; const float* my_in; const float* a_in; const float* r_in;
+    float* mx_out; float* my_out; float* a_out; float* r_out;
+    float tau1, tau2, atau1, r_scale;
+    double* partials;           // [G][strips * segs][kRec] when reducing
+    const int* stop;
+};
+
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ float f4c(const float4& q, int v) { return v == 0 ? q.x : (v == 1 ? q.y : (v == 2 ? q.z : q.w)); }
+
+template <int S, int RM, bool RED>
+__global__ void __launch_bounds__(kWaveWarps * 32, kWaveMinBlocks) k_wave(const WaveArgs A) {
+    static_assert(S >= 1 && S <= 4, "lanes 0 and 31 hold a 4-column halo");
+    constexpr int P = kWaveRing - S - 1;        // rows in flight ahead of the current one
+    extern __shared__ __align__(16) float4 wring[];
+    if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int upp = A.strips * A.segs;
+    const long long unit = (long long)blockIdx.x * kWaveWarps + w;
+    if (unit >= (long long)A.G * upp) return;   // whole warp: no block-level synchronisation below
+    const int pair = (int)(unit / upp), u = (int)(unit - (long long)pair * upp);
+    const int sy = u / A.strips, sx = u - sy * A.strips;
+    const int nx = A.nx, ny = A.ny;
+    const int gi = sx * kWaveOut - 4 + 4 * lane;                 // first column of this lane's quad
+    const bool lane_in = gi >= 0 && gi < nx;                     // whole quad in the grid (nx % 4 == 0)
+    const bool last_q = gi + 3 == nx - 1;                        // holds the pinned column nx-1 (L3)
+    const bool writer = lane >= 1 && lane <= 30 && lane_in;
+    const int y0 = sy * A.H, y1 = min(y0 + A.H, ny);             // output rows [y0, y1)
+    const size_t po = (size_t)pair * (size_t)A.N;
+    const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1;
+    float4* ring = wring + (size_t)w * (kWaveRing * 5 * 32) + lane;   // [slot][plane][lane]
+
+    auto issue = [&](int t) {                                    // row t -> slot t & 7 (zero outside)
+        const bool ok = lane_in && t >= 0 && t < ny;
+        const size_t g = ok ? po + (size_t)t * nx + gi : po;
+        float4* s = ring + (t & (kWaveRing - 1)) * (5 * 32);
+        cp_async16(reinterpret_cast<float*>(s), A.mx_in + g, ok);
+        cp_async16(reinterpret_cast<float*>(s + 32), A.my_in + g, ok);
+        cp_async16(reinterpret_cast<float*>(s + 64), A.r_in + g, ok);
+        cp_async16(reinterpret_cast<float*>(s + 96), A.a_in + g, ok);
+        cp_async16(reinterpret_cast<float*>(s + 128), A.f + g, ok);
+        cp_commit();
+    };
+
+    const int t0 = y0 - S, t1r = y1 - 1 + S;
+#pragma unroll
+    for (int p = 0; p < P; ++p) issue(t0 + p);
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 pMx[S], pMy[S], pR[S], pA[S], pK[S];   // level j-1's outputs at row t-j (index j-1)
+    float4 upY[S + 1];                            // level j's M_y at its previous row
+#pragma unroll
+    for (int j = 0; j < S; ++j) { pMx[j] = z4; pMy[j] = z4; pR[j] = z4; pA[j] = z4; pK[j] = z4; }
+#pragma unroll
+    for (int j = 0; j <= S; ++j) upY[j] = z4;
+    float s_tr = 0.f, s_gr = 0.f, s_k2 = 0.f, s_dz = 0.f, s_ub = 0.f;
+
+    for (int t = t0; t <= t1r; ++t) {
+        if (t + P <= t1r) issue(t + P);
+        else cp_commit();                                        // empty group: uniform wait count
+        cp_wait<P>();                                            // row t has landed (own lane's copies)
+        const float4* s = ring + (t & (kWaveRing - 1)) * (5 * 32);
+        float4 Mx = s[0], My = s[32];
+        const float4 R = s[64], Aa = s[96], F = s[128];
+        if (last_q) Mx.w = 0.f;                                  // pinned flux components (L3)
+        if (t == ny - 1) My = z4;
+        // ---- level 0: K^0 = div M - r - f at row t ----
+        const float mxl0 = __shfl_up_sync(kFull, Mx.w, 1);
+        float4 K;
+        K.x = ((Mx.x - mxl0) + (My.x - upY[0].x)) - R.x - F.x;
+        K.y = ((Mx.y - Mx.x) + (My.y - upY[0].y)) - R.y - F.y;
+        K.z = ((Mx.z - Mx.y) + (My.z - upY[0].z)) - R.z - F.z;
+        K.w = ((Mx.w - Mx.z) + (My.w - upY[0].w)) - R.w - F.w;
+        upY[0] = My;
+        float4 cMx = Mx, cMy = My, cR = R, cA = Aa, cK = K;     // level j-1 at row t-j+1
+#pragma unroll
+        for (int j = 1; j <= S; ++j) {
+            const int rho = t - j;
+            const float4 qmx = pMx[j - 1], qmy = pMy[j - 1], qr = pR[j - 1], qa = pA[j - 1], qk = pK[j - 1];
+            pMx[j - 1] = cMx; pMy[j - 1] = cMy; pR[j - 1] = cR; pA[j - 1] = cA; pK[j - 1] = cK;
+            const bool rin = (unsigned)rho < (unsigned)ny, rry = (unsigned)rho < (unsigned)(ny - 1);
+            // line 3: M^j(rho) = prox(M^{j-1} - tau1 div^* a^{j-1}); a at (rho, i+1) and (rho+1, i)
+            const float a5 = __shfl_down_sync(kFull, qa.x, 1);
+            const float av[5] = {qa.x, qa.y, qa.z, qa.w, a5};
+            float nmx[4], nmy[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const bool cx = rin && lane_in && !(v == 3 && last_q);
+                const bool cy = rry && lane_in;
+                const float gx = cx ? av[v] - av[v + 1] : 0.f;
+                const float gy = cy ? av[v] - f4c(cA, v) : 0.f;
+                const float qx = f4c(qmx, v) - t1 * gx;
+                const float qy = f4c(qmy, v) - t1 * gy;
+                const float n2 = qx * qx + qy * qy;
+                const float sf = shrink_factor(n2, rsqrtf(n2), t1);
+                nmx[v] = sf * qx;
+                nmy[v] = sf * qy;
+            }
+            // lines 5-7: r^j, a^j, K^j at rho from M^j (left neighbour by shuffle, up carried)
+            const float mxl = __shfl_up_sync(kFull, nmx[3], 1);
+            const float4 Fr = ring[(rho & (kWaveRing - 1)) * (5 * 32) + 128];
+            const bool in = rin && lane_in;
+            const float mxv[5] = {mxl, nmx[0], nmx[1], nmx[2], nmx[3]};
+            float rn[4], an[4], kn[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                rn[v] = in ? r_update(fmaf(t1, f4c(qa, v), f4c(qr, v)), RM, at1, A.r_scale) : 0.f;
+                const float divn = (mxv[v + 1] - mxv[v]) + (nmy[v] - f4c(upY[j], v));
+                kn[v] = divn - rn[v] - f4c(Fr, v);
+                an[v] = in ? fmaf(t2, 2.f * kn[v] - f4c(qk, v), f4c(qa, v)) : 0.f;
+                if (RED && j == S) {
+                    if (writer && rho >= y0 && rho < y1) {
+                        const float dmx = nmx[v] - f4c(qmx, v), dmy = nmy[v] - f4c(qmy, v), dr = rn[v] - f4c(qr, v);
+                        s_tr += sqrtf(nmx[v] * nmx[v] + nmy[v] * nmy[v]);
+                        s_gr += pw(rn[v], RM);
+                        s_k2 += kn[v] * kn[v];
+                        s_dz += dmx * dmx + dmy * dmy + dr * dr;
+                        s_ub += pw(divn - f4c(Fr, v), RM);
+                    }
+                }
+            }
+            upY[j] = make_float4(nmy[0], nmy[1], nmy[2], nmy[3]);
+            if (j < S) {
+                cMx = make_float4(nmx[0], nmx[1], nmx[2], nmx[3]);
+                cMy = upY[j];
+                cR = make_float4(rn[0], rn[1], rn[2], rn[3]);
+                cA = make_float4(an[0], an[1], an[2], an[3]);
+                cK = make_float4(kn[0], kn[1], kn[2], kn[3]);
+            } else if (writer && rho >= y0 && rho < y1) {
+                const size_t g = po + (size_t)rho * nx + gi;
+                *reinterpret_cast<float4*>(A.mx_out + g) = make_float4(nmx[0], nmx[1], nmx[2], nmx[3]);
+                *reinterpret_cast<float4*>(A.my_out + g) = upY[j];
+                *reinterpret_cast<float4*>(A.r_out + g) = make_float4(rn[0], rn[1], rn[2], rn[3]);
+                *reinterpret_cast<float4*>(A.a_out + g) = make_float4(an[0], an[1], an[2], an[3]);
+            }
+        }
+    }
+    cp_wait<0>();
+    if constexpr (RED) {                                         // fixed-order warp sums -> one record
+        double v[5] = {s_tr, s_gr, s_k2, s_dz, s_ub};
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(kFull, v[q], o);
+        }
+        if (lane == 0) {
+            double* Pp = A.partials + ((size_t)pair * upp + u) * kRec;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) Pp[q] = v[q];
+            Pp[5] = 0.0; Pp[6] = 0.0; Pp[7] = 0.0;
+        }
+    }
+}
+
+}  // namespace uotk

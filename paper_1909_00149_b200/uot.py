@@ -186,7 +186,7 @@ class Problem:
         check(lib().uot_get_timing(self._ctx, ctypes.byref(ms), ctypes.byref(n)), self._ctx)
         return ms.value, n.value
 
-    PATH_NAMES = ("k_iter", "k_iter2", "k_persist", "k_iter4", "k_df")
+    PATH_NAMES = ("k_iter", "k_iter2", "k_persist", "k_iter4", "k_df", "k_wave2", "k_wave4")
 
     def get_timing_paths(self):
         """{kernel: (summed device ms, launches)} of the timed launches, split by kernel
@@ -203,8 +203,9 @@ class Problem:
 
     @property
     def kernel_path(self) -> str:
-        """'k_iter' (one pass per iteration), 'k_iter2' (two per pass) or 'k_persist'."""
-        return {0: "k_iter", 1: "k_iter2", 2: "k_persist", 3: "k_iter4"}[int(lib().uot_kernel_path(self._ctx))]
+        """'k_iter' (one pass per iteration), 'k_iter2' / 'k_iter4' (SMEM tiles, two / four
+        iterations per pass), 'k_wave2' / 'k_wave4' (register wavefront) or 'k_persist'."""
+        return self.PATH_NAMES[int(lib().uot_kernel_path(self._ctx))]
 
     def set_temporal(self, enable: bool = True):
         """Fixed marginals: two iterations per HBM pass (k_iter2, default) or one (k_iter)."""

@@ -96,7 +96,8 @@ PATHS = [dict(UOT_VEC=1, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
          dict(UOT_VEC=4, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
          dict(UOT_VEC=2, UOT_SEG_H=5, UOT_PERSIST=0, UOT_TEMPORAL=0),
          dict(UOT_PERSIST=0, UOT_TEMPORAL=1), dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_T4=0),
-         dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_T4_TH=32, UOT_T2_WIDE=0), dict(UOT_PERSIST=1)]
+         dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=0),
+         dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=0, UOT_T4_TH=32, UOT_T2_WIDE=0), dict(UOT_PERSIST=1)]
 
 
 @pytest.mark.parametrize("env", PATHS, ids=lambda e: "-".join(f"{k[4:]}{v}" for k, v in e.items()))
@@ -311,10 +312,11 @@ def test_persistent_solve_stops_on_device():
 
 
 # ------------------------------------------------------------------------- temporal blocking (k_iter2)
-# temporal variants: four-iteration passes (tile rows 36 / 32), two-iteration passes only,
-# 320- or 640-thread CTAs
-TVARS = [dict(UOT_T4=1), dict(UOT_T4=1, UOT_T4_TH=32, UOT_T2_WIDE=0), dict(UOT_T4=1, UOT_T2_WIDE=1),
-         dict(UOT_T4=0), dict(UOT_T4=0, UOT_T2_WIDE=0)]
+# temporal variants: register wavefront (k_wave; segments of 128 / 16 / 24 rows) or SMEM
+# tiles (UOT_WAVE=0; tile rows 36 / 32, 320- or 640-thread CTAs), four- or two-iteration passes
+TVARS = [dict(UOT_T4=1), dict(UOT_T4=1, UOT_WAVE_H=16), dict(UOT_T4=0), dict(UOT_T4=0, UOT_WAVE_H=24),
+         dict(UOT_WAVE=0, UOT_T4=1), dict(UOT_WAVE=0, UOT_T4=1, UOT_T4_TH=32, UOT_T2_WIDE=0),
+         dict(UOT_WAVE=0, UOT_T4=1, UOT_T2_WIDE=1), dict(UOT_WAVE=0, UOT_T4=0), dict(UOT_WAVE=0, UOT_T4=0, UOT_T2_WIDE=0)]
 
 
 @pytest.mark.parametrize("tvar", TVARS, ids=lambda e: "-".join(f"{k[4:]}{v}" for k, v in e.items()))
@@ -330,7 +332,8 @@ def test_temporal_matches_streaming_and_oracle(n, check, tvar):
     _, st_s, rep_s = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 0}, check_every=check)
     prob, st_t, rep_t = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 1, **tvar},
                                 check_every=check)
-    assert prob.kernel_path == ("k_iter4" if tvar["UOT_T4"] else "k_iter2")
+    kind = "k_iter" if tvar.get("UOT_WAVE", 1) == 0 else "k_wave"
+    assert prob.kernel_path == kind + ("4" if tvar["UOT_T4"] else "2")
     for k in ("mx", "my", "r", "a"):
         scale = max(np.abs(st_s[k]).max(), 1e-30)
         assert np.abs(st_t[k] - st_s[k]).max() <= 1e-5 * scale, k
@@ -386,7 +389,7 @@ def test_path_switching_keeps_the_iterate():
             os.environ.pop("UOT_PERSIST", None)
         else:
             os.environ["UOT_PERSIST"] = old
-    assert prob.kernel_path in ("k_iter2", "k_iter4", "k_persist")
+    assert prob.kernel_path in ("k_iter2", "k_iter4", "k_wave2", "k_wave4", "k_persist")
     prob.step(7)                       # passes + an odd tail
     prob.set_temporal(False)
     path_off = prob.kernel_path
