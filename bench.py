@@ -347,6 +347,7 @@ def main():
     path = prob.kernel_path
     temporal = path in ("k_iter2", "k_iter4", "k_wave2", "k_wave4")
     kernel_name = {"k_wave4": "k_wave<S=4> (four fused Alg.1 iterations per HBM pass, register wavefront)",
+                   "k_wave3": "k_wave<S=3> (three fused Alg.1 iterations per HBM pass, register wavefront)",
                    "k_wave2": "k_wave<S=2> (two fused Alg.1 iterations per HBM pass, register wavefront)",
                    "k_iter4": "k_iter2<36, S=4> (four fused Alg.1 iterations per HBM pass, SMEM tiles)",
                    "k_iter2": "k_iter2<32, S=2> (two fused Alg.1 iterations per HBM pass, SMEM tiles)",

@@ -92,6 +92,7 @@ static bool wvar_fill(TVar& v) {
 
 static bool wvar_select(TVar& v, int S, int rm) {
     if (S == 4) return rm == 1 ? wvar_fill<4, 1>(v) : (rm == 2 ? wvar_fill<4, 2>(v) : wvar_fill<4, 0>(v));
+    if (S == 3) return rm == 1 ? wvar_fill<3, 1>(v) : (rm == 2 ? wvar_fill<3, 2>(v) : wvar_fill<3, 0>(v));
     return rm == 1 ? wvar_fill<2, 1>(v) : (rm == 2 ? wvar_fill<2, 2>(v) : wvar_fill<2, 0>(v));
 }
 
@@ -102,6 +103,7 @@ static bool tvar_fill_m(TVar& v, bool wide, int rm) {
 
 // Supported (S, TH): S = 2 with TH = 32; S = 4 with TH in {32, 36}.
 static bool tvar_select(TVar& v, int S, int th, bool wide, int rm) {
+    if (S == 3) return false;                   // SMEM tiles: two or four iterations per pass
     if (S == 4) return th == 32 ? tvar_fill_m<32, 4>(v, wide, rm) : tvar_fill_m<36, 4>(v, wide, rm);
     return tvar_fill_m<32, 2>(v, wide, rm);
 }
@@ -394,7 +396,8 @@ struct uot_ctx {
     bool t2ok;           // temporally blocked fixed-marginal kernel available (r_alt given)
     bool t2on;           // ... and enabled (uot_set_temporal)
     int t2vec;           // its 16-byte loads (nx % 4 == 0, aligned planes)
-    TVar tv[2];          // its variants: [0] two iterations per pass, [1] four
+    TVar tv[3];          // its variants: [0] two iterations per pass, [1] four, [2] three (k_wave)
+    float pass_cost[5];  // relative device time of a pass of S = 1..4 iterations (pass scheduler)
     bool t4on;           // four-iteration passes enabled (UOT_T4)
     struct LogE { int64_t iter; int slot, rcur; };
     std::vector<LogE> log;           // launches since the stop was armed (device-stop correction)
@@ -632,9 +635,21 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     memset(c->tv, 0, sizeof(c->tv));
     c->tv[0].th = 32;
     c->tv[1].th = env_int("UOT_T4_TH", 36) == 32 ? 32 : 36;   // 36: measured best on C4 (3 CTAs / SM)
+    c->tv[2].th = 32;                                           // (three-iteration passes: k_wave only)
     // register wavefront (k_wave) for 16-byte-aligned planes with nx % 4 == 0 (UOT_WAVE=0: SMEM tiles)
-    const bool wave = env_int("UOT_WAVE", 1) != 0 && (p.nx % 4 == 0);
-    const int wave_h = std::max(16, env_int("UOT_WAVE_H", 128));   // >= 16: records within uot_scratch_doubles
+    // Enough independent strips to fill the GPU: segment height 128 (64, 32 for smaller
+    // problems, >= 2 waves of 8 warps per SM); below one wave at 32 rows the SMEM tiles.
+    const long long strips = (p.nx + kWaveOut - 1) / kWaveOut;
+    int wave_h = env_int("UOT_WAVE_H", 0);
+    if (wave_h <= 0) {
+        wave_h = 128;
+        while (wave_h > 32 && (long long)c->G * strips * ((p.ny + wave_h - 1) / wave_h) < 2LL * kSMs * 8) wave_h /= 2;
+    }
+    wave_h = std::max(16, wave_h);                              // >= 16: records within uot_scratch_doubles
+    const int wenv_wave = env_int("UOT_WAVE", -1);
+    const bool wave = (p.nx % 4 == 0) &&
+                      (wenv_wave >= 0 ? wenv_wave != 0
+                                      : (long long)c->G * strips * ((p.ny + wave_h - 1) / wave_h) >= (long long)kSMs * 8);
     for (TVar& v : c->tv) {
         v.wave = wave;
         if (wave) {
@@ -667,16 +682,18 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->t4on = env_int("UOT_T4", 1) != 0;
     if (c->t2ok) {
         const int wenv = env_int("UOT_T2_WIDE", -1);
-        for (int k = 0; k < 2; ++k) {
+        static const int kVarS[3] = {2, 4, 3};
+        for (int k = 0; k < 3; ++k) {
             TVar& v = c->tv[k];
+            const int S = kVarS[k];
             const bool wide = wenv >= 0 ? (wenv != 0) : ((long long)c->G * v.tx * v.ty <= kSMs);
             if (v.wave && !c->t2vec) {          // unaligned planes: SMEM tiles
                 v.wave = false;
-                v.th = k ? (env_int("UOT_T4_TH", 36) == 32 ? 32 : 36) : 32;
+                v.th = S == 4 ? (env_int("UOT_T4_TH", 36) == 32 ? 32 : 36) : 32;
                 v.tx = (p.nx + kTW - 1) / kTW;
                 v.ty = (p.ny + v.th - 1) / v.th;
             }
-            v.ok = v.wave ? wvar_select(v, k ? 4 : 2, c->r_mode) : tvar_select(v, k ? 4 : 2, v.th, wide, c->r_mode);
+            v.ok = v.wave ? wvar_select(v, S, c->r_mode) : tvar_select(v, S, v.th, wide, c->r_mode);
             if (!v.ok) {
                 cudaGetLastError();
                 continue;
@@ -696,6 +713,21 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
             }
         }
         if (!c->tv[0].ok) c->t2ok = false;
+    }
+    {   // relative pass costs (C4 measurements): k_wave 1 : 1.11 : 1.13 : 1.29 (S = 1..4),
+        // SMEM tiles 1 : 1.46 : - : 2.19; UOT_PASS_COST="c2,c3,c4" overrides (c1 = 1)
+        const bool wv = c->tv[0].wave;
+        c->pass_cost[0] = 0.f; c->pass_cost[1] = 1.f;
+        c->pass_cost[2] = wv ? 1.11f : 1.46f;
+        c->pass_cost[3] = wv ? 1.13f : 1e9f;
+        c->pass_cost[4] = wv ? 1.29f : 2.19f;
+        const char* pc = getenv("UOT_PASS_COST");
+        if (pc) {
+            float a2, a3, a4;
+            if (sscanf(pc, "%f,%f,%f", &a2, &a3, &a4) == 3) {
+                c->pass_cost[2] = a2; c->pass_cost[3] = a3; c->pass_cost[4] = a4;
+            }
+        }
     }
     c->err[0] = 0;
     c->timing = false;
@@ -946,7 +978,7 @@ static int launch_pass(uot_ctx* c, int vi, bool red, const int* stop, double tol
         cudaEventRecord(c->ev[c->ev_used], c->s);
         e1 = c->ev[c->ev_used + 1];
         c->ev_used += 2;
-        c->ev_kind.push_back(v.wave ? (v.S == 4 ? 6 : 5) : (v.S == 4 ? 3 : 1));
+        c->ev_kind.push_back(v.wave ? (v.S == 4 ? 6 : (v.S == 3 ? 7 : 5)) : (v.S == 4 ? 3 : 1));
     }
     if (v.wave) {
         void* kargs[1] = {(void*)&W};
@@ -984,6 +1016,42 @@ static bool use_persist(const uot_ctx* c) {
     return !(c->t2ok && c->t2on && (long long)c->G * c->N > kPersistMaxPx);
 }
 
+// Temporally blocked pass of S iterations available in this context: its variant index, or -1.
+static int pass_variant(const uot_ctx* c, int S) {
+    if (!(c->t2ok && c->t2on)) return -1;
+    if (S == 2) return c->tv[0].ok ? 0 : -1;
+    if (!c->t4on) return -1;
+    if (S == 4) return c->tv[1].ok ? 1 : -1;
+    if (S == 3) return c->tv[2].ok ? 2 : -1;
+    return -1;
+}
+
+// Iterations of the first pass of the cheapest split of d iterations into passes of the
+// available S (a reduction may only follow the last pass; order is immaterial to the cost).
+static int pick_pass(const uot_ctx* c, int d) {
+    bool av[5] = {false, true, pass_variant(c, 2) >= 0, pass_variant(c, 3) >= 0, pass_variant(c, 4) >= 0};
+    if (d > 12) {                       // long runs: the best cost per iteration
+        int b = 1;
+        for (int S = 2; S <= 4; ++S)
+            if (av[S] && c->pass_cost[S] / S < c->pass_cost[b] / b) b = S;
+        return b;
+    }
+    float best[13];
+    int first[13];
+    best[0] = 0.f;
+    first[0] = 0;
+    for (int x = 1; x <= d; ++x) {
+        best[x] = 1e30f;
+        first[x] = 1;
+        for (int S = 4; S >= 1; --S)
+            if (av[S] && S <= x && c->pass_cost[S] + best[x - S] < best[x]) {
+                best[x] = c->pass_cost[S] + best[x - S];
+                first[x] = S;
+            }
+    }
+    return first[d];
+}
+
 static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
     if (use_persist(c) && n >= 2) return launch_persist(c, n, reduce_every, reduce_last, stop, tol);
     const bool poll = stop != nullptr && n > 2 * kPollChunk && c->poll.init();
@@ -1001,18 +1069,13 @@ static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, c
                 return UOT_OK;
             }
         }
-        int rc;
-        if (c->t2ok && c->t2on && c->t4on && c->tv[1].ok && n - k >= 4 && !need_red(k) && !need_red(k + 1) &&
-            !need_red(k + 2)) {                 // four iterations per pass (reductions of the 4th)
-            rc = launch_pass(c, 1, need_red(k + 3), stop, tol);
-            k += 4;
-        } else if (c->t2ok && c->t2on && n - k >= 2 && !need_red(k)) {   // two iterations per pass
-            rc = launch_pass(c, 0, need_red(k + 1), stop, tol);
-            k += 2;
-        } else {
-            rc = launch_one(c, UOT_PART_ALL, need_red(k), stop, tol);
-            k += 1;
-        }
+        // iterations up to and including the next reduction (or the end of the call)
+        int d = n - k;
+        if (reduce_every > 0) d = std::min(d, reduce_every - (k % reduce_every));
+        const int S = pick_pass(c, d);
+        const int rc = S == 1 ? launch_one(c, UOT_PART_ALL, need_red(k), stop, tol)
+                              : launch_pass(c, pass_variant(c, S), need_red(k + S - 1), stop, tol);
+        k += S;
         if (rc) return rc;
     }
     return UOT_OK;
@@ -1244,7 +1307,7 @@ int uot_kernel_path(const uot_ctx* c) {
     if (!(c->t2ok && c->t2on)) return 0;
     const bool four = c->t4on && c->tv[1].ok;
     const TVar& v = c->tv[four ? 1 : 0];
-    return v.wave ? (four ? 6 : 5) : (four ? 3 : 1);
+    return v.wave ? (four ? 6 : 5) : (four ? 3 : 1);   // the pass kind of long runs
 }
 
 int uot_set_temporal(uot_ctx* c, int enable) {

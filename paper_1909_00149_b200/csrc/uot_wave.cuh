@@ -22,7 +22,9 @@ namespace uotk {
 constexpr int kWaveOut = 120;                   // columns written per warp strip (lanes 1..30)
 constexpr int kWaveRing = 8;                    // rows per warp in the SMEM ring
 constexpr int kWaveWarps = 2;                   // warps (independent strips) per CTA
-constexpr int kWaveMinBlocks = 5;               // 10 warps / SM (registers: <= 204 per thread)
+template <int S> struct WaveCfg {               // CTAs (2 warps) per SM: registers <= 255 (S = 4) / 204
+    static constexpr int minb = S >= 4 ? 4 : 5;
+};
 constexpr size_t kWaveSmem = (size_t)kWaveWarps * kWaveRing * 5 * 32 * sizeof(float4);   // 40 KB
 
 struct WaveArgs {
@@ -42,10 +44,18 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// rsqrt without the denormal-input rescaling (n2 < 2^-126 flushes to 0 -> +inf -> shrink
+// factor 0, the value the unflushed rsqrt gives through max(1 - tau1 * huge, 0) anyway)
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ float f4c(const float4& q, int v) { return v == 0 ? q.x : (v == 1 ? q.y : (v == 2 ? q.z : q.w)); }
 
 template <int S, int RM, bool RED>
-__global__ void __launch_bounds__(kWaveWarps * 32, kWaveMinBlocks) k_wave(const WaveArgs A) {
+__global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S>::minb) k_wave(const WaveArgs A) {
     static_assert(S >= 1 && S <= 4, "lanes 0 and 31 hold a 4-column halo");
     constexpr int P = kWaveRing - S - 1;        // rows in flight ahead of the current one
     extern __shared__ __align__(16) float4 wring[];
@@ -63,7 +73,16 @@ __global__ void __launch_bounds__(kWaveWarps * 32, kWaveMinBlocks) k_wave(const 
     const bool writer = lane >= 1 && lane <= 30 && lane_in;
     const int y0 = sy * A.H, y1 = min(y0 + A.H, ny);             // output rows [y0, y1)
     const size_t po = (size_t)pair * (size_t)A.N;
-    const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1;
+    const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1, rsc = A.r_scale;
+    float* const mx_out = A.mx_out; float* const my_out = A.my_out;
+    float* const r_out = A.r_out; float* const a_out = A.a_out;
+    // Boundary handling without per-pixel masks: r, a, f, M are 0 outside the grid (zero-filled
+    // loads) and stay 0 there as long as div^* a is cut at the two places where one side of the
+    // difference is in the grid: column -1 / row -1 (outside, next to the grid) and the pinned
+    // column nx-1 / row ny-1 (L3).  Scaling tau1 by 0 there keeps those M components 0 exactly
+    // (then div M, K, r, a outside are exact zeros).  Column cut: the 4th pixel of the lane
+    // holding column -1 or nx-1; row cut: a row-uniform scale.
+    const float t1x3 = (gi + 3 == -1 || last_q) ? 0.f : t1;
     float4* ring = wring + (size_t)w * (kWaveRing * 5 * 32) + lane;   // [slot][plane][lane]
 
     auto issue = [&](int t) {                                    // row t -> slot t & 7 (zero outside)
@@ -90,6 +109,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, kWaveMinBlocks) k_wave(const 
     for (int j = 0; j <= S; ++j) upY[j] = z4;
     float s_tr = 0.f, s_gr = 0.f, s_k2 = 0.f, s_dz = 0.f, s_ub = 0.f;
 
+#pragma unroll 2                                             // the carried rows alternate registers
     for (int t = t0; t <= t1r; ++t) {
         if (t + P <= t1r) issue(t + P);
         else cp_commit();                                        // empty group: uniform wait count
@@ -113,45 +133,45 @@ __global__ void __launch_bounds__(kWaveWarps * 32, kWaveMinBlocks) k_wave(const 
             const int rho = t - j;
             const float4 qmx = pMx[j - 1], qmy = pMy[j - 1], qr = pR[j - 1], qa = pA[j - 1], qk = pK[j - 1];
             pMx[j - 1] = cMx; pMy[j - 1] = cMy; pR[j - 1] = cR; pA[j - 1] = cA; pK[j - 1] = cK;
-            const bool rin = (unsigned)rho < (unsigned)ny, rry = (unsigned)rho < (unsigned)(ny - 1);
+            const float t1y = (rho == -1 || rho == ny - 1) ? 0.f : t1;
             // line 3: M^j(rho) = prox(M^{j-1} - tau1 div^* a^{j-1}); a at (rho, i+1) and (rho+1, i)
             const float a5 = __shfl_down_sync(kFull, qa.x, 1);
             const float av[5] = {qa.x, qa.y, qa.z, qa.w, a5};
-            float nmx[4], nmy[4];
+            float nmx[4], nmy[4], nrm[4];
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                const bool cx = rin && lane_in && !(v == 3 && last_q);
-                const bool cy = rry && lane_in;
-                const float gx = cx ? av[v] - av[v + 1] : 0.f;
-                const float gy = cy ? av[v] - f4c(cA, v) : 0.f;
-                const float qx = f4c(qmx, v) - t1 * gx;
-                const float qy = f4c(qmy, v) - t1 * gy;
+                const float gx = av[v] - av[v + 1];
+                const float gy = av[v] - f4c(cA, v);
+                const float qx = f4c(qmx, v) - (v == 3 ? t1x3 : t1) * gx;
+                const float qy = f4c(qmy, v) - t1y * gy;
                 const float n2 = qx * qx + qy * qy;
-                const float sf = shrink_factor(n2, rsqrtf(n2), t1);
+                const float inv = rsqrt_ftz(n2);
+                const float sf = shrink_factor(n2, inv, t1);
                 nmx[v] = sf * qx;
                 nmy[v] = sf * qy;
+                // |M^j| = max(|q| - tau1, 0) (the l2 shrink); the clamp keeps n2 * inv
+                // finite where n2 is 0 or flushed (inv = +inf) -- those give 0
+                if (RED && j == S) nrm[v] = fmaxf(fmaf(n2, fminf(inv, 1e30f), -t1), 0.f);
             }
             // lines 5-7: r^j, a^j, K^j at rho from M^j (left neighbour by shuffle, up carried)
             const float mxl = __shfl_up_sync(kFull, nmx[3], 1);
+            const float wr = (writer && rho >= y0 && rho < y1) ? 1.f : 0.f;   // output pixel (reductions)
             const float4 Fr = ring[(rho & (kWaveRing - 1)) * (5 * 32) + 128];
-            const bool in = rin && lane_in;
             const float mxv[5] = {mxl, nmx[0], nmx[1], nmx[2], nmx[3]};
             float rn[4], an[4], kn[4];
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                rn[v] = in ? r_update(fmaf(t1, f4c(qa, v), f4c(qr, v)), RM, at1, A.r_scale) : 0.f;
+                rn[v] = r_update(fmaf(t1, f4c(qa, v), f4c(qr, v)), RM, at1, rsc);
                 const float divn = (mxv[v + 1] - mxv[v]) + (nmy[v] - f4c(upY[j], v));
                 kn[v] = divn - rn[v] - f4c(Fr, v);
-                an[v] = in ? fmaf(t2, 2.f * kn[v] - f4c(qk, v), f4c(qa, v)) : 0.f;
-                if (RED && j == S) {
-                    if (writer && rho >= y0 && rho < y1) {
-                        const float dmx = nmx[v] - f4c(qmx, v), dmy = nmy[v] - f4c(qmy, v), dr = rn[v] - f4c(qr, v);
-                        s_tr += sqrtf(nmx[v] * nmx[v] + nmy[v] * nmy[v]);
-                        s_gr += pw(rn[v], RM);
-                        s_k2 += kn[v] * kn[v];
-                        s_dz += dmx * dmx + dmy * dmy + dr * dr;
-                        s_ub += pw(divn - f4c(Fr, v), RM);
-                    }
+                an[v] = fmaf(t2, fmaf(2.f, kn[v], -f4c(qk, v)), f4c(qa, v));
+                if (RED && j == S) {                             // branch-free: weight 0 off the output
+                    const float dmx = nmx[v] - f4c(qmx, v), dmy = nmy[v] - f4c(qmy, v), dr = rn[v] - f4c(qr, v);
+                    s_tr = fmaf(wr, nrm[v], s_tr);
+                    s_gr = fmaf(wr, pw(rn[v], RM), s_gr);
+                    s_k2 = fmaf(wr * kn[v], kn[v], s_k2);
+                    s_dz = fmaf(wr, dmx * dmx + dmy * dmy + dr * dr, s_dz);
+                    s_ub = fmaf(wr, pw(divn - f4c(Fr, v), RM), s_ub);
                 }
             }
             upY[j] = make_float4(nmy[0], nmy[1], nmy[2], nmy[3]);
@@ -163,10 +183,10 @@ __global__ void __launch_bounds__(kWaveWarps * 32, kWaveMinBlocks) k_wave(const 
                 cK = make_float4(kn[0], kn[1], kn[2], kn[3]);
             } else if (writer && rho >= y0 && rho < y1) {
                 const size_t g = po + (size_t)rho * nx + gi;
-                *reinterpret_cast<float4*>(A.mx_out + g) = make_float4(nmx[0], nmx[1], nmx[2], nmx[3]);
-                *reinterpret_cast<float4*>(A.my_out + g) = upY[j];
-                *reinterpret_cast<float4*>(A.r_out + g) = make_float4(rn[0], rn[1], rn[2], rn[3]);
-                *reinterpret_cast<float4*>(A.a_out + g) = make_float4(an[0], an[1], an[2], an[3]);
+                *reinterpret_cast<float4*>(mx_out + g) = make_float4(nmx[0], nmx[1], nmx[2], nmx[3]);
+                *reinterpret_cast<float4*>(my_out + g) = upY[j];
+                *reinterpret_cast<float4*>(r_out + g) = make_float4(rn[0], rn[1], rn[2], rn[3]);
+                *reinterpret_cast<float4*>(a_out + g) = make_float4(an[0], an[1], an[2], an[3]);
             }
         }
     }

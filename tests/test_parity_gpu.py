@@ -95,7 +95,8 @@ PATHS = [dict(UOT_VEC=1, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
          dict(UOT_VEC=4, UOT_SEG_H=7, UOT_PERSIST=0, UOT_TEMPORAL=0),
          dict(UOT_VEC=4, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
          dict(UOT_VEC=2, UOT_SEG_H=5, UOT_PERSIST=0, UOT_TEMPORAL=0),
-         dict(UOT_PERSIST=0, UOT_TEMPORAL=1), dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_T4=0),
+         dict(UOT_PERSIST=0, UOT_TEMPORAL=1), dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=1),
+         dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=1, UOT_T4=0),
          dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=0),
          dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=0, UOT_T4_TH=32, UOT_T2_WIDE=0), dict(UOT_PERSIST=1)]
 
@@ -314,7 +315,9 @@ def test_persistent_solve_stops_on_device():
 # ------------------------------------------------------------------------- temporal blocking (k_iter2)
 # temporal variants: register wavefront (k_wave; segments of 128 / 16 / 24 rows) or SMEM
 # tiles (UOT_WAVE=0; tile rows 36 / 32, 320- or 640-thread CTAs), four- or two-iteration passes
-TVARS = [dict(UOT_T4=1), dict(UOT_T4=1, UOT_WAVE_H=16), dict(UOT_T4=0), dict(UOT_T4=0, UOT_WAVE_H=24),
+TVARS = [dict(UOT_WAVE=1, UOT_T4=1), dict(UOT_WAVE=1, UOT_T4=1, UOT_WAVE_H=16),
+         dict(UOT_WAVE=1, UOT_T4=0), dict(UOT_WAVE=1, UOT_T4=0, UOT_WAVE_H=24),
+         dict(UOT_WAVE=1, UOT_T4=1, UOT_PASS_COST="9,0.1,9"), dict(UOT_WAVE=1, UOT_T4=1, UOT_PASS_COST="1.2,9,1.26"),
          dict(UOT_WAVE=0, UOT_T4=1), dict(UOT_WAVE=0, UOT_T4=1, UOT_T4_TH=32, UOT_T2_WIDE=0),
          dict(UOT_WAVE=0, UOT_T4=1, UOT_T2_WIDE=1), dict(UOT_WAVE=0, UOT_T4=0), dict(UOT_WAVE=0, UOT_T4=0, UOT_T2_WIDE=0)]
 
@@ -332,7 +335,7 @@ def test_temporal_matches_streaming_and_oracle(n, check, tvar):
     _, st_s, rep_s = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 0}, check_every=check)
     prob, st_t, rep_t = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 1, **tvar},
                                 check_every=check)
-    kind = "k_iter" if tvar.get("UOT_WAVE", 1) == 0 else "k_wave"
+    kind = "k_wave" if tvar.get("UOT_WAVE", 0) == 1 else "k_iter"
     assert prob.kernel_path == kind + ("4" if tvar["UOT_T4"] else "2")
     for k in ("mx", "my", "r", "a"):
         scale = max(np.abs(st_s[k]).max(), 1e-30)

@@ -13,15 +13,16 @@ from paper_1909_00149_b200 import inputs
 from paper_1909_00149_b200.uot import Problem
 
 pytestmark = pytest.mark.gpu
-# one-pass k_iter ("stream"), temporally blocked passes (four / two iterations per pass;
-# prox contexts run k_iter there), SMEM-resident persistent kernel
-PATHS = ["stream", "temporal", "temporal2", "persist"]
+# one-pass k_iter ("stream"), register-wavefront passes (four / two iterations per pass;
+# prox contexts run k_iter there), SMEM-tile passes, SMEM-resident persistent kernel
+PATHS = ["stream", "temporal", "temporal2", "tiles", "persist"]
 
 
 def _run(monkeypatch, path, fr, alpha, rho, tau, n, **kw):
     monkeypatch.setenv("UOT_PERSIST", "1" if path == "persist" else "0")
     monkeypatch.setenv("UOT_TEMPORAL", "0" if path == "stream" else "1")
     monkeypatch.setenv("UOT_T4", "0" if path == "temporal2" else "1")
+    monkeypatch.setenv("UOT_WAVE", "0" if path == "tiles" else "1")
     prob = Problem(torch.from_numpy(fr).cuda(), alpha, rho=rho, tau1=tau, tau2=tau, **kw)
     rep = prob.step(n, report=True)
     st = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
