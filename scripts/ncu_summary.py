@@ -2,7 +2,7 @@
 """Summarise ncu outputs into profiles/ (run here, on the CPU box).
 
   python scripts/ncu_summary.py launches <launches.csv> <out.md>
-  python scripts/ncu_summary.py full <report.ncu-rep> <config> <alg_bytes_per_launch> <out.json>
+  python scripts/ncu_summary.py full <report.ncu-rep> <config> <alg_bytes_per_launch> <out.json> [kernel-substring]
 """
 import collections
 import csv
@@ -46,7 +46,7 @@ METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.
            "sm__cycles_elapsed.avg.per_second"]
 
 
-def full(rep, config, alg_bytes, out):
+def full(rep, config, alg_bytes, out, pick=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
@@ -61,7 +61,7 @@ def full(rep, config, alg_bytes, out):
     def gb(x):
         v = float(x["value"].replace(",", ""))
         return v * {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3}[x["unit"]]
-    k, d = next(iter(res.items()))
+    k, d = next((kv for kv in res.items() if pick is None or pick in kv[0]))
     traffic = (gb(d["dram__bytes_read.sum"]) + gb(d["dram__bytes_write.sum"])) * 1e9
     summ = {"kernel": k, "report": rep, "metrics": d, "dram_bytes_per_launch": traffic,
             "alg_bytes_per_launch": float(alg_bytes), "traffic_over_alg": traffic / float(alg_bytes)}
@@ -79,4 +79,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
-        full(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5])
+        full(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5], sys.argv[6] if len(sys.argv) > 6 else None)
