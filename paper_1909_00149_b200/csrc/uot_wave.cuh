@@ -101,38 +101,40 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S>::minb) k_wave(cons
 #pragma unroll
     for (int p = 0; p < P; ++p) issue(t0 + p);
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 pMx[S], pMy[S], pR[S], pA[S], pK[S];   // level j-1's outputs at row t-j (index j-1)
+    // Level j-1's outputs (M, r, a, K) at one row, in two register sets: a step reads the
+    // previous row from one set and writes the current row into the other, and the next
+    // step swaps them (two steps per loop trip: no register copies).
+    struct Lv { float4 mx, my, r, a, k; };
+    Lv SA[S], SB[S];
     float4 upY[S + 1];                            // level j's M_y at its previous row
 #pragma unroll
-    for (int j = 0; j < S; ++j) { pMx[j] = z4; pMy[j] = z4; pR[j] = z4; pA[j] = z4; pK[j] = z4; }
+    for (int j = 0; j < S; ++j) { SA[j] = {z4, z4, z4, z4, z4}; SB[j] = SA[j]; }
 #pragma unroll
     for (int j = 0; j <= S; ++j) upY[j] = z4;
     float s_tr = 0.f, s_gr = 0.f, s_k2 = 0.f, s_dz = 0.f, s_ub = 0.f;
 
-#pragma unroll 2                                             // the carried rows alternate registers
-    for (int t = t0; t <= t1r; ++t) {
+    auto step = [&](const int t, Lv (&Pv)[S], Lv (&Cv)[S]) {
         if (t + P <= t1r) issue(t + P);
         else cp_commit();                                        // empty group: uniform wait count
         cp_wait<P>();                                            // row t has landed (own lane's copies)
         const float4* s = ring + (t & (kWaveRing - 1)) * (5 * 32);
         float4 Mx = s[0], My = s[32];
-        const float4 R = s[64], Aa = s[96], F = s[128];
+        const float4 R = s[64], F = s[128];
         if (last_q) Mx.w = 0.f;                                  // pinned flux components (L3)
         if (t == ny - 1) My = z4;
         // ---- level 0: K^0 = div M - r - f at row t ----
         const float mxl0 = __shfl_up_sync(kFull, Mx.w, 1);
-        float4 K;
-        K.x = ((Mx.x - mxl0) + (My.x - upY[0].x)) - R.x - F.x;
-        K.y = ((Mx.y - Mx.x) + (My.y - upY[0].y)) - R.y - F.y;
-        K.z = ((Mx.z - Mx.y) + (My.z - upY[0].z)) - R.z - F.z;
-        K.w = ((Mx.w - Mx.z) + (My.w - upY[0].w)) - R.w - F.w;
+        Cv[0].mx = Mx; Cv[0].my = My; Cv[0].r = R; Cv[0].a = s[96];
+        Cv[0].k.x = ((Mx.x - mxl0) + (My.x - upY[0].x)) - R.x - F.x;
+        Cv[0].k.y = ((Mx.y - Mx.x) + (My.y - upY[0].y)) - R.y - F.y;
+        Cv[0].k.z = ((Mx.z - Mx.y) + (My.z - upY[0].z)) - R.z - F.z;
+        Cv[0].k.w = ((Mx.w - Mx.z) + (My.w - upY[0].w)) - R.w - F.w;
         upY[0] = My;
-        float4 cMx = Mx, cMy = My, cR = R, cA = Aa, cK = K;     // level j-1 at row t-j+1
 #pragma unroll
         for (int j = 1; j <= S; ++j) {
             const int rho = t - j;
-            const float4 qmx = pMx[j - 1], qmy = pMy[j - 1], qr = pR[j - 1], qa = pA[j - 1], qk = pK[j - 1];
-            pMx[j - 1] = cMx; pMy[j - 1] = cMy; pR[j - 1] = cR; pA[j - 1] = cA; pK[j - 1] = cK;
+            const float4 qmx = Pv[j - 1].mx, qmy = Pv[j - 1].my, qr = Pv[j - 1].r, qa = Pv[j - 1].a, qk = Pv[j - 1].k;
+            const float4 cA = Cv[j - 1].a;                       // a^{j-1} at rho + 1
             const float t1y = (rho == -1 || rho == ny - 1) ? 0.f : t1;
             // line 3: M^j(rho) = prox(M^{j-1} - tau1 div^* a^{j-1}); a at (rho, i+1) and (rho+1, i)
             const float a5 = __shfl_down_sync(kFull, qa.x, 1);
@@ -176,11 +178,11 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S>::minb) k_wave(cons
             }
             upY[j] = make_float4(nmy[0], nmy[1], nmy[2], nmy[3]);
             if (j < S) {
-                cMx = make_float4(nmx[0], nmx[1], nmx[2], nmx[3]);
-                cMy = upY[j];
-                cR = make_float4(rn[0], rn[1], rn[2], rn[3]);
-                cA = make_float4(an[0], an[1], an[2], an[3]);
-                cK = make_float4(kn[0], kn[1], kn[2], kn[3]);
+                Cv[j].mx = make_float4(nmx[0], nmx[1], nmx[2], nmx[3]);
+                Cv[j].my = upY[j];
+                Cv[j].r = make_float4(rn[0], rn[1], rn[2], rn[3]);
+                Cv[j].a = make_float4(an[0], an[1], an[2], an[3]);
+                Cv[j].k = make_float4(kn[0], kn[1], kn[2], kn[3]);
             } else if (writer && rho >= y0 && rho < y1) {
                 const size_t g = po + (size_t)rho * nx + gi;
                 *reinterpret_cast<float4*>(mx_out + g) = make_float4(nmx[0], nmx[1], nmx[2], nmx[3]);
@@ -189,7 +191,14 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S>::minb) k_wave(cons
                 *reinterpret_cast<float4*>(a_out + g) = make_float4(an[0], an[1], an[2], an[3]);
             }
         }
+    };
+    int t = t0;
+#pragma unroll 1
+    for (; t + 1 <= t1r; t += 2) {
+        step(t, SA, SB);
+        step(t + 1, SB, SA);
     }
+    if (t <= t1r) step(t, SA, SB);
     cp_wait<0>();
     if constexpr (RED) {                                         // fixed-order warp sums -> one record
         double v[5] = {s_tr, s_gr, s_k2, s_dz, s_ub};
