@@ -228,6 +228,7 @@ enum {
 __global__ void __launch_bounds__(256) k_pair_reduce(const ReduceArgs R) {
     __shared__ double sh[32];
     __shared__ int am_last;
+    pdl_wait();
     if (R.is_iteration && R.stop != nullptr && *reinterpret_cast<const volatile int*>(R.stop)) return;
     const int g = blockIdx.x;
     const double* base = R.partials + (size_t)g * R.recs_per_pair * kRec;
@@ -398,6 +399,7 @@ struct uot_ctx {
     int t2vec;           // its 16-byte loads (nx % 4 == 0, aligned planes)
     TVar tv[3];          // its variants: [0] two iterations per pass, [1] four, [2] three (k_wave)
     float pass_cost[5];  // relative device time of a pass of S = 1..4 iterations (pass scheduler)
+    bool pdl;            // programmatic dependent launch for the pass kernels (UOT_PDL)
     bool t4on;           // four-iteration passes enabled (UOT_T4)
     struct LogE { int64_t iter; int slot, rcur; };
     std::vector<LogE> log;           // launches since the stop was armed (device-stop correction)
@@ -680,6 +682,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->t2vec = (p.nx % 4 == 0) && al16(b.f) && al16(b.mx[0]) && al16(b.mx[1]) && al16(b.my[0]) && al16(b.my[1]) &&
                al16(b.a[0]) && al16(b.a[1]) && al16(b.r) && al16(b.r_alt);
     c->t4on = env_int("UOT_T4", 1) != 0;
+    c->pdl = env_int("UOT_PDL", 1) != 0;
     if (c->t2ok) {
         const int wenv = env_int("UOT_T2_WIDE", -1);
         static const int kVarS[3] = {2, 4, 3};
@@ -936,6 +939,23 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
     return UOT_OK;
 }
 
+// Launch with programmatic dependent launch when enabled (UOT_PDL, default on): the kernel
+// (k_wave, k_iter2, k_pair_reduce: pdl_wait() first) may be scheduled while its predecessor
+// drains, hiding the launch latency of back-to-back passes on small grids.
+static cudaError_t launch_k(const uot_ctx* c, const void* fn, dim3 grid, dim3 block, size_t smem, void** args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = c->pdl ? 1 : 0;
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 // S fixed-marginal iterations in one HBM pass (k_iter2<TH, S>, uot_temporal.cuh): iterations
 // iter+1 .. iter+S; reductions (red) for iteration iter+S.
 static int launch_pass(uot_ctx* c, int vi, bool red, const int* stop, double tol) {
@@ -982,10 +1002,10 @@ static int launch_pass(uot_ctx* c, int vi, bool red, const int* stop, double tol
     }
     if (v.wave) {
         void* kargs[1] = {(void*)&W};
-        cudaLaunchKernel(v.fn[red ? 1 : 0], dim3(blocks), dim3(v.threads), kargs, v.smem, c->s);
+        launch_k(c, v.fn[red ? 1 : 0], dim3(blocks), dim3(v.threads), v.smem, kargs);
     } else {
         void* kargs[2] = {(void*)&A, (void*)&Mp};
-        cudaLaunchKernel(v.fn[red ? 1 : 0], dim3(blocks), dim3(v.threads), kargs, v.smem, c->s);
+        launch_k(c, v.fn[red ? 1 : 0], dim3(blocks), dim3(v.threads), v.smem, kargs);
     }
     if (e1) cudaEventRecord(e1, c->s);
     int rc = check_launch(c, "k_iter2");
@@ -1000,7 +1020,10 @@ static int launch_pass(uot_ctx* c, int vi, bool red, const int* stop, double tol
         R.pair_out = c->pair_it; R.glob = c->glob; R.counter = c->counter;
         R.stop = const_cast<int*>(stop); R.max_mask = 0u; R.is_iteration = 1; R.is_setup = 0;
         R.iteration = c->iter; R.tol = tol; R.tau1 = c->tau1;
-        k_pair_reduce<<<c->G, 256, 0, c->s>>>(R);
+        {
+            void* rargs[1] = {(void*)&R};
+            launch_k(c, (const void*)k_pair_reduce, dim3(c->G), dim3(256), 0, rargs);
+        }
         rc = check_launch(c, "k_pair_reduce(iter2)");
         if (rc) return rc;
     }

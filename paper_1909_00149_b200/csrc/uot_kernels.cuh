@@ -136,6 +136,14 @@ __device__ __forceinline__ float r_update(float q, int mode, float at1, float rs
 // |v|^p for the growth / repaired-bound reductions
 __device__ __forceinline__ float pw(float v, int mode) { return mode == 1 ? v * v : fabsf(v); }
 
+// Programmatic dependent launch: a kernel launched with the PDL attribute may start while
+// its predecessor on the stream drains; pdl_wait() blocks until the predecessor has
+// completed and its writes are visible (no-op without the attribute).  It precedes every
+// global read and write of the kernels that use it.  pdl_trigger() lets the successor
+// launch once every CTA has triggered or exited.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // Fused iteration.  PROX = false: fixed marginals (rho = inf), K = div M - r - f.
 // PROX = true: Alg.1 line 4 as well: frames x are iterates with
 // centres p; the warp of pair t also updates x_t (and x_{T-1} for the last

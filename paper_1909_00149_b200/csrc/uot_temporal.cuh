@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(NT, NT > kT2Threads ? 1 : TB<TH, S>::minb) k_i
     constexpr int kTH = TH, kRH = TB<TH, S>::RH;
     extern __shared__ __align__(128) float4 sm4[];
     __shared__ double red_sh[5 * (NT / 32)];
+    pdl_wait();
     if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
     const int tiles = A.tiles_x * A.tiles_y;
     const int pair = blockIdx.x / tiles, tile = blockIdx.x - pair * tiles;
@@ -384,6 +385,7 @@ __global__ void __launch_bounds__(NT, NT > kT2Threads ? 1 : TB<TH, S>::minb) k_i
     }
     if (edge) iter_tile<TH, S, RED, true, NT, RM>(A, sm, red_sh, pair, tile, gi0, gj0);
     else iter_tile<TH, S, RED, false, NT, RM>(A, sm, red_sh, pair, tile, gi0, gj0);
+    pdl_trigger();
 }
 
 }  // namespace uotk

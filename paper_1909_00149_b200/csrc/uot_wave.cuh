@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S>::minb) k_wave(cons
     static_assert(S >= 1 && S <= 4, "lanes 0 and 31 hold a 4-column halo");
     constexpr int P = kWaveRing - S - 1;        // rows in flight ahead of the current one
     extern __shared__ __align__(16) float4 wring[];
+    pdl_wait();
     if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int upp = A.strips * A.segs;
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S>::minb) k_wave(cons
     }
     if (t <= t1r) step(t, SA, SB);
     cp_wait<0>();
+    pdl_trigger();
     if constexpr (RED) {                                         // fixed-order warp sums -> one record
         double v[5] = {s_tr, s_gr, s_k2, s_dz, s_ub};
 #pragma unroll
