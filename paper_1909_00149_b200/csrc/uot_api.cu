@@ -796,11 +796,29 @@ int uot_load_frames(uot_ctx* c, const float* host_frames) {
     return launch_setup(c);
 }
 
+// Launch with programmatic dependent launch when enabled (UOT_PDL, default on): the kernel
+// (k_wave, k_iter2, k_pair_reduce: pdl_wait() first) may be scheduled while its predecessor
+// drains, hiding the launch latency of back-to-back passes on small grids.
+static cudaError_t launch_k(const uot_ctx* c, const void* fn, dim3 grid, dim3 block, size_t smem, void** args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = c->pdl ? 1 : 0;
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 extern "C++" {
 template <int V, bool RED, bool PROX>
 static void launch_iter_t(uot_ctx* c, const IterArgs& A) {
     const int blocks = (A.items + kWarps - 1) / kWarps;
-    k_iter<V, RED, PROX><<<blocks, kWarps * 32, 0, c->s>>>(A);
+    void* args[1] = {(void*)&A};
+    launch_k(c, (const void*)k_iter<V, RED, PROX>, dim3(blocks), dim3(kWarps * 32), 0, args);
 }
 template <int V>
 static void launch_iter_v(uot_ctx* c, const IterArgs& A, bool red, bool prox) {
@@ -883,7 +901,10 @@ static int launch_one(uot_ctx* c, int part, bool red, const int* stop, double to
         R.pair_out = c->pair_it; R.glob = c->glob; R.counter = c->counter;
         R.stop = const_cast<int*>(stop); R.max_mask = 0u; R.is_iteration = 1; R.is_setup = 0;
         R.iteration = c->iter; R.tol = tol; R.tau1 = c->tau1;
-        k_pair_reduce<<<c->G, 256, 0, c->s>>>(R);
+        {
+            void* rargs[1] = {(void*)&R};
+            launch_k(c, (const void*)k_pair_reduce, dim3(c->G), dim3(256), 0, rargs);
+        }
         int rc = check_launch(c, "k_pair_reduce(iter)");
         if (rc) return rc;
     }
@@ -937,23 +958,6 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
     c->iter += n;            // uot_get_report corrects it if the device stopped early
     c->persist_launches++;
     return UOT_OK;
-}
-
-// Launch with programmatic dependent launch when enabled (UOT_PDL, default on): the kernel
-// (k_wave, k_iter2, k_pair_reduce: pdl_wait() first) may be scheduled while its predecessor
-// drains, hiding the launch latency of back-to-back passes on small grids.
-static cudaError_t launch_k(const uot_ctx* c, const void* fn, dim3 grid, dim3 block, size_t smem, void** args) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = c->s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = c->pdl ? 1 : 0;
-    return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 // S fixed-marginal iterations in one HBM pass (k_iter2<TH, S>, uot_temporal.cuh): iterations

@@ -154,6 +154,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 template <int V, bool RED, bool PROX, bool DF = false>
 __global__ void __launch_bounds__(kWarps * 32, (PROX || DF) ? kMinBlocksProx : 1)
 k_iter(const IterArgs A) {
+    pdl_wait();
     if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
     const int lane = threadIdx.x & 31;
     const int item = blockIdx.x * kWarps + (threadIdx.x >> 5);
@@ -480,6 +481,7 @@ k_iter(const IterArgs A) {
             P[0] = d0; P[1] = d1; P[2] = d2; P[3] = d3; P[4] = d4; P[5] = (PROX || DF) ? d5 : 0.0; P[6] = 0.0; P[7] = 0.0;
         }
     }
+    pdl_trigger();
 }
 
 // ------------------------------------------------------------------------------------------
