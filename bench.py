@@ -394,7 +394,10 @@ def main():
         d2h = sum_over_ranks(32.0 * 8)                         # report readback (uot_solve), all ranks
 
         def e2e_step():
-            upload(host_pinned)
+            if world == 1:                  # the C-ABI's own H2D (uot_load_frames) from pinned host memory
+                prob.load_frames_host(host_pinned)
+            else:                           # owned frames + the boundary frame from the next rank (NCCL)
+                upload(host_pinned)
             prob.reset()
             return driver.run(cfg.iters, check_every=args.check_every, tol=1e-12)
 
