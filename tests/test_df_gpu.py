@@ -26,11 +26,15 @@ def _cmp(name, g, r, scale, tol=1e-3):
     assert e <= tol, (name, e)
 
 
-@pytest.mark.parametrize("persist", ["0", "1"])
+# path: "stream" (one fused k_iter<DF> launch per ADMM iteration), "wave" (k_wave_df, 2-3
+# ADMM iterations per pass, nx % 4 == 0), "persist" (persistent inner kernel, inner > 1)
+@pytest.mark.parametrize("path", ["stream", "wave", "persist"])
 @pytest.mark.parametrize("inner", [1, 3])
-@pytest.mark.parametrize("shape", [(1, 16, 16), (2, 33, 64), (1, 64, 130)])
-def test_df_parity(monkeypatch, shape, inner, persist):
-    monkeypatch.setenv("UOT_PERSIST", persist)
+@pytest.mark.parametrize("shape,check", [((1, 16, 16), 60), ((2, 33, 64), 7), ((1, 64, 130), 60),
+                                         ((1, 70, 260), 60), ((2, 37, 132), 10)])
+def test_df_parity(monkeypatch, shape, check, inner, path):
+    monkeypatch.setenv("UOT_PERSIST", "1" if path == "persist" else "0")
+    monkeypatch.setenv("UOT_WAVE", "1" if path == "wave" else "0")
     B, ny, nx = shape
     y, s0 = _problem(B, ny, nx, seed=nx + inner)
     mu, kappa, rho = 0.8, 0.5, 1.0
@@ -38,7 +42,12 @@ def test_df_parity(monkeypatch, shape, inner, persist):
     n = 60
     dfp = DFProblem(torch.from_numpy(y).cuda(), torch.from_numpy(s0).cuda(), mu, kappa, rho, tau1=t, tau2=t,
                     inner_iters=inner)
-    rep = dfp.solve(n, eps=0.0, check_every=n)
+    l0 = dfp.launches
+    rep = dfp.solve(n, eps=0.0, check_every=check)
+    if path == "wave" and inner == 1 and nx % 4 == 0:        # 2-3 ADMM iterations per launch
+        assert dfp.launches - l0 < 0.75 * n
+    elif inner == 1:
+        assert dfp.launches - l0 >= n
     st, res = oracle.df_admm(y, s0, mu, kappa, rho, t, t, n, inner_iters=inner)
     scale = max(np.abs(y).max(), np.abs(s0).max())
     for k in ("s", "x", "a", "b"):
@@ -52,9 +61,13 @@ def test_df_parity(monkeypatch, shape, inner, persist):
     assert rep["iterations"] == n
 
 
-def test_df_device_stop_matches_oracle_residuals():
+@pytest.mark.parametrize("wave", ["0", "1"])
+def test_df_device_stop_matches_oracle_residuals(monkeypatch, wave):
     """eps = 1e-3: the device stops at the first checked iteration where both
-    residuals are below eps; the oracle run to that count satisfies the same test."""
+    residuals are below eps; the oracle run to that count satisfies the same test (with
+    k_wave_df passes of 3 + 2 iterations per check the state of the stopping iteration is
+    recovered from the launch log)."""
+    monkeypatch.setenv("UOT_WAVE", wave)
     y, s0 = _problem(1, 32, 32, seed=3)
     t = oracle.default_steps(32, 32, prox=True, fix_first=True, safety=0.95)[0]
     dfp = DFProblem(torch.from_numpy(y).cuda(), torch.from_numpy(s0).cuda(), 0.8, 0.5, 1.0, tau1=t, tau2=t)
@@ -64,3 +77,14 @@ def test_df_device_stop_matches_oracle_residuals():
     st, res = oracle.df_admm(y, s0, 0.8, 0.5, 1.0, t, t, kc)
     assert res[-1, 0] < 1.05e-3 and res[-1, 1] < 1.05e-3
     np.testing.assert_allclose(dfp.s.double().cpu().numpy(), st["s"], atol=2e-3 * max(y.max(), 1))
+    inn = dfp.inner_state()
+    scale = max(np.abs(y).max(), np.abs(s0).max())
+    for k in ("mx", "my", "ain", "z"):
+        _cmp(k, inn[k].double().cpu().numpy(), st[k], max(scale, np.abs(st[k]).max()), tol=2e-3)
+    for k in ("x", "a", "b"):
+        _cmp(k, getattr(dfp, k).double().cpu().numpy(), st[k], scale, tol=2e-3)
+    # warm continuation from the recovered state matches a fresh run of kc + 7 iterations
+    dfp.solve(7, eps=0.0, check_every=7)
+    st2, _ = oracle.df_admm(y, s0, 0.8, 0.5, 1.0, t, t, kc + 7)
+    for k in ("x", "a", "b", "s"):
+        _cmp(k, getattr(dfp, k).double().cpu().numpy(), st2[k], scale, tol=2e-3)
