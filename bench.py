@@ -339,7 +339,7 @@ def main():
     alg_bytes_launch = bytes_iter
     dom = max(by_path, key=lambda k: by_path[k][0])
     dom_ms, dom_n = by_path[dom]
-    if prox or dom == "k_persist":
+    if prox or dom in ("k_persist", "k_tpersist"):
         avg_launch_s = (dom_ms / max(iters_timed, 1)) / 1e3
     else:
         avg_launch_s = (dom_ms / max(dom_n, 1)) / 1e3
@@ -351,7 +351,8 @@ def main():
                    "k_wave2": "k_wave<S=2> (two fused Alg.1 iterations per HBM pass, register wavefront)",
                    "k_iter4": "k_iter2<36, S=4> (four fused Alg.1 iterations per HBM pass, SMEM tiles)",
                    "k_iter2": "k_iter2<32, S=2> (two fused Alg.1 iterations per HBM pass, SMEM tiles)",
-                   "k_persist": "k_persist (all iterations in one cooperative launch, SMEM-resident)"}.get(
+                   "k_persist": "k_persist (all iterations in one cooperative launch, SMEM-resident)",
+                   "k_tpersist": "k_tpersist (all passes of a call in one cooperative launch, SMEM tiles)"}.get(
         dom, f"k_iter<{'prox' if prox else 'fixed'}> (fused Alg.1 iteration)")
     shares = {k: {"ms": v[0], "launches": v[1], "share": v[0] / max(kern_ms, 1e-30)} for k, v in by_path.items()}
 

@@ -191,9 +191,9 @@ int uot_set_timing(uot_ctx* ctx, int enable);
 int uot_get_timing(uot_ctx* ctx, double* ms_total, int64_t* n_launches);
 /* As uot_get_timing, split by kernel: ms[k], n[k] for k = uot_kernel_path codes (0 k_iter,
  * 1 / 3 two- / four-iteration k_iter2 pass, 2 k_persist, 5 / 6 / 7 two- / four- / three-
- * iteration k_wave pass) and 4 = the UOT-DF ADMM kernel; both arrays hold UOT_N_PATHS
- * entries.  Clears the record. */
-#define UOT_N_PATHS 8
+ * iteration k_wave pass, 8 k_tpersist) and 4 = the UOT-DF ADMM kernel; both arrays hold
+ * UOT_N_PATHS entries.  Clears the record. */
+#define UOT_N_PATHS 9
 int uot_get_timing_paths(uot_ctx* ctx, double* ms, int64_t* n);
 
 /* Which ping-pong slot (0/1) of mx/my/a/x holds the current iterate. */
@@ -208,8 +208,10 @@ int uot_set_temporal(uot_ctx* ctx, int enable);
  * 1 = k_iter2 (SMEM tiles, two iterations per pass, fixed marginals), 2 = k_persist (all
  * iterations of a call in one cooperative launch, small grids), 3 = k_iter2 with
  * four-iteration passes, 5 / 6 = k_wave (register wavefront, 16-byte-aligned planes with
- * nx % 4 == 0) with two / four iterations per pass.  Four-iteration contexts fill in with
- * two-iteration passes / k_iter where a reduction falls inside four iterations. */
+ * nx % 4 == 0) with two / four iterations per pass, 8 = k_tpersist (small grids: all
+ * iterations of a call in one cooperative launch of SMEM-tile passes, when every run up to a
+ * check has even length; otherwise the per-pass kernels).  Four-iteration contexts fill in
+ * with two-iteration passes / k_iter where a reduction falls inside four iterations. */
 int uot_kernel_path(const uot_ctx* ctx);
 
 /* CUDA kernels launched by this context since creation (for accounting). */

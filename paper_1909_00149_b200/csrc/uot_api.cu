@@ -293,6 +293,10 @@ __global__ void __launch_bounds__(256) k_pair_reduce(const ReduceArgs R) {
     }
 }
 
+}  // namespace uotk (k_pair_reduce)
+#include "uot_tpersist.inc"
+namespace uotk {
+
 // prox cold start (L8): x^0 = 0, or max(p, 0) with UOT_RESET_X_FROM_P
 // with UOT_FIX_FIRST_FRAME, frame 0 of each chain is the constant argument s = p_0
 __global__ void __launch_bounds__(256) k_init_x(const float* p, float* x, long long n, int from_p,
@@ -400,6 +404,13 @@ struct uot_ctx {
     TVar tv[3];          // its variants: [0] two iterations per pass, [1] four, [2] three (k_wave)
     float pass_cost[5];  // relative device time of a pass of S = 1..4 iterations (pass scheduler)
     bool pdl;            // programmatic dependent launch for the pass kernels (UOT_PDL)
+    struct {             // persistent temporally blocked passes (k_tpersist, small grids)
+        bool ok;
+        int th, tx, ty, ctas, nt;
+        size_t smem;
+        const void* fn;
+        CUtensorMap mx[2][2], my[2][2], a[2][2], r[2][2], f[2];   // [S = 4, 2][slot / r buffer]
+    } tp;
     bool t4on;           // four-iteration passes enabled (UOT_T4)
     struct LogE { int64_t iter; int slot, rcur; };
     std::vector<LogE> log;           // launches since the stop was armed (device-stop correction)
@@ -540,6 +551,16 @@ static void plan_persist(uot_ctx* c) {
     c->pg.ok = true;
     c->pg.TW = TW; c->pg.TH = TH; c->pg.tx = tx; c->pg.ty = ty; c->pg.ctas = ctas;
     c->pg.threads = threads; c->pg.smem = smem;
+}
+
+template <int TH, int RM>
+static const void* tp_kernel_t(int nt) {
+    return nt == uotk::kT2Wide ? (const void*)uotk::k_tpersist<TH, RM, uotk::kT2Wide>
+                               : (const void*)uotk::k_tpersist<TH, RM, uotk::kT2Threads>;
+}
+static const void* tp_kernel(int th, int rm, int nt) {
+    if (th == 36) return rm == 1 ? tp_kernel_t<36, 1>(nt) : (rm == 2 ? tp_kernel_t<36, 2>(nt) : tp_kernel_t<36, 0>(nt));
+    return rm == 1 ? tp_kernel_t<16, 1>(nt) : (rm == 2 ? tp_kernel_t<16, 2>(nt) : tp_kernel_t<16, 0>(nt));
 }
 
 extern "C" {
@@ -716,6 +737,44 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
             }
         }
         if (!c->tv[0].ok) c->t2ok = false;
+    }
+    // persistent temporally blocked passes for grids of at most one co-resident wave of tiles
+    memset(&c->tp, 0, sizeof(c->tp));
+    if (c->t2ok && c->t2vec && env_int("UOT_TPERSIST", 1) != 0) {
+        // tile rows: 36 (one 76 KB CTA per SM), 16 for tiny grids (more, shorter tiles: C1 1.47e9
+        // vs 1.27e9 px-it/s; C2 with 36: 8.0e10 vs 7.8e10)
+        const long long t36 = (long long)c->G * ((p.nx + kTW - 1) / kTW) * ((p.ny + 35) / 36);
+        const int thenv = env_int("UOT_TP_TH", 0);
+        const int TH = thenv == 16 ? 16 : (thenv == 36 ? 36 : (t36 * 2 < kSMs ? 16 : 36));
+        c->tp.th = TH;
+        c->tp.tx = (p.nx + kTW - 1) / kTW;
+        c->tp.ty = (p.ny + TH - 1) / TH;
+        c->tp.smem = TH == 36 ? TB<36, 4>::smem : TB<16, 4>::smem;
+        c->tp.nt = env_int("UOT_TP_NT", kT2Threads) == kT2Wide ? kT2Wide : kT2Threads;
+        c->tp.fn = tp_kernel(TH, c->r_mode, c->tp.nt);
+        int nb = 0, dev = 0, nsm = kSMs;
+        bool ok = cudaFuncSetAttribute(c->tp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->tp.smem) ==
+                      cudaSuccess &&
+                  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, c->tp.fn, c->tp.nt, c->tp.smem) == cudaSuccess;
+        if (ok && cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const long long ctas = (long long)c->G * c->tp.tx * c->tp.ty;
+        // only where a launch per pass is latency-bound: at most one CTA per SM
+        const int tpenv = env_int("UOT_TPERSIST", -1);
+        ok = ok && nb >= 1 && ctas <= (long long)nb * nsm && (tpenv == 1 || ctas <= 2LL * nsm);
+        for (int si = 0; si < 2 && ok; ++si) {
+            const int rows = TH + 2 * (si == 0 ? 4 : 2);
+            for (int q = 0; q < 2; ++q) {
+                ok = ok && encode_plane_map(&c->tp.mx[si][q], b.mx[q], p.nx, p.ny, c->G, rows);
+                ok = ok && encode_plane_map(&c->tp.my[si][q], b.my[q], p.nx, p.ny, c->G, rows);
+                ok = ok && encode_plane_map(&c->tp.a[si][q], b.a[q], p.nx, p.ny, c->G, rows);
+            }
+            ok = ok && encode_plane_map(&c->tp.r[si][0], b.r, p.nx, p.ny, c->G, rows);
+            ok = ok && encode_plane_map(&c->tp.r[si][1], b.r_alt, p.nx, p.ny, c->G, rows);
+            ok = ok && encode_plane_map(&c->tp.f[si], b.f, p.nx, p.ny, c->G, rows);
+        }
+        c->tp.ctas = (int)ctas;
+        c->tp.ok = ok;
+        if (!ok) cudaGetLastError();
     }
     {   // relative pass costs (C4 measurements): k_wave 1 : 1.11 : 1.13 : 1.29 (S = 1..4),
         // SMEM tiles 1 : 1.46 : - : 2.19; UOT_PASS_COST="c2,c3,c4" overrides (c1 = 1)
@@ -960,6 +1019,74 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
     return UOT_OK;
 }
 
+// All n iterations in one cooperative launch of k_tpersist (uot_tpersist.inc): passes of 4 (2
+// before a checked iteration) on SMEM tiles, one grid barrier per pass.  Requires every run up
+// to a check to be even (use_tpersist).  The host replays the pass plan for the slot / r-buffer
+// bookkeeping and the device-stop log.
+static bool use_tpersist(const uot_ctx* c, int n, int reduce_every) {
+    return c->tp.ok && c->t2ok && c->t2on && n >= 2 && (n % 2 == 0) && (reduce_every % 2 == 0);
+}
+
+static int launch_tpersist(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
+    cudaError_t e = cudaMemsetAsync(c->pflags + kMaxPersistCtas, 0, 2 * sizeof(int), c->s);
+    if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "memset barrier: %s", cudaGetErrorString(e));
+    TPArgs P{};
+    Iter2Args& A = P.A;
+    A.nx = c->nx; A.ny = c->ny; A.tiles_x = c->tp.tx; A.tiles_y = c->tp.ty; A.N = c->N;
+    A.f = c->b.f;
+    A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1);
+    A.r_mode = c->r_mode; A.r_scale = c->r_scale;
+    A.vec = 1; A.tma = 1;
+    A.partials = c->part;
+    for (int q = 0; q < 2; ++q) { P.mxb[q] = c->b.mx[q]; P.myb[q] = c->b.my[q]; P.ab[q] = c->b.a[q]; }
+    P.rb[0] = c->b.r; P.rb[1] = c->b.r_alt;
+    P.slot0 = c->slot; P.rcur0 = c->rcur;
+    P.n_iters = n; P.red_every = reduce_every; P.red_last = reduce_last ? 1 : 0;
+    P.iter0 = c->iter;
+    P.bar = c->pflags + kMaxPersistCtas;
+    P.stop = const_cast<int*>(stop);
+    P.pair_out = c->pair_it; P.glob = c->glob; P.tol = tol; P.tau1d = c->tau1;
+    TPMaps M;
+    memset(&M, 0, sizeof(M));
+    for (int si = 0; si < 2; ++si)
+        for (int par = 0; par < 2; ++par) {
+            const int sl = c->slot ^ par, rb = c->rcur ^ par;
+            M.m[si][par][0] = c->tp.mx[si][sl]; M.m[si][par][1] = c->tp.my[si][sl];
+            M.m[si][par][2] = c->tp.r[si][rb]; M.m[si][par][3] = c->tp.a[si][sl]; M.m[si][par][4] = c->tp.f[si];
+        }
+    void* args[2] = {(void*)&P, (void*)&M};
+    cudaEvent_t e1 = nullptr;
+    if (c->timing) {
+        while (c->ev_used + 2 > c->ev.size()) {
+            cudaEvent_t ev;
+            if (cudaEventCreate(&ev) != cudaSuccess) return fail(c, UOT_E_CUDA, "cudaEventCreate");
+            c->ev.push_back(ev);
+        }
+        cudaEventRecord(c->ev[c->ev_used], c->s);
+        e1 = c->ev[c->ev_used + 1];
+        c->ev_used += 2;
+        c->ev_kind.push_back(8);
+    }
+    e = cudaLaunchCooperativeKernel(c->tp.fn, dim3(c->tp.ctas), dim3(c->tp.nt), args, c->tp.smem, c->s);
+    if (e1) cudaEventRecord(e1, c->s);
+    if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "k_tpersist launch: %s", cudaGetErrorString(e));
+    int rc = check_launch(c, "k_tpersist");
+    if (rc) return rc;
+    // replay the device's pass plan: slots, r buffer and the device-stop log per pass
+    for (int k = 0; k < n;) {
+        int d = n - k;
+        if (reduce_every > 0) d = std::min(d, reduce_every - (k % reduce_every));
+        const int S = d >= 4 ? 4 : 2;
+        k += S;
+        c->iter += S;
+        c->slot ^= 1;
+        c->rcur ^= 1;
+        log_launch(c);
+    }
+    c->persist_launches++;
+    return UOT_OK;
+}
+
 // S fixed-marginal iterations in one HBM pass (k_iter2<TH, S>, uot_temporal.cuh): iterations
 // iter+1 .. iter+S; reductions (red) for iteration iter+S.
 static int launch_pass(uot_ctx* c, int vi, bool red, const int* stop, double tol) {
@@ -1080,6 +1207,7 @@ static int pick_pass(const uot_ctx* c, int d) {
 }
 
 static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
+    if (use_tpersist(c, n, reduce_every)) return launch_tpersist(c, n, reduce_every, reduce_last, stop, tol);
     if (use_persist(c) && n >= 2) return launch_persist(c, n, reduce_every, reduce_last, stop, tol);
     const bool poll = stop != nullptr && n > 2 * kPollChunk && c->poll.init();
     if (poll) c->poll.begin();
@@ -1330,6 +1458,7 @@ int uot_r_slot(const uot_ctx* c) { return c ? c->rcur : -1; }
 
 int uot_kernel_path(const uot_ctx* c) {
     if (!c) return -1;
+    if (c->tp.ok && c->t2ok && c->t2on) return 8;
     if (use_persist(c)) return 2;
     if (!(c->t2ok && c->t2on)) return 0;
     const bool four = c->t4on && c->tv[1].ok;

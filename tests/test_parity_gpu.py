@@ -333,7 +333,7 @@ def test_temporal_matches_streaming_and_oracle(n, check, tvar):
     fr = inputs.gen_random(2, 3, 150, 200, seed=91, kind="sparse")
     tau = tau_for(150, 200)
     _, st_s, rep_s = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 0}, check_every=check)
-    prob, st_t, rep_t = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 1, **tvar},
+    prob, st_t, rep_t = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 1, "UOT_TPERSIST": 0, **tvar},
                                 check_every=check)
     kind = "k_wave" if tvar.get("UOT_WAVE", 0) == 1 else "k_iter"
     assert prob.kernel_path == kind + ("4" if tvar["UOT_T4"] else "2")
@@ -392,7 +392,7 @@ def test_path_switching_keeps_the_iterate():
             os.environ.pop("UOT_PERSIST", None)
         else:
             os.environ["UOT_PERSIST"] = old
-    assert prob.kernel_path in ("k_iter2", "k_iter4", "k_wave2", "k_wave4", "k_persist")
+    assert prob.kernel_path in ("k_iter2", "k_iter4", "k_wave2", "k_wave4", "k_persist", "k_tpersist")
     prob.step(7)                       # passes + an odd tail
     prob.set_temporal(False)
     path_off = prob.kernel_path
@@ -403,3 +403,61 @@ def test_path_switching_keeps_the_iterate():
     st = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
     compare(fr, st, ref)
     assert path_off in ("k_iter", "k_persist")
+
+
+# ------------------------------------------------------------------ persistent tile passes (k_tpersist)
+@pytest.mark.parametrize("shape", [(1, 2, 64, 64), (2, 3, 150, 200), (1, 2, 37, 260)])
+@pytest.mark.parametrize("n,check", [(40, 10), (36, 6), (20, 0), (41, 10), (30, 7)])
+def test_tpersist_matches_oracle(shape, n, check):
+    """All passes of a call in one cooperative launch (4-iteration passes, 2 before a check;
+    even runs only -- odd ones fall back to the per-pass kernels), parity with the oracle and
+    with the one-pass kernel, reductions of the checked iterations."""
+    B, T, ny, nx = shape
+    fr = inputs.gen_random(B, T, ny, nx, seed=7 + nx, kind="sparse")
+    tau = tau_for(ny, nx)
+    _, st_s, rep_s = gpu_run(fr, 1.1, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 0}, check_every=check)
+    prob, st_t, rep_t = gpu_run(fr, 1.1, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 1, "UOT_TPERSIST": 1,
+                                                     "UOT_WAVE": 0}, check_every=check)
+    assert prob.kernel_path == "k_tpersist"
+    l0 = prob.launches
+    prob.iterate(8)                        # 8 iterations, reductions on the last: ONE launch
+    assert prob.launches - l0 == 1
+    prob.iterate(7)                        # odd: per-pass kernels
+    assert prob.launches - l0 > 2
+    for k in ("mx", "my", "r", "a"):
+        scale = max(np.abs(st_s[k]).max(), 1e-30)
+        assert np.abs(st_t[k] - st_s[k]).max() <= 1e-5 * scale, k
+    ref, rrep = oracle.iterate(fr, 1.1, math.inf, tau, tau, n)
+    compare(fr, st_t, ref)
+    assert rep_t["iterations"] == n
+    assert rep_t["objective"] == pytest.approx(rrep[:, 0].sum() + 1.1 * rrep[:, 1].sum(), rel=OBJ_RTOL)
+    assert rep_t["primal_res"] == pytest.approx(math.sqrt(rrep[:, 2].sum()), rel=1e-2, abs=1e-5)
+    assert rep_t["dual_res"] == pytest.approx(rep_s["dual_res"], rel=1e-3, abs=1e-6)
+
+
+@pytest.mark.parametrize("check", [10, 4])
+def test_tpersist_device_stop(check):
+    """Device-side stop inside a persistent launch: the stop iteration's slots are recovered
+    from the replayed pass plan; a warm continuation matches a fresh run."""
+    fr = inputs.gen_random(1, 2, 96, 128, seed=97, kind="uniform")
+    tau = tau_for(96, 128)
+    old = {k: os.environ.get(k) for k in ("UOT_PERSIST", "UOT_TPERSIST", "UOT_WAVE")}
+    os.environ.update({"UOT_PERSIST": "0", "UOT_TPERSIST": "1", "UOT_WAVE": "0"})
+    try:
+        prob = Problem(torch.from_numpy(fr).cuda(), 0.8, tau1=tau, tau2=tau)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert prob.kernel_path == "k_tpersist"
+    rep = prob.solve(20000, tol=1e-4, check_every=check)
+    assert rep["converged"] == 1
+    kc = rep["iterations"]
+    assert kc % check == 0 and 0 < kc < 20000
+    ref, _ = oracle.iterate(fr, 0.8, math.inf, tau, tau, kc)
+    compare(fr, {k: v.double().cpu().numpy() for k, v in prob.state().items()}, ref)
+    prob.step(10)
+    ref2, _ = oracle.iterate(fr, 0.8, math.inf, tau, tau, kc + 10)
+    compare(fr, {k: v.double().cpu().numpy() for k, v in prob.state().items()}, ref2)
