@@ -88,3 +88,26 @@ def test_df_device_stop_matches_oracle_residuals(monkeypatch, wave):
     st2, _ = oracle.df_admm(y, s0, 0.8, 0.5, 1.0, t, t, kc + 7)
     for k in ("x", "a", "b", "s"):
         _cmp(k, getattr(dfp, k).double().cpu().numpy(), st2[k], scale, tol=2e-3)
+
+
+@pytest.mark.parametrize("wave", ["0", "1"])
+@pytest.mark.parametrize("mu,p_norm", [(0.8, 2), (math.inf, 1)])
+def test_df_variants(monkeypatch, wave, mu, p_norm):
+    """UOT-DF with the p = 2 residual and the balanced limit mu = inf (r dropped,
+    P:609) on both the per-iteration kernel and the wavefront passes."""
+    monkeypatch.setenv("UOT_WAVE", wave)
+    y, s0 = _problem(1, 40, 132, seed=17)
+    if not math.isfinite(mu):
+        s0 = s0 / s0.sum() * y.clip(0).sum()          # equal masses keep the balanced problem feasible
+    t = oracle.default_steps(132, 40, prox=True, fix_first=True, safety=0.95)[0]
+    n = 50
+    dfp = DFProblem(torch.from_numpy(y).cuda(), torch.from_numpy(s0.astype(np.float32)).cuda(), mu, 0.5, 1.0,
+                    tau1=t, tau2=t, p_norm=p_norm)
+    dfp.solve(n, eps=0.0, check_every=10)
+    st, res = oracle.df_admm(y, s0.astype(np.float32), mu, 0.5, 1.0, t, t, n, p_norm=p_norm)
+    scale = max(np.abs(y).max(), np.abs(s0).max())
+    for k in ("s", "x", "a", "b"):
+        _cmp(k, getattr(dfp, k).double().cpu().numpy(), st[k], scale)
+    inn = dfp.inner_state()
+    for k in ("mx", "my", "ain", "z"):
+        _cmp(k, inn[k].double().cpu().numpy(), st[k], max(scale, np.abs(st[k]).max()))
