@@ -22,8 +22,8 @@ namespace uotk {
 constexpr int kWaveOut = 120;                   // columns written per warp strip (lanes 1..30)
 constexpr int kWaveRing = 8;                    // rows per warp in the SMEM ring
 constexpr int kWaveWarps = 2;                   // warps (independent strips) per CTA
-template <int S> struct WaveCfg {               // CTAs (2 warps) per SM: registers <= 255 (S = 4) / 204
-    static constexpr int minb = S >= 4 ? 4 : 5;
+template <int S, bool RED> struct WaveCfg {     // CTAs (2 warps) per SM: registers <= 255 (S = 4; a 168
+    static constexpr int minb = S >= 4 ? 4 : 5;   // cap for 10 warps / SM spills and is 5% slower) / 204
 };
 constexpr size_t kWaveSmem = (size_t)kWaveWarps * kWaveRing * 5 * 32 * sizeof(float4);   // 40 KB
 
@@ -55,7 +55,7 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 __device__ __forceinline__ float f4c(const float4& q, int v) { return v == 0 ? q.x : (v == 1 ? q.y : (v == 2 ? q.z : q.w)); }
 
 template <int S, int RM, bool RED>
-__global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S>::minb) k_wave(const WaveArgs A) {
+__global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S, RED>::minb) k_wave(const WaveArgs A) {
     static_assert(S >= 1 && S <= 4, "lanes 0 and 31 hold a 4-column halo");
     constexpr int P = kWaveRing - S - 1;        // rows in flight ahead of the current one
     extern __shared__ __align__(16) float4 wring[];
