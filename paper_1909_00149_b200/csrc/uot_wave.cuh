@@ -99,9 +99,14 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S, RED>::minb) k_wave
     };
 
     const int t0 = y0 - S, t1r = y1 - 1 + S;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    // The first steps' deeper levels read f of rows above t0 that are never loaded: clear the
+    // ring so those discarded rows are finite (a NaN there would poison the weight-0 terms of
+    // the reductions).  Each lane clears and later reads only its own slots.
+#pragma unroll
+    for (int q = 0; q < kWaveRing * 5; ++q) ring[q * 32] = z4;
 #pragma unroll
     for (int p = 0; p < P; ++p) issue(t0 + p);
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     // Level j-1's outputs (M, r, a, K) at one row, in two register sets: a step reads the
     // previous row from one set and writes the current row into the other, and the next
     // step swaps them (two steps per loop trip: no register copies).
@@ -296,9 +301,13 @@ __global__ void __launch_bounds__(kWaveWarps * 32, 4) k_wave_df(const WaveDfArgs
     };
 
     const int t0 = y0 - S, t1r = y1 - 1 + S;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < kWaveDfState * 8; ++q) sring[q * 32] = z4;       // (see k_wave: rows never loaded)
+#pragma unroll
+    for (int q = 0; q < kWaveRing * 2; ++q) cring[q * 32] = z4;
 #pragma unroll
     for (int p = 0; p < P; ++p) issue(t0 + p);
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     struct Lv { float4 mx, my, r, a, k, z, x, ax, b; };
     Lv SA[S], SB[S];
     float4 upY[S + 1];
