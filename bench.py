@@ -345,8 +345,9 @@ def main():
         avg_launch_s = (dom_ms / max(dom_n, 1)) / 1e3
     achieved = alg_bytes_launch / avg_launch_s / 1e9
     path = prob.kernel_path
-    temporal = path in ("k_iter2", "k_iter4", "k_wave2", "k_wave4")
-    kernel_name = {"k_wave4": "k_wave<S=4> (four fused Alg.1 iterations per HBM pass, register wavefront)",
+    temporal = path in ("k_iter2", "k_iter4", "k_wave2", "k_wave4", "k_wave3", "k_wave5")
+    kernel_name = {"k_wave5": "k_wave<S=5> (five fused Alg.1 iterations per HBM pass, register wavefront)",
+                   "k_wave4": "k_wave<S=4> (four fused Alg.1 iterations per HBM pass, register wavefront)",
                    "k_wave3": "k_wave<S=3> (three fused Alg.1 iterations per HBM pass, register wavefront)",
                    "k_wave2": "k_wave<S=2> (two fused Alg.1 iterations per HBM pass, register wavefront)",
                    "k_iter4": "k_iter2<36, S=4> (four fused Alg.1 iterations per HBM pass, SMEM tiles)",

@@ -190,10 +190,10 @@ int uot_objective(uot_ctx* ctx, double* per_pair, uot_report* out);
 int uot_set_timing(uot_ctx* ctx, int enable);
 int uot_get_timing(uot_ctx* ctx, double* ms_total, int64_t* n_launches);
 /* As uot_get_timing, split by kernel: ms[k], n[k] for k = uot_kernel_path codes (0 k_iter,
- * 1 / 3 two- / four-iteration k_iter2 pass, 2 k_persist, 5 / 6 / 7 two- / four- / three-
- * iteration k_wave pass, 8 k_tpersist) and 4 = the UOT-DF ADMM kernel; both arrays hold
+ * 1 / 3 two- / four-iteration k_iter2 pass, 2 k_persist, 5 / 7 / 6 / 9 two- / three- / four- /
+ * five-iteration k_wave pass, 8 k_tpersist) and 4 = the UOT-DF ADMM kernel; both arrays hold
  * UOT_N_PATHS entries.  Clears the record. */
-#define UOT_N_PATHS 9
+#define UOT_N_PATHS 10
 int uot_get_timing_paths(uot_ctx* ctx, double* ms, int64_t* n);
 
 /* Which ping-pong slot (0/1) of mx/my/a/x holds the current iterate. */

@@ -33,7 +33,7 @@ EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset
             "uot_rpca_scratch_doubles", "uot_rpca_create", "uot_rpca_reset", "uot_rpca_solve",
             "uot_rpca_set_timing", "uot_rpca_get_timing", "uot_rpca_state_slot", "uot_rpca_launch_count",
             "uot_rpca_destroy", "uot_rpca_last_error")
-UOT_N_PATHS = 9
+UOT_N_PATHS = 10
 UOT_RPCA_MAX_T = 128
 UOT_RPCA_SIGNED = 8
 

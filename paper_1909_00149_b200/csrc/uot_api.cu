@@ -91,6 +91,7 @@ static bool wvar_fill(TVar& v) {
 }
 
 static bool wvar_select(TVar& v, int S, int rm) {
+    if (S == 5) return rm == 1 ? wvar_fill<5, 1>(v) : (rm == 2 ? wvar_fill<5, 2>(v) : wvar_fill<5, 0>(v));
     if (S == 4) return rm == 1 ? wvar_fill<4, 1>(v) : (rm == 2 ? wvar_fill<4, 2>(v) : wvar_fill<4, 0>(v));
     if (S == 3) return rm == 1 ? wvar_fill<3, 1>(v) : (rm == 2 ? wvar_fill<3, 2>(v) : wvar_fill<3, 0>(v));
     return rm == 1 ? wvar_fill<2, 1>(v) : (rm == 2 ? wvar_fill<2, 2>(v) : wvar_fill<2, 0>(v));
@@ -103,7 +104,7 @@ static bool tvar_fill_m(TVar& v, bool wide, int rm) {
 
 // Supported (S, TH): S = 2 with TH = 32; S = 4 with TH in {32, 36}.
 static bool tvar_select(TVar& v, int S, int th, bool wide, int rm) {
-    if (S == 3) return false;                   // SMEM tiles: two or four iterations per pass
+    if (S == 3 || S == 5) return false;         // SMEM tiles: two or four iterations per pass
     if (S == 4) return th == 32 ? tvar_fill_m<32, 4>(v, wide, rm) : tvar_fill_m<36, 4>(v, wide, rm);
     return tvar_fill_m<32, 2>(v, wide, rm);
 }
@@ -401,8 +402,8 @@ struct uot_ctx {
     bool t2ok;           // temporally blocked fixed-marginal kernel available (r_alt given)
     bool t2on;           // ... and enabled (uot_set_temporal)
     int t2vec;           // its 16-byte loads (nx % 4 == 0, aligned planes)
-    TVar tv[3];          // its variants: [0] two iterations per pass, [1] four, [2] three (k_wave)
-    float pass_cost[5];  // relative device time of a pass of S = 1..4 iterations (pass scheduler)
+    TVar tv[4];          // its variants: [0] two iterations per pass, [1] four, [2] three, [3] five (k_wave)
+    float pass_cost[6];  // relative device time of a pass of S = 1..5 iterations (pass scheduler)
     bool pdl;            // programmatic dependent launch for the pass kernels (UOT_PDL)
     struct {             // persistent temporally blocked passes (k_tpersist, small grids)
         bool ok;
@@ -658,7 +659,8 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     memset(c->tv, 0, sizeof(c->tv));
     c->tv[0].th = 32;
     c->tv[1].th = env_int("UOT_T4_TH", 36) == 32 ? 32 : 36;   // 36: measured best on C4 (3 CTAs / SM)
-    c->tv[2].th = 32;                                           // (three-iteration passes: k_wave only)
+    c->tv[2].th = 32;                                           // (three- and five-iteration passes: k_wave only)
+    c->tv[3].th = 32;
     // register wavefront (k_wave) for 16-byte-aligned planes with nx % 4 == 0 (UOT_WAVE=0: SMEM tiles)
     // Enough independent strips to fill the GPU: segment height 128 (64, 32 for smaller
     // problems, >= 2 waves of 8 warps per SM); below one wave at 32 rows the SMEM tiles.
@@ -673,11 +675,13 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     const bool wave = (p.nx % 4 == 0) &&
                       (wenv_wave >= 0 ? wenv_wave != 0
                                       : (long long)c->G * strips * ((p.ny + wave_h - 1) / wave_h) >= (long long)kSMs * 8);
-    for (TVar& v : c->tv) {
+    static const int kVarS[4] = {2, 4, 3, 5};
+    for (int k = 0; k < 4; ++k) {
+        TVar& v = c->tv[k];
         v.wave = wave;
         if (wave) {
             v.th = wave_h;
-            v.tx = (p.nx + kWaveOut - 1) / kWaveOut;
+            v.tx = (p.nx + wave_out(kVarS[k]) - 1) / wave_out(kVarS[k]);
         } else {
             v.tx = (p.nx + kTW - 1) / kTW;
         }
@@ -706,8 +710,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->pdl = env_int("UOT_PDL", 1) != 0;
     if (c->t2ok) {
         const int wenv = env_int("UOT_T2_WIDE", -1);
-        static const int kVarS[3] = {2, 4, 3};
-        for (int k = 0; k < 3; ++k) {
+        for (int k = 0; k < 4; ++k) {
             TVar& v = c->tv[k];
             const int S = kVarS[k];
             const bool wide = wenv >= 0 ? (wenv != 0) : ((long long)c->G * v.tx * v.ty <= kSMs);
@@ -776,18 +779,21 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
         c->tp.ok = ok;
         if (!ok) cudaGetLastError();
     }
-    {   // relative pass costs (C4 measurements): k_wave 1 : 1.11 : 1.13 : 1.29 (S = 1..4),
+    {   // relative pass costs (C4 measurements): k_wave 1 : 1.155 : 1.15 : 1.137 : 1.35 (S = 1..5),
         // SMEM tiles 1 : 1.46 : - : 2.19; UOT_PASS_COST="c2,c3,c4" overrides (c1 = 1)
         const bool wv = c->tv[0].wave;
         c->pass_cost[0] = 0.f; c->pass_cost[1] = 1.f;
-        c->pass_cost[2] = wv ? 1.11f : 1.46f;
-        c->pass_cost[3] = wv ? 1.13f : 1e9f;
-        c->pass_cost[4] = wv ? 1.29f : 2.19f;
+        c->pass_cost[2] = wv ? 1.155f : 1.46f;
+        c->pass_cost[3] = wv ? 1.15f : 1e9f;
+        c->pass_cost[4] = wv ? 1.137f : 2.19f;
+        c->pass_cost[5] = wv ? 1.35f : 1e9f;
         const char* pc = getenv("UOT_PASS_COST");
         if (pc) {
-            float a2, a3, a4;
-            if (sscanf(pc, "%f,%f,%f", &a2, &a3, &a4) == 3) {
+            float a2, a3, a4, a5 = 1e9f;
+            const int got = sscanf(pc, "%f,%f,%f,%f", &a2, &a3, &a4, &a5);
+            if (got >= 3) {
                 c->pass_cost[2] = a2; c->pass_cost[3] = a3; c->pass_cost[4] = a4;
+                if (got == 4) c->pass_cost[5] = a5;
             }
         }
     }
@@ -1129,7 +1135,7 @@ static int launch_pass(uot_ctx* c, int vi, bool red, const int* stop, double tol
         cudaEventRecord(c->ev[c->ev_used], c->s);
         e1 = c->ev[c->ev_used + 1];
         c->ev_used += 2;
-        c->ev_kind.push_back(v.wave ? (v.S == 4 ? 6 : (v.S == 3 ? 7 : 5)) : (v.S == 4 ? 3 : 1));
+        c->ev_kind.push_back(v.wave ? (v.S == 5 ? 9 : (v.S == 4 ? 6 : (v.S == 3 ? 7 : 5))) : (v.S == 4 ? 3 : 1));
     }
     if (v.wave) {
         void* kargs[1] = {(void*)&W};
@@ -1177,16 +1183,18 @@ static int pass_variant(const uot_ctx* c, int S) {
     if (!c->t4on) return -1;
     if (S == 4) return c->tv[1].ok ? 1 : -1;
     if (S == 3) return c->tv[2].ok ? 2 : -1;
+    if (S == 5) return c->tv[3].ok ? 3 : -1;
     return -1;
 }
 
 // Iterations of the first pass of the cheapest split of d iterations into passes of the
 // available S (a reduction may only follow the last pass; order is immaterial to the cost).
 static int pick_pass(const uot_ctx* c, int d) {
-    bool av[5] = {false, true, pass_variant(c, 2) >= 0, pass_variant(c, 3) >= 0, pass_variant(c, 4) >= 0};
+    bool av[6] = {false, true, pass_variant(c, 2) >= 0, pass_variant(c, 3) >= 0, pass_variant(c, 4) >= 0,
+                  pass_variant(c, 5) >= 0};
     if (d > 12) {                       // long runs: the best cost per iteration
         int b = 1;
-        for (int S = 2; S <= 4; ++S)
+        for (int S = 2; S <= 5; ++S)
             if (av[S] && c->pass_cost[S] / S < c->pass_cost[b] / b) b = S;
         return b;
     }
@@ -1197,7 +1205,7 @@ static int pick_pass(const uot_ctx* c, int d) {
     for (int x = 1; x <= d; ++x) {
         best[x] = 1e30f;
         first[x] = 1;
-        for (int S = 4; S >= 1; --S)
+        for (int S = 5; S >= 1; --S)
             if (av[S] && S <= x && c->pass_cost[S] + best[x - S] < best[x]) {
                 best[x] = c->pass_cost[S] + best[x - S];
                 first[x] = S;

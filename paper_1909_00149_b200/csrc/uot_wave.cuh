@@ -19,11 +19,14 @@
 
 namespace uotk {
 
-constexpr int kWaveOut = 120;                   // columns written per warp strip (lanes 1..30)
+constexpr int kWaveOut = 120;                   // columns written per warp strip (lanes 1..30), S <= 4
+// S iterations invalidate S columns at each strip side: ceil(S/4) halo lanes per side
+__host__ __device__ constexpr int wave_halo_lanes(int S) { return (S + 3) / 4; }
+__host__ __device__ constexpr int wave_out(int S) { return 128 - 8 * wave_halo_lanes(S); }
 constexpr int kWaveRing = 8;                    // rows per warp in the SMEM ring
-constexpr int kWaveWarps = 2;                   // warps (independent strips) per CTA
-template <int S, bool RED> struct WaveCfg {     // CTAs (2 warps) per SM: registers <= 255 (S = 4; a 168
-    static constexpr int minb = S >= 4 ? 4 : 5;   // cap for 10 warps / SM spills and is 5% slower) / 204
+constexpr int kWaveWarps = 1;                   // warps (independent strips) per CTA
+template <int S, bool RED> struct WaveCfg {     // warps per SM: registers <= 255 (S >= 4; a 168 cap for
+    static constexpr int minb = (S >= 4 ? 8 : 10) / kWaveWarps;   // 10 warps / SM spills and is slower) / 204
 };
 constexpr size_t kWaveSmem = (size_t)kWaveWarps * kWaveRing * 5 * 32 * sizeof(float4);   // 40 KB
 
@@ -56,7 +59,8 @@ __device__ __forceinline__ float f4c(const float4& q, int v) { return v == 0 ? q
 
 template <int S, int RM, bool RED>
 __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S, RED>::minb) k_wave(const WaveArgs A) {
-    static_assert(S >= 1 && S <= 4, "lanes 0 and 31 hold a 4-column halo");
+    static_assert(S >= 1 && S <= 5, "ring of 8 rows: S + prefetch + 1 <= 8");
+    constexpr int HL = wave_halo_lanes(S), OUT = wave_out(S);
     constexpr int P = kWaveRing - S - 1;        // rows in flight ahead of the current one
     extern __shared__ __align__(16) float4 wring[];
     pdl_wait();
@@ -68,10 +72,10 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S, RED>::minb) k_wave
     const int pair = (int)(unit / upp), u = (int)(unit - (long long)pair * upp);
     const int sy = u / A.strips, sx = u - sy * A.strips;
     const int nx = A.nx, ny = A.ny;
-    const int gi = sx * kWaveOut - 4 + 4 * lane;                 // first column of this lane's quad
+    const int gi = sx * OUT - 4 * HL + 4 * lane;                 // first column of this lane's quad
     const bool lane_in = gi >= 0 && gi < nx;                     // whole quad in the grid (nx % 4 == 0)
     const bool last_q = gi + 3 == nx - 1;                        // holds the pinned column nx-1 (L3)
-    const bool writer = lane >= 1 && lane <= 30 && lane_in;
+    const bool writer = lane >= HL && lane <= 31 - HL && lane_in;
     const int y0 = sy * A.H, y1 = min(y0 + A.H, ny);             // output rows [y0, y1)
     const size_t po = (size_t)pair * (size_t)A.N;
     const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1, rsc = A.r_scale;
@@ -256,7 +260,7 @@ constexpr int kWaveDfState = 4;     // rows of the state ring (current + 3 in fl
 constexpr size_t kWaveDfSmem = (size_t)kWaveWarps * (kWaveDfState * 8 + kWaveRing * 2) * 32 * sizeof(float4);   // 48 KB
 
 template <int S, int RM, bool RED>
-__global__ void __launch_bounds__(kWaveWarps * 32, 4) k_wave_df(const WaveDfArgs A) {
+__global__ void __launch_bounds__(kWaveWarps * 32, 8 / kWaveWarps) k_wave_df(const WaveDfArgs A) {
     static_assert(S >= 1 && S <= 4, "lanes 0 and 31 hold a 4-column halo");
     constexpr int P = kWaveDfState - 1;          // rows in flight ahead of the current one
     static_assert(S + P + 1 <= kWaveRing, "constant ring holds rows t-S .. t+P");

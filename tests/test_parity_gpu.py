@@ -317,7 +317,9 @@ def test_persistent_solve_stops_on_device():
 # tiles (UOT_WAVE=0; tile rows 36 / 32, 320- or 640-thread CTAs), four- or two-iteration passes
 TVARS = [dict(UOT_WAVE=1, UOT_T4=1), dict(UOT_WAVE=1, UOT_T4=1, UOT_WAVE_H=16),
          dict(UOT_WAVE=1, UOT_T4=0), dict(UOT_WAVE=1, UOT_T4=0, UOT_WAVE_H=24),
-         dict(UOT_WAVE=1, UOT_T4=1, UOT_PASS_COST="9,0.1,9"), dict(UOT_WAVE=1, UOT_T4=1, UOT_PASS_COST="1.2,9,1.26"),
+         dict(UOT_WAVE=1, UOT_T4=1, UOT_PASS_COST="9,0.1,9,9"), dict(UOT_WAVE=1, UOT_T4=1, UOT_PASS_COST="1.2,9,1.26,9"),
+         dict(UOT_WAVE=1, UOT_T4=1, UOT_PASS_COST="9,9,9,0.1"), dict(UOT_WAVE=1, UOT_T4=1, UOT_PASS_COST="1.2,1.2,1.3,0.1",
+                                                                  UOT_WAVE_H=16),
          dict(UOT_WAVE=0, UOT_T4=1), dict(UOT_WAVE=0, UOT_T4=1, UOT_T4_TH=32, UOT_T2_WIDE=0),
          dict(UOT_WAVE=0, UOT_T4=1, UOT_T2_WIDE=1), dict(UOT_WAVE=0, UOT_T4=0), dict(UOT_WAVE=0, UOT_T4=0, UOT_T2_WIDE=0)]
 
