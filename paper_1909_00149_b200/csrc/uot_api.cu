@@ -1205,7 +1205,7 @@ static int pick_pass(const uot_ctx* c, int d) {
     for (int x = 1; x <= d; ++x) {
         best[x] = 1e30f;
         first[x] = 1;
-        for (int S = 5; S >= 1; --S)
+        for (int S = 1; S <= 5; ++S)            // ties: the short pass first (the checked pass is a long one)
             if (av[S] && S <= x && c->pass_cost[S] + best[x - S] < best[x]) {
                 best[x] = c->pass_cost[S] + best[x - S];
                 first[x] = S;

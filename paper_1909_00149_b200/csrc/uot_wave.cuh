@@ -257,10 +257,14 @@ struct WaveDfArgs {
 };
 
 constexpr int kWaveDfState = 4;     // rows of the state ring (current + 3 in flight)
-constexpr size_t kWaveDfSmem = (size_t)kWaveWarps * (kWaveDfState * 8 + kWaveRing * 2) * 32 * sizeof(float4);   // 48 KB
+#ifndef UOT_WAVE_DF_WARPS
+#define UOT_WAVE_DF_WARPS 2
+#endif
+constexpr int kWaveDfWarps = UOT_WAVE_DF_WARPS;    // warps (independent strips) per CTA
+constexpr size_t kWaveDfSmem = (size_t)kWaveDfWarps * (kWaveDfState * 8 + kWaveRing * 2) * 32 * sizeof(float4);
 
 template <int S, int RM, bool RED>
-__global__ void __launch_bounds__(kWaveWarps * 32, 8 / kWaveWarps) k_wave_df(const WaveDfArgs A) {
+__global__ void __launch_bounds__(kWaveDfWarps * 32, 8 / kWaveDfWarps) k_wave_df(const WaveDfArgs A) {
     static_assert(S >= 1 && S <= 4, "lanes 0 and 31 hold a 4-column halo");
     constexpr int P = kWaveDfState - 1;          // rows in flight ahead of the current one
     static_assert(S + P + 1 <= kWaveRing, "constant ring holds rows t-S .. t+P");
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, 8 / kWaveWarps) k_wave_df(con
     if (A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop)) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int upp = A.strips * A.segs;
-    const long long unit = (long long)blockIdx.x * kWaveWarps + w;
+    const long long unit = (long long)blockIdx.x * kWaveDfWarps + w;
     if (unit >= (long long)A.G * upp) return;
     const int pair = (int)(unit / upp), u = (int)(unit - (long long)pair * upp);
     const int sy = u / A.strips, sx = u - sy * A.strips;
