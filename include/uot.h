@@ -165,8 +165,11 @@ int uot_iterate_part(uot_ctx* ctx, int32_t part, int32_t reduce);
 int uot_get_report(uot_ctx* ctx, uot_report* out);
 
 /* Run n_iters >= 0 iterations (Alg.1 lines 3-7).  out == NULL: fully async
- * (graph-capturable, no host sync); out != NULL: the last iteration also
- * computes the reductions and the call synchronises the stream to fill *out. */
+ * (graph-capturable, no host sync; under capture the call ends in the buffer slots it
+ * started from -- device copies are appended when the passes flipped them -- so every
+ * replay continues from the previous one; replays do not advance the context's
+ * iteration count); out != NULL: the last iteration also computes the reductions and
+ * the call synchronises the stream to fill *out. */
 int uot_prox_step(uot_ctx* ctx, int32_t n_iters, uot_report* out);
 
 /* Iterate until primal_res <= tol*max(f_norm, 1e-30) and dual_res <= the same

@@ -1326,8 +1326,31 @@ int uot_get_report(uot_ctx* c, uot_report* out) {
 int uot_prox_step(uot_ctx* c, int32_t n, uot_report* out) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     if (n < 0) return fail(c, UOT_E_INVALID, "n_iters < 0");
+    const int slot0 = c->slot, rcur0 = c->rcur;
     int rc = launch_iters(c, n, 0, out != nullptr && n > 0, nullptr, 0.0);
     if (rc) return rc;
+    // Under CUDA-graph capture every replay re-runs the captured launches with the captured
+    // buffer pointers, so the call must end in the slots it started from: copy the iterate
+    // back when the passes flipped them an odd number of times.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(c->s, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusActive &&
+        (c->slot != slot0 || c->rcur != rcur0)) {
+        const size_t plane = (size_t)c->G * c->N * sizeof(float);
+        cudaError_t e = cudaSuccess;
+        if (c->slot != slot0) {
+            e = cudaMemcpyAsync(c->b.mx[slot0], c->b.mx[c->slot], plane, cudaMemcpyDeviceToDevice, c->s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(c->b.my[slot0], c->b.my[c->slot], plane, cudaMemcpyDeviceToDevice, c->s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(c->b.a[slot0], c->b.a[c->slot], plane, cudaMemcpyDeviceToDevice, c->s);
+            if (e == cudaSuccess && c->prox && c->b.x[0] && c->b.x[1])
+                e = cudaMemcpyAsync(c->b.x[slot0], c->b.x[c->slot], (size_t)c->B * c->T * c->N * sizeof(float),
+                                    cudaMemcpyDeviceToDevice, c->s);
+        }
+        if (e == cudaSuccess && c->rcur != rcur0)
+            e = cudaMemcpyAsync(rcur0 ? c->b.r_alt : c->b.r, rbuf(c), plane, cudaMemcpyDeviceToDevice, c->s);
+        if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "graph slot restore: %s", cudaGetErrorString(e));
+        c->slot = slot0;
+        c->rcur = rcur0;
+    }
     return out ? uot_get_report(c, out) : UOT_OK;
 }
 

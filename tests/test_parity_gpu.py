@@ -463,3 +463,38 @@ def test_tpersist_device_stop(check):
     prob.step(10)
     ref2, _ = oracle.iterate(fr, 0.8, math.inf, tau, tau, kc + 10)
     compare(fr, {k: v.double().cpu().numpy() for k, v in prob.state().items()}, ref2)
+
+
+# ------------------------------------------------------------------------- CUDA graph capture
+@pytest.mark.parametrize("env", [dict(UOT_WAVE=1, UOT_TPERSIST=0, UOT_PERSIST=0),
+                                 dict(UOT_WAVE=0, UOT_TPERSIST=1, UOT_PERSIST=0),
+                                 dict(UOT_TEMPORAL=0, UOT_PERSIST=0)],
+                         ids=["k_wave", "k_tpersist", "k_iter"])
+def test_graph_capture_replays_iterations(env):
+    """uot_prox_step without a report is graph-capturable (include/uot.h): capture 10
+    iterations (an even number of slot flips for every pass split), replay 3 times, and the
+    state is the oracle's iterate 10 + 30 (the warm-up step runs 10 before the capture)."""
+    fr = inputs.gen_random(1, 3, 48, 136, seed=31, kind="sparse")
+    tau = tau_for(48, 136)
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
+    try:
+        s = torch.cuda.Stream()
+        prob = Problem(torch.from_numpy(fr).cuda(), 0.9, tau1=tau, tau2=tau, stream=s)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    torch.cuda.synchronize()
+    prob.step(10)                                   # warm-up outside the capture
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        prob.step(10)
+    for _ in range(3):
+        g.replay()
+    s.synchronize()
+    ref, _ = oracle.iterate(fr, 0.9, math.inf, tau, tau, 40)
+    compare(fr, {k: v.double().cpu().numpy() for k, v in prob.state().items()}, ref)
