@@ -498,3 +498,24 @@ def test_graph_capture_replays_iterations(env):
     s.synchronize()
     ref, _ = oracle.iterate(fr, 0.9, math.inf, tau, tau, 40)
     compare(fr, {k: v.double().cpu().numpy() for k, v in prob.state().items()}, ref)
+
+
+# ------------------------------------------------------------------ k_wave edge shapes
+@pytest.mark.parametrize("shape", [(1, 2, 1, 8), (1, 2, 3, 4), (2, 3, 5, 116), (1, 2, 130, 228), (3, 2, 17, 240)],
+                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("costs", ["1.155,1.15,1.137,1.35", "9,9,9,0.1"], ids=["default", "S5"])
+def test_wave_edge_shapes(shape, costs):
+    """The register wavefront on degenerate / ragged grids: one row, rows < S, one quad per
+    row, widths just under / over one 112- or 120-column strip, with 16-row segments and
+    reductions every 10 and 7 iterations."""
+    B, T, ny, nx = shape
+    fr = inputs.gen_random(B, T, ny, nx, seed=3 + ny + nx, kind="uniform")
+    tau = tau_for(ny, nx)
+    for n, check in ((30, 10), (23, 7)):
+        prob, st, rep = gpu_run(fr, 1.2, n, tau, env={"UOT_WAVE": 1, "UOT_TPERSIST": 0, "UOT_PERSIST": 0,
+                                                     "UOT_WAVE_H": 16, "UOT_PASS_COST": costs}, check_every=check)
+        assert prob.kernel_path.startswith("k_wave")
+        ref, rrep = oracle.iterate(fr, 1.2, math.inf, tau, tau, n)
+        compare(fr, st, ref)
+        assert rep["iterations"] == n and np.isfinite(rep["objective"])
+        assert rep["objective"] == pytest.approx(rrep[:, 0].sum() + 1.2 * rrep[:, 1].sum(), rel=OBJ_RTOL, abs=1e-6)
