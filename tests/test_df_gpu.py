@@ -111,3 +111,35 @@ def test_df_variants(monkeypatch, wave, mu, p_norm):
     inn = dfp.inner_state()
     for k in ("mx", "my", "ain", "z"):
         _cmp(k, inn[k].double().cpu().numpy(), st[k], max(scale, np.abs(st[k]).max()))
+
+
+def test_df_random_wave_matches_stream():
+    """Seeded random UOT-DF problems: the wavefront passes (2-3 ADMM iterations per pass,
+    random segment heights and splits) give the per-iteration kernel's state and residuals."""
+    import os
+    rng = np.random.default_rng(int(os.environ.get("UOT_RANDOM_SEED", 99)))
+    for case in range(int(os.environ.get("UOT_RANDOM_CASES", 12))):
+        B, ny, nx = int(rng.integers(1, 3)), int(rng.integers(1, 120)), 4 * int(rng.integers(1, 70))
+        n, check = int(rng.integers(1, 30)), int(rng.choice([1, 3, 7, 10]))
+        y, s0 = _problem(B, ny, nx, seed=500 + case)
+        t = oracle.default_steps(nx, ny, prox=True, fix_first=True, safety=0.95)[0]
+        out = {}
+        for wave in ("0", "1"):
+            os.environ["UOT_WAVE"] = wave
+            os.environ["UOT_WAVE_H"] = str(int(rng.choice([16, 32, 64]))) if wave == "1" else "0"
+            os.environ["UOT_DF_PASS_COST"] = ",".join(f"{c:.2f}" for c in rng.uniform(0.5, 2.0, 2))
+            try:
+                d = DFProblem(torch.from_numpy(y).cuda(), torch.from_numpy(s0).cuda(), 0.8, 0.5, 1.0, tau1=t, tau2=t)
+                rep = d.solve(n, eps=0.0, check_every=check)
+            finally:
+                for k in ("UOT_WAVE", "UOT_WAVE_H", "UOT_DF_PASS_COST"):
+                    os.environ.pop(k, None)
+            out[wave] = ({k: getattr(d, k).double().cpu().numpy() for k in ("s", "x", "a", "b")},
+                         {k: v.double().cpu().numpy() for k, v in d.inner_state().items()}, rep)
+        scale = max(np.abs(y).max(), np.abs(s0).max())
+        for k in ("x", "a", "b"):
+            _cmp(k, out["1"][0][k], out["0"][0][k], scale, tol=3e-5)
+        for k in ("mx", "my", "r", "ain", "z"):
+            _cmp(k, out["1"][1][k], out["0"][1][k], max(scale, np.abs(out["0"][1][k]).max()), tol=3e-5)
+        assert out["1"][2]["iterations"] == n
+        assert out["1"][2]["primal_res"] == pytest.approx(out["0"][2]["primal_res"], rel=1e-4, abs=1e-7), case

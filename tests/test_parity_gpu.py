@@ -519,3 +519,38 @@ def test_wave_edge_shapes(shape, costs):
         compare(fr, st, ref)
         assert rep["iterations"] == n and np.isfinite(rep["objective"])
         assert rep["objective"] == pytest.approx(rrep[:, 0].sum() + 1.2 * rrep[:, 1].sum(), rel=OBJ_RTOL, abs=1e-6)
+
+
+# ------------------------------------------------------------------ randomized differential test
+def test_random_pass_schedules_match_one_pass_kernel():
+    """Seeded random shapes, iteration counts, check intervals, segment heights and pass
+    splits: the multi-iteration passes (k_wave S = 2..5, SMEM tiles, persistent tiles) give
+    the one-pass kernel's iterates to fp32 rounding and the same residuals."""
+    rng = np.random.default_rng(int(os.environ.get("UOT_RANDOM_SEED", 2024)))
+    for case in range(int(os.environ.get("UOT_RANDOM_CASES", 24))):
+        B, T = int(rng.integers(1, 3)), int(rng.integers(2, 4))
+        ny = int(rng.integers(1, 160))
+        nx = 4 * int(rng.integers(1, 90))
+        n = int(rng.integers(1, 37))
+        check = int(rng.choice([0, 2, 3, 7, 10]))
+        alpha = float(rng.uniform(0.3, 3.0))
+        path = rng.choice(["wave", "tiles", "tpersist"])
+        env = {"UOT_PERSIST": 0}
+        if path == "wave":
+            env.update(UOT_WAVE=1, UOT_TPERSIST=0, UOT_WAVE_H=int(rng.choice([16, 32, 64, 128])),
+                       UOT_PASS_COST=",".join(f"{c:.2f}" for c in rng.uniform(0.5, 2.0, 4)))
+        elif path == "tiles":
+            env.update(UOT_WAVE=0, UOT_TPERSIST=0)
+        else:
+            env.update(UOT_WAVE=0, UOT_TPERSIST=1)
+        fr = inputs.gen_random(B, T, ny, nx, seed=1000 + case, kind=str(rng.choice(["uniform", "sparse"])))
+        tau = tau_for(ny, nx)
+        _, st_s, rep_s = gpu_run(fr, alpha, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 0}, check_every=check)
+        _, st_t, rep_t = gpu_run(fr, alpha, n, tau, env=env, check_every=check)
+        for k in ("mx", "my", "r", "a"):
+            scale = max(np.abs(st_s[k]).max(), 1e-30)
+            err = np.abs(st_t[k] - st_s[k]).max() / scale
+            assert err <= 3e-5, (case, path, env, (B, T, ny, nx, n, check), k, err)   # fp32 rounding
+        assert rep_t["iterations"] == n
+        assert rep_t["objective"] == pytest.approx(rep_s["objective"], rel=1e-5, abs=1e-7), (case, path, env)
+        assert rep_t["primal_res"] == pytest.approx(rep_s["primal_res"], rel=1e-4, abs=1e-7), (case, path, env)
