@@ -397,13 +397,13 @@ def main():
         h2d = sum_over_ranks(float(host_pinned.numel() * 4))   # owned frames, all ranks
         d2h = sum_over_ranks(32.0 * 8)                         # report readback (uot_solve), all ranks
 
-        # N = 1, fixed marginals: the pairs are independent given the frames, so the
+        # N = 1 or batched pairs, fixed marginals: the pairs are independent given the frames, so the
         # rank's pairs are solved as K pair-range problems on K streams and the H2D copy of
         # one range (uot_load_frames) overlaps the iterations of the others.  Chains: range
         # [q0, q1) owns frames [q0, q1] (the boundary frame is copied twice).  The work per
         # step is the single problem's (same pairs, iterations and checks).
         chunks = []
-        if world == 1 and not prox and args.e2e_chunks > 1:
+        if (world == 1 or cfg.n_chains > 1) and not prox and args.e2e_chunks > 1:
             K = min(args.e2e_chunks, G)
             del driver
             for i in range(K):
@@ -414,8 +414,8 @@ def main():
                 dfr.copy_(hc)
                 torch.cuda.synchronize(dev)
                 chunks.append((Problem(dfr, cfg.alpha, rho=rho, tau1=tau, tau2=tau, stream=st_i), hc, st_i))
-            h2d = float(sum(c[1].numel() * 4 for c in chunks))
-            d2h = 32.0 * 8 * K
+            h2d = sum_over_ranks(float(sum(c[1].numel() * 4 for c in chunks)))
+            d2h = sum_over_ranks(32.0 * 8 * K)
 
         def e2e_step():
             if chunks:
