@@ -403,8 +403,9 @@ def main():
         # [q0, q1) owns frames [q0, q1] (the boundary frame is copied twice).  The work per
         # step is the single problem's (same pairs, iterations and checks).
         chunks = []
-        if (world == 1 or cfg.n_chains > 1) and not prox and args.e2e_chunks > 1:
-            K = min(args.e2e_chunks, G)
+        K = min(args.e2e_chunks, G)
+        # only where the copy is worth hiding: ranges of >= 16 Mpx keep every problem GPU-filling
+        if (world == 1 or cfg.n_chains > 1) and not prox and K > 1 and G * N // K >= (1 << 24):
             del driver
             for i in range(K):
                 q0, q1 = (G * i) // K, (G * (i + 1)) // K
