@@ -3,17 +3,18 @@
 //
 // One warp owns a strip of 128 columns (32 lanes x one float4 quad) and marches down H + 2S
 // rows of one pair.  At step t it receives row t of the iterate (M, r, a, f; cp.async into a
-// per-warp SMEM ring, 3..5 rows ahead) and advances every level j = 1..S by one row: level
-// j updates row t - j from level j-1's rows t - j (carried in registers) and t - j + 1 (just
-// produced), so the S iterations run as a wavefront with no block barrier and no SMEM
-// traffic beyond the ring.  Horizontal neighbours (a at i+1 for div^*, M_x at i-1 for div)
-// come from the adjacent lane by shuffle; vertical ones are the carried rows.  Each
-// iteration invalidates one more column at each strip side, so lanes 0 and 31 (4 columns
-// each) are halo and the warp writes the 120 columns of lanes 1..30 (S <= 4); the S rows
-// above / below the H output rows are halo likewise (re-read from L2 by the neighbours).
-// K^{j-1} (line 7's previous K) is carried with the level, so div M is evaluated once per
-// pixel and iteration.  The arithmetic per pixel is k_iter's, in the same order.
-// HBM traffic: 36 B per pair-pixel per S iterations (+ 6.7% column and 2S/H row halo, L2).
+// per-warp SMEM ring of 8 rows, 7 - S rows ahead) and advances every level j = 1..S by one
+// row: level j updates row t - j from level j-1's rows t - j (carried in registers) and
+// t - j + 1 (just produced), so the S iterations run as a wavefront with no block barrier
+// and no SMEM traffic beyond the ring.  Horizontal neighbours (a at i+1 for div^*, M_x at
+// i-1 for div) come from the adjacent lane by shuffle; vertical ones are the carried rows.
+// Each iteration invalidates one more column at each strip side, so ceil(S/4) lanes per side
+// are halo: the warp writes the 120 columns of lanes 1..30 (S <= 4) or the 112 of lanes
+// 2..29 (S = 5); the S rows above / below the H output rows are halo likewise (re-read
+// from L2 by the neighbours).  K^{j-1} (line 7's previous K) is carried with the level, so
+// div M is evaluated once per pixel and iteration.  The arithmetic per pixel is k_iter's,
+// in the same order.  HBM traffic: 36 B per pair-pixel per S iterations (+ column and 2S/H
+// row halo, mostly from L2: ncu 1.004x algorithmic at S = 5, H = 512).
 #pragma once
 #include "uot_temporal.cuh"
 
@@ -28,7 +29,7 @@ constexpr int kWaveWarps = 1;                   // warps (independent strips) pe
 template <int S, bool RED> struct WaveCfg {     // warps per SM: registers <= 255 (S >= 4; a 168 cap for
     static constexpr int minb = (S >= 4 ? 8 : 10) / kWaveWarps;   // 10 warps / SM spills and is slower) / 204
 };
-constexpr size_t kWaveSmem = (size_t)kWaveWarps * kWaveRing * 5 * 32 * sizeof(float4);   // 40 KB
+constexpr size_t kWaveSmem = (size_t)kWaveWarps * kWaveRing * 5 * 32 * sizeof(float4);   // 20 KB per warp
 
 struct WaveArgs {
     int nx, ny;                 // nx % 4 == 0, 16-byte aligned planes
