@@ -555,9 +555,8 @@ static void plan_persist(uot_ctx* c) {
 }
 
 template <int TH, int RM>
-static const void* tp_kernel_t(int nt) {
-    return nt == uotk::kT2Wide ? (const void*)uotk::k_tpersist<TH, RM, uotk::kT2Wide>
-                               : (const void*)uotk::k_tpersist<TH, RM, uotk::kT2Threads>;
+static const void* tp_kernel_t(int) {      // 320 threads (640 measured slower on C1 / C2)
+    return (const void*)uotk::k_tpersist<TH, RM, uotk::kT2Threads>;
 }
 static const void* tp_kernel(int th, int rm, int nt) {
     if (th == 36) return rm == 1 ? tp_kernel_t<36, 1>(nt) : (rm == 2 ? tp_kernel_t<36, 2>(nt) : tp_kernel_t<36, 0>(nt));
@@ -753,7 +752,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
         c->tp.tx = (p.nx + kTW - 1) / kTW;
         c->tp.ty = (p.ny + TH - 1) / TH;
         c->tp.smem = TH == 36 ? TB<36, 4>::smem : TB<16, 4>::smem;
-        c->tp.nt = env_int("UOT_TP_NT", kT2Threads) == kT2Wide ? kT2Wide : kT2Threads;
+        c->tp.nt = kT2Threads;
         c->tp.fn = tp_kernel(TH, c->r_mode, c->tp.nt);
         int nb = 0, dev = 0, nsm = kSMs;
         bool ok = cudaFuncSetAttribute(c->tp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->tp.smem) ==
