@@ -210,8 +210,8 @@ int uot_set_temporal(uot_ctx* ctx, int enable);
 /* Kernel that runs the iterations of this context: 0 = k_iter (one pass per iteration),
  * 1 = k_iter2 (SMEM tiles, two iterations per pass, fixed marginals), 2 = k_persist (all
  * iterations of a call in one cooperative launch, small grids), 3 = k_iter2 with
- * four-iteration passes, 5 / 6 = k_wave (register wavefront, 16-byte-aligned planes with
- * nx % 4 == 0) with two / four iterations per pass, 8 = k_tpersist (small grids: all
+ * four-iteration passes, 5 / 6 / 9 = k_wave (register wavefront, 16-byte-aligned planes
+ * with nx % 4 == 0) with two / four / five iterations per pass, 8 = k_tpersist (small grids: all
  * iterations of a call in one cooperative launch of SMEM-tile passes, when every run up to a
  * check has even length; otherwise the per-pass kernels).  Four-iteration contexts fill in
  * with two-iteration passes / k_iter where a reduction falls inside four iterations. */

@@ -1493,7 +1493,8 @@ int uot_kernel_path(const uot_ctx* c) {
     if (!(c->t2ok && c->t2on)) return 0;
     const bool four = c->t4on && c->tv[1].ok;
     const TVar& v = c->tv[four ? 1 : 0];
-    return v.wave ? (four ? 6 : 5) : (four ? 3 : 1);   // the pass kind of long runs
+    if (v.wave && four && c->tv[3].ok) return 9;        // the pass kind of long runs: five per pass
+    return v.wave ? (four ? 6 : 5) : (four ? 3 : 1);
 }
 
 int uot_set_temporal(uot_ctx* c, int enable) {

@@ -337,8 +337,10 @@ def test_temporal_matches_streaming_and_oracle(n, check, tvar):
     _, st_s, rep_s = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 0}, check_every=check)
     prob, st_t, rep_t = gpu_run(fr, 1.4, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 1, "UOT_TPERSIST": 0, **tvar},
                                 check_every=check)
-    kind = "k_wave" if tvar.get("UOT_WAVE", 0) == 1 else "k_iter"
-    assert prob.kernel_path == kind + ("4" if tvar["UOT_T4"] else "2")
+    if tvar.get("UOT_WAVE", 0) == 1:
+        assert prob.kernel_path == ("k_wave5" if tvar["UOT_T4"] else "k_wave2")
+    else:
+        assert prob.kernel_path == ("k_iter4" if tvar["UOT_T4"] else "k_iter2")
     for k in ("mx", "my", "r", "a"):
         scale = max(np.abs(st_s[k]).max(), 1e-30)
         assert np.abs(st_t[k] - st_s[k]).max() <= 1e-5 * scale, k
@@ -394,7 +396,7 @@ def test_path_switching_keeps_the_iterate():
             os.environ.pop("UOT_PERSIST", None)
         else:
             os.environ["UOT_PERSIST"] = old
-    assert prob.kernel_path in ("k_iter2", "k_iter4", "k_wave2", "k_wave4", "k_persist", "k_tpersist")
+    assert prob.kernel_path in ("k_iter2", "k_iter4", "k_wave2", "k_wave4", "k_wave5", "k_persist", "k_tpersist")
     prob.step(7)                       # passes + an odd tail
     prob.set_temporal(False)
     path_off = prob.kernel_path
