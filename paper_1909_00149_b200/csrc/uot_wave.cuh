@@ -259,7 +259,7 @@ struct WaveDfArgs {
 
 constexpr int kWaveDfState = 4;     // rows of the state ring (current + 3 in flight)
 #ifndef UOT_WAVE_DF_WARPS
-#define UOT_WAVE_DF_WARPS 2
+#define UOT_WAVE_DF_WARPS 1
 #endif
 constexpr int kWaveDfWarps = UOT_WAVE_DF_WARPS;    // warps (independent strips) per CTA
 constexpr size_t kWaveDfSmem = (size_t)kWaveDfWarps * (kWaveDfState * 8 + kWaveRing * 2) * 32 * sizeof(float4);
