@@ -661,13 +661,13 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->tv[2].th = 32;                                           // (three- and five-iteration passes: k_wave only)
     c->tv[3].th = 32;
     // register wavefront (k_wave) for 16-byte-aligned planes with nx % 4 == 0 (UOT_WAVE=0: SMEM tiles)
-    // Enough independent strips to fill the GPU: segment height 512 (halved down to 32 for
-    // smaller problems, >= 2 waves of 8 warps per SM); below one wave at 32 rows the SMEM tiles.
+    // Enough independent strips to fill the GPU: segment height 512 (halved down to 16 for
+    // smaller problems, >= 2 waves of 8 warps per SM); below one wave at 16 rows the SMEM tiles.
     const long long strips = (p.nx + kWaveOut - 1) / kWaveOut;
     int wave_h = env_int("UOT_WAVE_H", 0);
     if (wave_h <= 0) {                  // fewer segments = less row halo (C4: 512 rows 6.29e11, 128: 6.18e11)
         wave_h = 512;
-        while (wave_h > 32 && (long long)c->G * strips * ((p.ny + wave_h - 1) / wave_h) < 2LL * kSMs * 8) wave_h /= 2;
+        while (wave_h > 16 && (long long)c->G * strips * ((p.ny + wave_h - 1) / wave_h) < 2LL * kSMs * 8) wave_h /= 2;
     }
     wave_h = std::max(16, wave_h);                              // >= 16: records within uot_scratch_doubles
     const int wenv_wave = env_int("UOT_WAVE", -1);
