@@ -24,14 +24,14 @@ OBJ_RTOL = 1e-4
 ITER_TOL = 1e-3
 
 
-def gpu_run(frames_np, alpha, n, tau, env=None, report=True, check_every=0):
+def gpu_run(frames_np, alpha, n, tau, env=None, report=True, check_every=0, p_norm=1):
     old = {}
     for k, v in (env or {}).items():
         old[k] = os.environ.get(k)
         os.environ[k] = str(v)
     try:
         fr = torch.from_numpy(frames_np).cuda()
-        prob = Problem(fr, alpha, tau1=tau, tau2=tau)
+        prob = Problem(fr, alpha, tau1=tau, tau2=tau, p_norm=p_norm)
     finally:
         for k, v in old.items():
             if v is None:
@@ -525,9 +525,10 @@ def test_wave_edge_shapes(shape, costs):
 
 # ------------------------------------------------------------------ randomized differential test
 def test_random_pass_schedules_match_one_pass_kernel():
-    """Seeded random shapes, iteration counts, check intervals, segment heights and pass
-    splits: the multi-iteration passes (k_wave S = 2..5, SMEM tiles, persistent tiles) give
-    the one-pass kernel's iterates to fp32 rounding and the same residuals."""
+    """Seeded random shapes, iteration counts, check intervals, segment heights, pass splits
+    and residual models (l1, p = 2, balanced): the multi-iteration passes (k_wave S = 2..5,
+    SMEM tiles, persistent tiles) give the one-pass kernel's iterates to fp32 rounding and
+    the same residuals."""
     rng = np.random.default_rng(int(os.environ.get("UOT_RANDOM_SEED", 2024)))
     for case in range(int(os.environ.get("UOT_RANDOM_CASES", 24))):
         B, T = int(rng.integers(1, 3)), int(rng.integers(2, 4))
@@ -535,7 +536,9 @@ def test_random_pass_schedules_match_one_pass_kernel():
         nx = 4 * int(rng.integers(1, 90))
         n = int(rng.integers(1, 37))
         check = int(rng.choice([0, 2, 3, 7, 10]))
-        alpha = float(rng.uniform(0.3, 3.0))
+        variant = int(rng.integers(0, 4))       # residual: l1 (0, 1), p = 2 (2), balanced alpha = inf (3)
+        alpha = math.inf if variant == 3 else float(rng.uniform(0.3, 3.0))
+        p_norm = 2 if variant == 2 else 1
         path = rng.choice(["wave", "tiles", "tpersist"])
         env = {"UOT_PERSIST": 0}
         if path == "wave":
@@ -547,12 +550,15 @@ def test_random_pass_schedules_match_one_pass_kernel():
             env.update(UOT_WAVE=0, UOT_TPERSIST=1)
         fr = inputs.gen_random(B, T, ny, nx, seed=1000 + case, kind=str(rng.choice(["uniform", "sparse"])))
         tau = tau_for(ny, nx)
-        _, st_s, rep_s = gpu_run(fr, alpha, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 0}, check_every=check)
-        _, st_t, rep_t = gpu_run(fr, alpha, n, tau, env=env, check_every=check)
+        _, st_s, rep_s = gpu_run(fr, alpha, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 0}, check_every=check,
+                                 p_norm=p_norm)
+        _, st_t, rep_t = gpu_run(fr, alpha, n, tau, env=env, check_every=check, p_norm=p_norm)
         for k in ("mx", "my", "r", "a"):
             scale = max(np.abs(st_s[k]).max(), 1e-30)
             err = np.abs(st_t[k] - st_s[k]).max() / scale
             assert err <= 3e-5, (case, path, env, (B, T, ny, nx, n, check), k, err)   # fp32 rounding
         assert rep_t["iterations"] == n
-        assert rep_t["objective"] == pytest.approx(rep_s["objective"], rel=1e-5, abs=1e-7), (case, path, env)
+        if math.isfinite(rep_s["objective"]):
+            assert rep_t["objective"] == pytest.approx(rep_s["objective"], rel=1e-5, abs=1e-7), (case, path, env)
         assert rep_t["primal_res"] == pytest.approx(rep_s["primal_res"], rel=1e-4, abs=1e-7), (case, path, env)
+    print(f"random pass schedules: {case + 1} cases")
