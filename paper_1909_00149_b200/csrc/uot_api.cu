@@ -663,7 +663,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     // register wavefront (k_wave) for 16-byte-aligned planes with nx % 4 == 0 (UOT_WAVE=0: SMEM tiles)
     // Enough independent strips to fill the GPU: segment height 512 (halved down to 16 for
     // smaller problems, >= 2 waves of 8 warps per SM); below one wave at 16 rows the SMEM tiles.
-    const long long strips = (p.nx + kWaveOut - 1) / kWaveOut;
+    const long long strips = wave_strips(p.nx, 4);
     int wave_h = env_int("UOT_WAVE_H", 0);
     if (wave_h <= 0) {                  // fewer segments = less row halo (C4: 512 rows 6.29e11, 128: 6.18e11)
         wave_h = 512;
@@ -680,7 +680,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
         v.wave = wave;
         if (wave) {
             v.th = wave_h;
-            v.tx = (p.nx + wave_out(kVarS[k]) - 1) / wave_out(kVarS[k]);
+            v.tx = wave_strips(p.nx, kVarS[k]);
         } else {
             v.tx = (p.nx + kTW - 1) / kTW;
         }

@@ -24,6 +24,13 @@ constexpr int kWaveOut = 120;                   // columns written per warp stri
 // S iterations invalidate S columns at each strip side: ceil(S/4) halo lanes per side
 __host__ __device__ constexpr int wave_halo_lanes(int S) { return (S + 3) / 4; }
 __host__ __device__ constexpr int wave_out(int S) { return 128 - 8 * wave_halo_lanes(S); }
+// Strips of 128 loaded columns start at s * wave_out(S): neighbouring strips overlap by the two
+// halos, the first strip starts at column 0 (nothing is unknown left of the grid) and the last
+// one reaches the right edge (nothing unknown right of it), so those two need no halo lanes on
+// the grid side.  Strips needed for nx columns:
+__host__ __device__ constexpr int wave_strips(int nx, int S) {
+    return nx <= 128 ? 1 : (nx - 128 + wave_out(S) - 1) / wave_out(S) + 1;
+}
 constexpr int kWaveRing = 8;                    // rows per warp in the SMEM ring
 constexpr int kWaveWarps = 1;                   // warps (independent strips) per CTA
 template <int S, bool RED> struct WaveCfg {     // warps per SM: registers <= 255 (S >= 4; a 168 cap for
@@ -73,10 +80,12 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S, RED>::minb) k_wave
     const int pair = (int)(unit / upp), u = (int)(unit - (long long)pair * upp);
     const int sy = u / A.strips, sx = u - sy * A.strips;
     const int nx = A.nx, ny = A.ny;
-    const int gi = sx * OUT - 4 * HL + 4 * lane;                 // first column of this lane's quad
-    const bool lane_in = gi >= 0 && gi < nx;                     // whole quad in the grid (nx % 4 == 0)
+    const int gs = sx * OUT;                                     // first loaded column of the strip
+    const int gi = gs + 4 * lane;                                // first column of this lane's quad
+    const bool lane_in = gi < nx;                                // whole quad in the grid (nx % 4 == 0)
     const bool last_q = gi + 3 == nx - 1;                        // holds the pinned column nx-1 (L3)
-    const bool writer = lane >= HL && lane <= 31 - HL && lane_in;
+    const bool left_edge = lane == 0 && sx == 0;                 // column -1 is outside: M_x there = 0
+    const bool writer = lane_in && (lane >= HL || sx == 0) && (lane <= 31 - HL || gs + 128 >= nx);
     const int y0 = sy * A.H, y1 = min(y0 + A.H, ny);             // output rows [y0, y1)
     const size_t po = (size_t)pair * (size_t)A.N;
     const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1, rsc = A.r_scale;
@@ -88,7 +97,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S, RED>::minb) k_wave
     // column nx-1 / row ny-1 (L3).  Scaling tau1 by 0 there keeps those M components 0 exactly
     // (then div M, K, r, a outside are exact zeros).  Column cut: the 4th pixel of the lane
     // holding column -1 or nx-1; row cut: a row-uniform scale.
-    const float t1x3 = (gi + 3 == -1 || last_q) ? 0.f : t1;
+    const float t1x3 = last_q ? 0.f : t1;
     float4* ring = wring + (size_t)w * (kWaveRing * 5 * 32) + lane;   // [slot][plane][lane]
 
     auto issue = [&](int t) {                                    // row t -> slot t & 7 (zero outside)
@@ -134,7 +143,8 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S, RED>::minb) k_wave
         if (last_q) Mx.w = 0.f;                                  // pinned flux components (L3)
         if (t == ny - 1) My = z4;
         // ---- level 0: K^0 = div M - r - f at row t ----
-        const float mxl0 = __shfl_up_sync(kFull, Mx.w, 1);
+        const float sh0 = __shfl_up_sync(kFull, Mx.w, 1);   // all lanes shuffle, then select
+        const float mxl0 = left_edge ? 0.f : sh0;
         Cv[0].mx = Mx; Cv[0].my = My; Cv[0].r = R; Cv[0].a = s[96];
         Cv[0].k.x = ((Mx.x - mxl0) + (My.x - upY[0].x)) - R.x - F.x;
         Cv[0].k.y = ((Mx.y - Mx.x) + (My.y - upY[0].y)) - R.y - F.y;
@@ -167,7 +177,8 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S, RED>::minb) k_wave
                 if (RED && j == S) nrm[v] = fmaxf(fmaf(n2, fminf(inv, 1e30f), -t1), 0.f);
             }
             // lines 5-7: r^j, a^j, K^j at rho from M^j (left neighbour by shuffle, up carried)
-            const float mxl = __shfl_up_sync(kFull, nmx[3], 1);
+            const float shl = __shfl_up_sync(kFull, nmx[3], 1);   // all lanes shuffle, then select
+            const float mxl = left_edge ? 0.f : shl;
             const float wr = (writer && rho >= y0 && rho < y1) ? 1.f : 0.f;   // output pixel (reductions)
             const float4 Fr = ring[(rho & (kWaveRing - 1)) * (5 * 32) + 128];
             const float mxv[5] = {mxl, nmx[0], nmx[1], nmx[2], nmx[3]};
@@ -279,15 +290,17 @@ __global__ void __launch_bounds__(kWaveDfWarps * 32, 8 / kWaveDfWarps) k_wave_df
     const int pair = (int)(unit / upp), u = (int)(unit - (long long)pair * upp);
     const int sy = u / A.strips, sx = u - sy * A.strips;
     const int nx = A.nx, ny = A.ny;
-    const int gi = sx * kWaveOut - 4 + 4 * lane;
-    const bool lane_in = gi >= 0 && gi < nx;
+    const int gs = sx * kWaveOut;                                // strip layout as k_wave (wave_strips)
+    const int gi = gs + 4 * lane;
+    const bool lane_in = gi < nx;
     const bool last_q = gi + 3 == nx - 1;
-    const bool writer = lane >= 1 && lane <= 30 && lane_in;
+    const bool left_edge = lane == 0 && sx == 0;
+    const bool writer = lane_in && (lane >= 1 || sx == 0) && (lane <= 30 || gs + 128 >= nx);
     const int y0 = sy * A.H, y1 = min(y0 + A.H, ny);
     const size_t po = (size_t)pair * (size_t)A.N, pz = ((size_t)pair * 2 + 1) * (size_t)A.N;
     const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1, rsc = A.r_scale;
     const float c1 = A.c1, c2 = A.c2, c3 = A.c3, rho = A.rho, i1r = A.inv1prho;
-    const float t1x3 = (gi + 3 == -1 || last_q) ? 0.f : t1;
+    const float t1x3 = last_q ? 0.f : t1;
     float4* sring = wdring + (size_t)w * ((kWaveDfState * 8 + kWaveRing * 2) * 32) + lane;   // [slot][8][lane]
     float4* cring = sring + kWaveDfState * 8 * 32;                                            // [slot][2][lane]
 
@@ -337,7 +350,8 @@ __global__ void __launch_bounds__(kWaveDfWarps * 32, 8 / kWaveDfWarps) k_wave_df
         if (last_q) Mx.w = 0.f;                                  // pinned flux components (L3)
         if (t == ny - 1) My = z4;
         // level 0: K^0 = div M - r - (z - s0)
-        const float mxl0 = __shfl_up_sync(kFull, Mx.w, 1);
+        const float sh0 = __shfl_up_sync(kFull, Mx.w, 1);   // all lanes shuffle, then select
+        const float mxl0 = left_edge ? 0.f : sh0;
         Cv[0].mx = Mx; Cv[0].my = My; Cv[0].r = R; Cv[0].a = s[96]; Cv[0].z = Z;
         Cv[0].x = s[160]; Cv[0].ax = s[192]; Cv[0].b = s[224];
         Cv[0].k.x = ((Mx.x - mxl0) + (My.x - upY[0].x)) - R.x - (Z.x - S0.x);
@@ -367,7 +381,8 @@ __global__ void __launch_bounds__(kWaveDfWarps * 32, 8 / kWaveDfWarps) k_wave_df
                 nmy[v] = sf * qy;
                 if (RED && j == S) nrm[v] = fmaxf(fmaf(n2, fminf(inv, 1e30f), -t1), 0.f);
             }
-            const float mxl = __shfl_up_sync(kFull, nmx[3], 1);
+            const float shl = __shfl_up_sync(kFull, nmx[3], 1);   // all lanes shuffle, then select
+            const float mxl = left_edge ? 0.f : shl;
             const float wr = (writer && rho_ >= y0 && rho_ < y1) ? 1.f : 0.f;
             const float4* cr = cring + (rho_ & (kWaveRing - 1)) * (2 * 32);
             const float4 Yr = cr[0], S0r = cr[32];
