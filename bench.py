@@ -176,6 +176,39 @@ def cpu_oracle_rate(cfg, seconds_target=12.0, rho=math.inf):
     return pairs * N * its / dt, threads, sample, dt
 
 
+def lscpu_info():
+    """Host CPU model / sockets / cores (BASELINE.md section 4 protocol)."""
+    info = {}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            k, v = k.strip(), v.strip()
+            if k in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "CPU(s)"):
+                info[k] = v
+    except Exception as ex:
+        info["error"] = str(ex)
+    return info
+
+
+def cpu_oracle_rate_1thread(cfg, seconds_target, rho):
+    """The same oracle sample with OMP_NUM_THREADS=1 (OpenMP reads it at start-up, so in a
+    child process).  Returns (px-it/s, sample) or (None, reason)."""
+    code = ("import json, math, sys; sys.path.insert(0, %r); import bench; "
+            "from paper_1909_00149_b200 import inputs; "
+            "r = bench.cpu_oracle_rate(inputs.CONFIGS[%r], %r, rho=%r); print(json.dumps([r[0], r[2]]))"
+            % (ROOT, cfg.name, seconds_target, rho if math.isfinite(rho) else float("inf")))
+    code = code.replace("rho=inf", "rho=float('inf')")
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                             timeout=20 * seconds_target + 120)
+        v, sample = json.loads(out.stdout.strip().splitlines()[-1])
+        return v, sample
+    except Exception as ex:
+        return None, f"failed: {ex}"
+
+
 # ------------------------------------------------------------------------------------------ reference arm
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
@@ -211,8 +244,33 @@ def config_dict(cfg, gpus, mode="fixed"):
 
 
 # ------------------------------------------------------------------------------------------ main arm
+def relaunch_distributed(args):
+    """`python bench.py --gpus N` without a launcher: start N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1 and return its exit code; rank 0 prints the JSON line.
+    NCCL's communicator-init lines go to stderr (NCCL_DEBUG=INFO, subsystem INIT) so the rank
+    count of every communicator is visible in the log."""
+    import socket
+    import torch
+    if torch.cuda.device_count() < args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but only {torch.cuda.device_count()} CUDA devices are visible")
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args)
     from paper_1909_00149_b200 import inputs
     cfg = inputs.CONFIGS[args.config]
     if args.iters:
@@ -234,6 +292,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # communicator-init lines (rank counts) on stderr, also when a launcher started us
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
 
     # ---- this rank's shard: pairs [p0, p1) -> frames [p0, p1] (last = shared boundary frame)
@@ -395,7 +457,9 @@ def main():
     e2e = None
     if not args.no_e2e:
         h2d = sum_over_ranks(float(host_pinned.numel() * 4))   # owned frames, all ranks
-        d2h = sum_over_ranks(32.0 * 8)                         # report readback (uot_solve), all ranks
+        # the step's result read back: the per-pair objective / certificate rows of the 255
+        # evaluated regularisers (uot_objective, 8 doubles per pair) + the solve report
+        d2h = sum_over_ranks(float(G * 8 * 8 + 32 * 8))
 
         # N = 1 or batched pairs, fixed marginals: the pairs are independent given the frames, so the
         # rank's pairs are solved as K pair-range problems on K streams and the H2D copy of
@@ -416,7 +480,7 @@ def main():
                 torch.cuda.synchronize(dev)
                 chunks.append((Problem(dfr, cfg.alpha, rho=rho, tau1=tau, tau2=tau, stream=st_i), hc, st_i))
             h2d = sum_over_ranks(float(sum(c[1].numel() * 4 for c in chunks)))
-            d2h = sum_over_ranks(32.0 * 8 * K)
+            d2h = sum_over_ranks(float(G * 8 * 8 + 32 * 8 * K))
 
         def e2e_step():
             if chunks:
@@ -424,13 +488,17 @@ def main():
                     p_i.load_frames_host(hc)
                     p_i.reset()
                     p_i.iterate(cfg.iters, check_every=args.check_every, tol=1e-12)
-                return {"iterations": min(p_i.report()["iterations"] for p_i, _, _ in chunks)}
+                its = min(p_i.report()["iterations"] for p_i, _, _ in chunks)
+                rows = [p_i.objective(per_pair=True)[1] for p_i, _, _ in chunks]   # D2H of the result
+                return {"iterations": its, "rows": sum(r.shape[0] for r in rows)}
             if world == 1:                  # the C-ABI's own H2D (uot_load_frames) from pinned host memory
                 prob.load_frames_host(host_pinned)
             else:                           # owned frames + the boundary frame from the next rank (NCCL)
                 upload(host_pinned)
             prob.reset()
-            return driver.run(cfg.iters, check_every=args.check_every, tol=1e-12)
+            rep = driver.run(cfg.iters, check_every=args.check_every, tol=1e-12)
+            rows = prob.objective(per_pair=True)[1]                               # D2H of the result
+            return {"iterations": rep["iterations"], "rows": rows.shape[0]}
 
         for _ in range(max(1, args.warmup // 2)):
             e2e_step()
@@ -458,7 +526,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             rate, threads, sample, _ = cpu_oracle_rate(cfg, args.cpu_seconds, rho=rho)
-            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
+            r1, s1 = cpu_oracle_rate_1thread(cfg, max(2.0, args.cpu_seconds / 3), rho)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                   "one_thread": {"value": r1, "unit": UNIT, "cores": 1, "sample": s1},
+                   "host": lscpu_info()}
         except Exception as ex:   # the oracle is a reported baseline, not the product
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {ex}"}
 
@@ -474,13 +545,20 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": kernel_name,
                          "alg_bytes_per_launch": alg_bytes_launch, "avg_launch_ms": avg_launch_s * 1e3,
-                         "launches_timed": dom_n, "kernels_in_step": shares, "peak_source": peak_src},
+                         "launches_timed": dom_n, "kernels_in_step": shares, "peak_source": peak_src,
+                         "traffic_source": "profiles/ncu_summary.json: dram__bytes_read.sum + dram__bytes_write.sum "
+                                           "per launch from an ncu --set full capture of this kernel on this config "
+                                           "(stored, not measured in this run)" if traffic else None},
             "one_pass_kernel": one_pass,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "hbm_gbs_step": alg_gbs_job,
+            # one-pass-equivalent ALGORITHMIC bandwidth of the whole step (36 B per px-it, as if every
+            # iteration were its own HBM pass): a rate, not a DRAM measurement -- it exceeds the HBM
+            # peak because the passes fuse up to five iterations; see roofline for the DRAM side
+            "alg_equiv_gbs_step": alg_gbs_job,
+            "dram_bytes_per_step_est": (traffic * dom_n / max(min(args.steps, 3), 1)) if traffic else None,
             "objective": last["objective"], "iterations_per_step": iters_done // args.steps,
         }
         print(json.dumps(line), flush=True)

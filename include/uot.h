@@ -145,7 +145,11 @@ int uot_load_frames(uot_ctx* ctx, const float* host_frames);
  * reductions every check_every-th iteration (0 = none) and on the last one;
  * tol > 0 arms the device-side stopping test (L13) -- later launches exit
  * immediately once it passes.  No host synchronisation; read the result with
- * uot_get_report. */
+ * uot_get_report.  A stop armed this way stays pending until uot_get_report, or until
+ * the next entry point that enqueues work on the iterate (uot_iterate, _part,
+ * uot_prox_step, uot_solve, uot_objective, uot_load_frames), which first synchronises
+ * the stream once and applies it; under graph capture such a call returns
+ * UOT_E_INVALID instead.  uot_reset discards it. */
 int uot_iterate(uot_ctx* ctx, int32_t n_iters, int32_t check_every, double tol);
 
 /* One iteration restricted to a part of the pairs, for overlapping the shard
@@ -169,7 +173,7 @@ int uot_get_report(uot_ctx* ctx, uot_report* out);
  * started from -- device copies are appended when the passes flipped them -- so every
  * replay continues from the previous one; replays do not advance the context's
  * iteration count); out != NULL: the last iteration also computes the reductions and
- * the call synchronises the stream to fill *out. */
+ * the call synchronises the stream to fill *out (UOT_E_INVALID under graph capture). */
 int uot_prox_step(uot_ctx* ctx, int32_t n_iters, uot_report* out);
 
 /* Iterate until primal_res <= tol*max(f_norm, 1e-30) and dual_res <= the same
@@ -216,6 +220,25 @@ int uot_set_temporal(uot_ctx* ctx, int enable);
  * check has even length; otherwise the per-pass kernels).  Four-iteration contexts fill in
  * with two-iteration passes / k_iter where a reduction falls inside four iterations. */
 int uot_kernel_path(const uot_ctx* ctx);
+
+/* Cross-rank stopping test for a chain sharded over ranks: the
+ * L13 test must use the residuals and ||f|| summed over ALL shards, so no rank may stop on
+ * its own sums.  Stream-ordered, no host synchronisation:
+ *   uot_stop_external(ctx)            arm the stop flag (launches exit once it is set) with
+ *                                     the local test disabled, until uot_get_report;
+ *   uot_iterate(ctx, d, d, 0.0)       a chunk of d iterations, reductions on its last;
+ *   uot_stop_pack(ctx, sums8)         sums8 (8 device doubles, caller-owned) <- this rank's
+ *                                     [transport, growth, ||K||^2, ||dz||^2, ub, prox, ||f||^2,
+ *                                     nonfinite] of the last checked iteration;
+ *   (caller: all-reduce sums8 over the ranks, e.g. ncclAllReduce sum, same stream order)
+ *   uot_stop_apply(ctx, sums8, tol)   set the stop if the GLOBAL sums pass the L13 test
+ *                                     (or any rank saw a non-finite value).
+ * Every rank takes the same decision at the same iteration; uot_get_report rewinds to it.
+ * UOT_E_INVALID: NULL pointers, uot_stop_apply without uot_stop_external, or
+ * uot_iterate(tol > 0) while armed. */
+int uot_stop_external(uot_ctx* ctx);
+int uot_stop_pack(uot_ctx* ctx, double* sums8);
+int uot_stop_apply(uot_ctx* ctx, const double* sums8, double tol);
 
 /* CUDA kernels launched by this context since creation (for accounting). */
 int64_t uot_launch_count(const uot_ctx* ctx);

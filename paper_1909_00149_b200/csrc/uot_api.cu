@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(256) k_objective(const ObjArgs O) {
         mg = fmax(mg, sqrt(gx * gx + gy * gy));
         ma = fmax(ma, fabs((double)a[k]));
         if (O.p != nullptr) {
-            const int s_hi = (t == O.P - 1) ? t + 1 : t;         // frames attributed to pair t
+            // frames attributed to pair t; a shard's last frame belongs to the next rank
+            const int s_hi = (t == O.P - 1 && !O.next_owns_last) ? t + 1 : t;
             for (int s = t; s <= s_hi; ++s) {
                 const size_t fo = ((size_t)b * O.T + s) * (size_t)O.N + k;
                 const double d = (double)O.x[fo] - (double)O.p[fo];
@@ -320,6 +321,25 @@ __global__ void k_init_glob(double* glob, int* stop, int* counter, int reset_all
     }
 }
 
+// Cross-rank stopping test (uot_stop_pack / uot_stop_apply): pack this rank's sums of the last
+// checked iteration; after the caller's all-reduce, apply the L13 test to the GLOBAL sums.
+__global__ void k_stop_pack(const double* glob, double* out) {
+    if (threadIdx.x < 6) out[threadIdx.x] = glob[threadIdx.x];     // TR GR K2 DZ UB PX
+    if (threadIdx.x == 6) out[6] = glob[GL_FSQ];
+    if (threadIdx.x == 7) out[7] = glob[GL_NONF];
+}
+__global__ void k_stop_apply(const double* sums, double* glob, int* stop, double tol, double tau1) {
+    if (threadIdx.x != 0 || *stop) return;
+    if (sums[7] != 0.0) { glob[GL_NONF] = 1.0; *stop = 1; return; }
+    if (!(tol > 0.0)) return;
+    const double scale = tol * fmax(sqrt(sums[6]), 1e-30);
+    if (sqrt(sums[2]) <= scale && sqrt(sums[3]) / tau1 <= scale) {
+        glob[GL_CONV] = glob[GL_LASTRED];
+        __threadfence();
+        *stop = 1;
+    }
+}
+
 }  // namespace uotk
 
 // ============================================================================ host side
@@ -397,6 +417,7 @@ struct uot_ctx {
     int fix_first;
     bool timing;
     bool stop_armed;
+    bool ext_stop;       // stop armed by uot_stop_external: the test runs in uot_stop_apply (global sums)
     int slot;            // ping-pong slot of mx/my/a(/x) holding the current iterate
     int rcur;            // 0: r holds the current r, 1: r_alt (after an odd number of k_iter2 passes)
     bool t2ok;           // temporally blocked fixed-marginal kernel available (r_alt given)
@@ -799,6 +820,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->err[0] = 0;
     c->timing = false;
     c->stop_armed = false;
+    c->ext_stop = false;
     c->persist_launches = 0;
     c->ev_used = 0;
     *out = c;
@@ -825,6 +847,8 @@ static int launch_setup(uot_ctx* c) {
     return check_launch(c, "k_pair_reduce(setup)");
 }
 
+static int resolve_pending(uot_ctx* c);
+
 int uot_reset(uot_ctx* c, uint32_t flags) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     const size_t bytes = (size_t)c->G * c->N * sizeof(float);
@@ -834,6 +858,8 @@ int uot_reset(uot_ctx* c, uint32_t flags) {
     cudaMemsetAsync(c->b.a[0], 0, bytes, c->s);
     c->slot = 0;
     c->rcur = 0;
+    c->stop_armed = false;          // the cold start supersedes any pending device-side stop
+    c->ext_stop = false;
     c->log.clear();
     c->persist_base.clear();
     int rc = check_launch(c, "memset", false);
@@ -854,6 +880,8 @@ int uot_reset(uot_ctx* c, uint32_t flags) {
 
 int uot_load_frames(uot_ctx* c, const float* host_frames) {
     if (!c || !host_frames) return fail(c, UOT_E_INVALID, "null argument");
+    int prc = resolve_pending(c);       // the setup reduction rewrites the report slots
+    if (prc) return prc;
     const size_t bytes = (size_t)c->B * c->T * c->N * sizeof(float);
     cudaError_t e = cudaMemcpyAsync(const_cast<float*>(c->b.frames), host_frames, bytes, cudaMemcpyHostToDevice, c->s);
     if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "cudaMemcpyAsync: %s", cudaGetErrorString(e));
@@ -1271,6 +1299,12 @@ static void fill_report(const uot_ctx* c, const double* h, uot_report* out) {
 int uot_iterate(uot_ctx* c, int32_t n, int32_t check_every, double tol) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     if (n < 0 || check_every < 0) return fail(c, UOT_E_INVALID, "n_iters and check_every must be >= 0");
+    if (c->ext_stop) {                   // one chunk of a cross-rank stopped run: no local test
+        if (tol > 0.0) return fail(c, UOT_E_INVALID, "external stop armed: pass tol = 0 and test with uot_stop_apply");
+        return launch_iters(c, n, check_every, n > 0, c->stop, 0.0);
+    }
+    int prc = resolve_pending(c);
+    if (prc) return prc;
     const int* stop = nullptr;
     if (tol > 0.0) {
         k_init_glob<<<1, 32, 0, c->s>>>(c->glob, c->stop, c->counter, 0);
@@ -1289,7 +1323,54 @@ int uot_iterate_part(uot_ctx* c, int32_t part, int32_t reduce) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     if (part != UOT_PART_ALL && part != UOT_PART_INTERIOR && part != UOT_PART_BOUNDARY)
         return fail(c, UOT_E_INVALID, "bad part %d", part);
+    if (c->ext_stop) return launch_one(c, part, reduce != 0, c->stop, 0.0);
+    int prc = resolve_pending(c);
+    if (prc) return prc;
     return launch_one(c, part, reduce != 0, nullptr, 0.0);
+}
+
+// Apply a device-side stop armed by uot_iterate(tol > 0) / uot_solve: the launches after
+// the stopping iteration exited without writing, so the host's iteration count, slot and r
+// buffer are rewound to the stop entry of the launch log.
+static void apply_stop(uot_ctx* c, const double* h) {
+    if (!c->stop_armed) return;
+    const int64_t planned = c->iter;
+    if (h[GL_CONV] >= 0.0) c->iter = (int64_t)h[GL_CONV];             // later launches exited early
+    else if (h[GL_NONF] != 0.0 && h[GL_LASTRED] > 0) c->iter = (int64_t)h[GL_LASTRED];
+    if (c->iter != planned) {
+        // slot / r buffer of the iterate the device stopped at: replay the launch log
+        // (a k_iter2 pass advances 2 iterations but flips the slots once)
+        bool found = false;
+        for (const auto& e : c->log)
+            if (e.iter == c->iter) { c->slot = e.slot; c->rcur = e.rcur; found = true; break; }
+        if (!found)                                                   // stopped inside a persistent launch
+            for (const auto& e : c->persist_base)
+                if (e.iter <= c->iter) { c->slot = e.slot ^ (int)((c->iter - e.iter) & 1); c->rcur = e.rcur; }
+    }
+    c->stop_armed = false;
+    c->ext_stop = false;
+    c->log.clear();
+    c->persist_base.clear();
+}
+
+static bool capturing(const uot_ctx* c) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(c->s, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusActive;
+}
+
+// Every entry point that enqueues work on the iterate first resolves a stop armed by an
+// earlier asynchronous uot_iterate(tol > 0): otherwise it would read a slot the device may
+// never have written, and a later report would rewind past its work.  Resolving needs one
+// stream synchronisation, which a graph capture cannot contain.
+static int resolve_pending(uot_ctx* c) {
+    if (!c->stop_armed) return UOT_OK;
+    if (capturing(c))
+        return fail(c, UOT_E_INVALID, "a device-side stop is pending: call uot_get_report before capturing");
+    double h[GL_N];
+    int rc = read_glob(c, h);
+    if (rc) return rc;
+    apply_stop(c, h);
+    return UOT_OK;
 }
 
 int uot_get_report(uot_ctx* c, uot_report* out) {
@@ -1297,24 +1378,7 @@ int uot_get_report(uot_ctx* c, uot_report* out) {
     double h[GL_N];
     int rc = read_glob(c, h);
     if (rc) return rc;
-    if (c->stop_armed) {
-        const int64_t planned = c->iter;
-        if (h[GL_CONV] >= 0.0) c->iter = (int64_t)h[GL_CONV];             // later launches exited early
-        else if (h[GL_NONF] != 0.0 && h[GL_LASTRED] > 0) c->iter = (int64_t)h[GL_LASTRED];
-        if (c->iter != planned) {
-            // slot / r buffer of the iterate the device stopped at: replay the launch log
-            // (a k_iter2 pass advances 2 iterations but flips the slots once)
-            bool found = false;
-            for (const auto& e : c->log)
-                if (e.iter == c->iter) { c->slot = e.slot; c->rcur = e.rcur; found = true; break; }
-            if (!found)                                                   // stopped inside a persistent launch
-                for (const auto& e : c->persist_base)
-                    if (e.iter <= c->iter) { c->slot = e.slot ^ (int)((c->iter - e.iter) & 1); c->rcur = e.rcur; }
-        }
-        c->stop_armed = false;
-        c->log.clear();
-        c->persist_base.clear();
-    }
+    apply_stop(c, h);
     uot_report rep;
     fill_report(c, h, &rep);
     if (out) *out = rep;
@@ -1325,15 +1389,17 @@ int uot_get_report(uot_ctx* c, uot_report* out) {
 int uot_prox_step(uot_ctx* c, int32_t n, uot_report* out) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     if (n < 0) return fail(c, UOT_E_INVALID, "n_iters < 0");
+    const bool cap = capturing(c);
+    if (cap && out) return fail(c, UOT_E_INVALID, "a host report needs a stream synchronisation: pass out = NULL under graph capture");
+    int rc = resolve_pending(c);
+    if (rc) return rc;
     const int slot0 = c->slot, rcur0 = c->rcur;
-    int rc = launch_iters(c, n, 0, out != nullptr && n > 0, nullptr, 0.0);
+    rc = launch_iters(c, n, 0, out != nullptr && n > 0, nullptr, 0.0);
     if (rc) return rc;
     // Under CUDA-graph capture every replay re-runs the captured launches with the captured
     // buffer pointers, so the call must end in the slots it started from: copy the iterate
     // back when the passes flipped them an odd number of times.
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(c->s, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusActive &&
-        (c->slot != slot0 || c->rcur != rcur0)) {
+    if (cap && (c->slot != slot0 || c->rcur != rcur0)) {
         const size_t plane = (size_t)c->G * c->N * sizeof(float);
         cudaError_t e = cudaSuccess;
         if (c->slot != slot0) {
@@ -1356,6 +1422,8 @@ int uot_prox_step(uot_ctx* c, int32_t n, uot_report* out) {
 int uot_solve(uot_ctx* c, int32_t max_iters, double tol, int32_t check_every, uot_report* out) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     if (max_iters < 0 || check_every < 1) return fail(c, UOT_E_INVALID, "max_iters >= 0 and check_every >= 1 required");
+    int prc = resolve_pending(c);
+    if (prc) return prc;
     // always arm the device-side stop (tol <= 0 never triggers it, but non-finite values do)
     k_init_glob<<<1, 32, 0, c->s>>>(c->glob, c->stop, c->counter, 0);
     int rc = check_launch(c, "k_init_glob");
@@ -1376,11 +1444,14 @@ int uot_solve(uot_ctx* c, int32_t max_iters, double tol, int32_t check_every, uo
 
 int uot_objective(uot_ctx* c, double* per_pair, uot_report* out) {
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    int prc = resolve_pending(c);
+    if (prc) return prc;
     const int slot = c->slot;
     ObjArgs O{};
     O.nx = c->nx; O.ny = c->ny; O.T = c->T; O.P = c->P; O.N = c->N; O.bpp = c->bpp;
     O.x = c->prox ? c->b.x[slot] : c->b.frames;
     O.p = c->prox ? c->b.frames : nullptr;
+    O.next_owns_last = c->b.a_next_halo != nullptr;
     O.mx = c->b.mx[slot]; O.my = c->b.my[slot]; O.r = rbuf(c); O.a = c->b.a[slot];
     O.partials = c->part;
     O.p2 = c->r_mode == 1;
@@ -1502,6 +1573,34 @@ int uot_set_temporal(uot_ctx* c, int enable) {
     if (enable && !c->t2ok) return fail(c, UOT_E_INVALID, "k_iter2 unavailable (prox mode, no r_alt, or UOT_TEMPORAL=0)");
     c->t2on = enable != 0;
     return UOT_OK;
+}
+
+int uot_stop_external(uot_ctx* c) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    int rc = resolve_pending(c);
+    if (rc) return rc;
+    k_init_glob<<<1, 32, 0, c->s>>>(c->glob, c->stop, c->counter, 0);
+    rc = check_launch(c, "k_init_glob");
+    if (rc) return rc;
+    c->stop_armed = true;
+    c->ext_stop = true;
+    c->log.clear();
+    c->persist_base.clear();
+    c->log.push_back({c->iter, c->slot, c->rcur});
+    return UOT_OK;
+}
+
+int uot_stop_pack(uot_ctx* c, double* sums8) {
+    if (!c || !sums8) return fail(c, UOT_E_INVALID, "null argument");
+    k_stop_pack<<<1, 32, 0, c->s>>>(c->glob, sums8);
+    return check_launch(c, "k_stop_pack");
+}
+
+int uot_stop_apply(uot_ctx* c, const double* sums8, double tol) {
+    if (!c || !sums8) return fail(c, UOT_E_INVALID, "null argument");
+    if (!c->ext_stop) return fail(c, UOT_E_INVALID, "uot_stop_external was not called");
+    k_stop_apply<<<1, 32, 0, c->s>>>(sums8, c->glob, c->stop, tol, c->tau1);
+    return check_launch(c, "k_stop_apply");
 }
 
 int64_t uot_launch_count(const uot_ctx* c) { return c ? c->launches : -1; }

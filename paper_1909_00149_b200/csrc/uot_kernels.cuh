@@ -212,7 +212,7 @@ k_iter(const IterArgs A) {
     const float* __restrict__ p0i = nullptr; const float* __restrict__ p1i = nullptr;
     const float* __restrict__ ami = nullptr; const float* __restrict__ api = nullptr;
     float* __restrict__ x0o = nullptr; float* __restrict__ x1o = nullptr;
-    bool last_pair = false;
+    bool last_pair = false, own_last = false;
     const float* __restrict__ ypi = nullptr;
     float* __restrict__ xap = nullptr; float* __restrict__ aap = nullptr; float* __restrict__ bap = nullptr;
     float* __restrict__ sop = nullptr;
@@ -229,6 +229,9 @@ k_iter(const IterArgs A) {
         p0i = A.p + f0; p1i = p0i + A.N;
         x0o = A.x_out + f0;
         last_pair = (t == A.P - 1);
+        // the shard's last frame is the next rank's first frame when a next halo exists: both
+        // ranks update it (bit-identically), only the owner (the next rank) reduces its terms
+        own_last = last_pair && A.a_next_halo == nullptr;
         if (last_pair) x1o = x0o + A.N;
         ami = (t > 0) ? A.a_in + po - A.N : (A.a_prev_halo ? A.a_prev_halo + (size_t)b * A.N : nullptr);
         api = (t < A.P - 1) ? A.a_in + po + A.N : (A.a_next_halo ? A.a_next_halo + (size_t)b * A.N : nullptr);
@@ -434,7 +437,7 @@ k_iter(const IterArgs A) {
                     const float d0 = x0n[v] - c_x0[v], e0 = x0n[v] - c_p0[v];
                     s_dz += d0 * d0;
                     s_px += e0 * e0;
-                    if (last_pair) {
+                    if (own_last) {
                         const float d1 = x1n[v] - c_x1[v], e1 = x1n[v] - c_p1[v];
                         s_dz += d1 * d1;
                         s_px += e1 * e1;
@@ -508,6 +511,7 @@ struct ObjArgs {
     const float* mx; const float* my; const float* r; const float* a;
     double* partials;
     int p2;                   // p = 2 sums (r^2, (div M - f)^2)
+    int next_owns_last;       // shard with a next halo: its last frame is reduced by the next rank
 };
 __global__ void __launch_bounds__(256) k_objective(const ObjArgs O);
 

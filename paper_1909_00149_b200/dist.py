@@ -24,23 +24,57 @@ def shard_range(n_pairs: int, world: int, rank: int):
     return p0, p1
 
 
+def _staged(t: torch.Tensor, group=None) -> bool:
+    """gloo has no CUDA point-to-point: device tensors go through host copies (the CPU
+    multi-process tests run two ranks on one device this way).  NCCL moves them directly."""
+    return t.is_cuda and dist.get_backend(group) != "nccl"
+
+
+def _p2p(sends, recvs, group=None):
+    """Grouped point-to-point: sends = [(tensor, peer)], recvs = [(tensor, peer)] (filled in
+    place).  Returns the works; staged (gloo) transfers complete before returning."""
+    if not sends and not recvs:
+        return []
+    probe = (sends or recvs)[0][0]
+    if _staged(probe, group):
+        ops, fix = [], []
+        for t, peer in sends:
+            ops.append(dist.P2POp(dist.isend, t.detach().cpu().contiguous(), peer, group))
+        for t, peer in recvs:
+            h = torch.empty(t.shape, dtype=t.dtype)
+            ops.append(dist.P2POp(dist.irecv, h, peer, group))
+            fix.append((t, h))
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        for t, h in fix:
+            t.copy_(h)
+        return []
+    ops = [dist.P2POp(dist.isend, t.contiguous(), peer, group) for t, peer in sends]
+    ops += [dist.P2POp(dist.irecv, t, peer, group) for t, peer in recvs]
+    return dist.batch_isend_irecv(ops)
+
+
+def all_reduce_sum_(t: torch.Tensor, group=None):
+    """In-place sum over ranks (NCCL on the current stream; gloo through a host copy)."""
+    if _staged(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, group=group)
+
+
 def exchange_boundary_frame(frames: torch.Tensor, rank: int, world: int, group=None):
     """frames: [1][n][ny][nx] of this rank (frames p0..p1).  Send frame 0 to
     rank-1 (its boundary frame), receive frame n-1 from rank+1.  The last rank
     owns its final frame.  Grouped P2P so neither side blocks the other."""
     if world == 1:
         return
-    ops = []
-    send_buf = frames[:, 0].contiguous()
-    recv_buf = None
-    if rank > 0:
-        ops.append(dist.P2POp(dist.isend, send_buf, rank - 1, group))
-    if rank < world - 1:
-        recv_buf = torch.empty_like(frames[:, -1])
-        ops.append(dist.P2POp(dist.irecv, recv_buf, rank + 1, group))
-    if ops:
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
+    recv_buf = torch.empty_like(frames[:, -1]) if rank < world - 1 else None
+    works = _p2p([(frames[:, 0].contiguous(), rank - 1)] if rank > 0 else [],
+                 [(recv_buf, rank + 1)] if recv_buf is not None else [], group)
+    for w in works:
+        w.wait()
     if recv_buf is not None:
         frames[:, -1].copy_(recv_buf)
 
@@ -52,14 +86,14 @@ def exchange_boundary_duals(a_first: torch.Tensor, a_last: torch.Tensor, prev_ha
     wait=False returns the works (the caller waits before the boundary pairs)."""
     if world == 1:
         return []
-    ops = []
+    sends, recvs = [], []
     if rank > 0:
-        ops.append(dist.P2POp(dist.isend, a_first.contiguous(), rank - 1, group))
-        ops.append(dist.P2POp(dist.irecv, prev_halo, rank - 1, group))
+        sends.append((a_first, rank - 1))
+        recvs.append((prev_halo, rank - 1))
     if rank < world - 1:
-        ops.append(dist.P2POp(dist.isend, a_last.contiguous(), rank + 1, group))
-        ops.append(dist.P2POp(dist.irecv, next_halo, rank + 1, group))
-    works = dist.batch_isend_irecv(ops)
+        sends.append((a_last, rank + 1))
+        recvs.append((next_halo, rank + 1))
+    works = _p2p(sends, recvs, group)
     if wait:
         for w in works:
             w.wait()
@@ -67,13 +101,14 @@ def exchange_boundary_duals(a_first: torch.Tensor, a_last: torch.Tensor, prev_ha
     return works
 
 
-def all_reduce_report(rep: dict, device, keys=("objective", "transport", "growth", "prox_term", "upper_bound")):
+def all_reduce_report(rep: dict, device, keys=("objective", "transport", "growth", "prox_term", "upper_bound"),
+                      group=None):
     """Sum additive report fields over ranks (residual norms combine as sqrt of summed squares)."""
-    if not dist.is_initialized() or dist.get_world_size() == 1:
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return dict(rep)
     v = [rep[k] for k in keys] + [rep["primal_res"] ** 2, (rep["dual_res"]) ** 2, rep["f_norm"] ** 2]
     t = torch.tensor(v, dtype=torch.float64, device=device)
-    dist.all_reduce(t)
+    all_reduce_sum_(t, group)
     out = dict(rep)
     for i, k in enumerate(keys):
         out[k] = float(t[i])
@@ -86,12 +121,17 @@ def all_reduce_report(rep: dict, device, keys=("objective", "transport", "growth
 class ShardedChain:
     """Drive one rank's shard of a chain (or batch) problem (a `uot.Problem`).
 
-    Fixed marginals: iterations have no data-path exchange -- one async
-    `uot_iterate` call.  Chain prox with world > 1: every iteration k sends the
-    shard's first/last pair duals a^k to the neighbours (NCCL P2P over NVLink)
-    while the INTERIOR pairs of iteration k run; the two boundary pairs run
-    after the receive completes (`uot_iterate_part`), so the exchange overlaps
-    compute (DESIGN.md "Multi-GPU").
+    Fixed marginals: iterations have no data-path exchange.  Chain prox with world > 1:
+    every iteration k sends the shard's first/last pair duals a^k to the neighbours (NCCL
+    P2P over NVLink) while the INTERIOR pairs of iteration k run; the two boundary pairs run
+    after the receive completes (`uot_iterate_part`), so the exchange overlaps compute.
+
+    Stopping (L13) with world > 1 is GLOBAL: the residuals and ||f|| of every shard are
+    summed before the test, so all ranks stop at the same checked iteration.  The run arms
+    the C-ABI's external stop once, and at every checked iteration packs this shard's sums
+    (uot_stop_pack), all-reduces them (8 doubles, on the stream) and applies the test
+    (uot_stop_apply) -- no host synchronisation inside the run.  run() returns the report
+    summed over ranks (all_reduce_report).  World 1: the device-side test of uot_iterate.
     """
 
     def __init__(self, prob, rank: int = 0, world: int = 1, group=None, overlap: bool = True):
@@ -99,23 +139,44 @@ class ShardedChain:
         self.exchanging = prob.prox and world > 1
         if self.exchanging and (prob.a_prev_halo is None or prob.a_next_halo is None):
             raise ValueError("chain-prox shards need Problem(..., halos=True)")
+        self._sums = None
+
+    def _global_check(self, tol):
+        p = self.prob
+        if self._sums is None:
+            self._sums = torch.zeros(8, dtype=torch.float64, device=p.frames.device)
+        p.stop_pack(self._sums)
+        all_reduce_sum_(self._sums, self.group)
+        p.stop_apply(self._sums, tol)
 
     def run(self, n_iters: int, check_every: int = 10, tol: float = 0.0) -> dict:
         from ._lib import UOT_PART_ALL, UOT_PART_BOUNDARY, UOT_PART_INTERIOR
         p = self.prob
-        if not self.exchanging:
+        if self.world == 1:
             p.iterate(n_iters, check_every=check_every, tol=tol)
             return p.report()
-        for k in range(n_iters):
-            red = (check_every > 0 and (k + 1) % check_every == 0) or k == n_iters - 1
-            s = p.slot
-            works = exchange_boundary_duals(p.a[s][:, 0], p.a[s][:, -1], p.a_prev_halo, p.a_next_halo,
-                                            self.rank, self.world, self.group, wait=not self.overlap)
-            if self.overlap:
-                p.iterate_part(UOT_PART_INTERIOR, red)
-                for w in works:
-                    w.wait()
-                p.iterate_part(UOT_PART_BOUNDARY, red)
-            else:
-                p.iterate_part(UOT_PART_ALL, red)
-        return p.report()
+        p.stop_external()
+        ce = check_every if check_every > 0 else max(n_iters, 1)
+        if not self.exchanging:
+            k = 0
+            while k < n_iters:
+                d = min(ce - k % ce, n_iters - k)
+                p.iterate(d, check_every=d, tol=0.0)          # reductions on the chunk's last iteration
+                k += d
+                self._global_check(tol)
+        else:
+            for k in range(n_iters):
+                red = (k + 1) % ce == 0 or k == n_iters - 1
+                s = p.slot
+                works = exchange_boundary_duals(p.a[s][:, 0], p.a[s][:, -1], p.a_prev_halo, p.a_next_halo,
+                                                self.rank, self.world, self.group, wait=not self.overlap)
+                if self.overlap:
+                    p.iterate_part(UOT_PART_INTERIOR, red)
+                    for w in works:
+                        w.wait()
+                    p.iterate_part(UOT_PART_BOUNDARY, red)
+                else:
+                    p.iterate_part(UOT_PART_ALL, red)
+                if red:
+                    self._global_check(tol)
+        return all_reduce_report(p.report(), p.frames.device, group=self.group)

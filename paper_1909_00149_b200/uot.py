@@ -153,6 +153,21 @@ class Problem:
         """One iteration on a part of the pairs (_lib.UOT_PART_INTERIOR / _BOUNDARY / _ALL)."""
         check(lib().uot_iterate_part(self._ctx, int(part), int(bool(reduce))), self._ctx)
 
+    def stop_external(self):
+        """Arm the cross-rank stop (uot_stop_external): chunks then run with tol = 0 and the
+        L13 test is applied to all-reduced sums by stop_apply."""
+        check(lib().uot_stop_external(self._ctx), self._ctx)
+
+    def stop_pack(self, sums8: torch.Tensor):
+        """sums8 (8 float64 on the device) <- this shard's sums of the last checked iteration."""
+        if not (sums8.is_cuda and sums8.dtype == torch.float64 and sums8.numel() >= 8 and sums8.is_contiguous()):
+            raise ValueError("sums8 must be a contiguous CUDA float64 tensor of >= 8 elements")
+        check(lib().uot_stop_pack(self._ctx, ctypes.c_void_p(sums8.data_ptr())), self._ctx)
+
+    def stop_apply(self, sums8: torch.Tensor, tol: float):
+        """Set the stop flag if the (all-reduced) sums8 pass the L13 test at tol."""
+        check(lib().uot_stop_apply(self._ctx, ctypes.c_void_p(sums8.data_ptr()), float(tol)), self._ctx)
+
     def report(self) -> dict:
         """Sync and return the reductions of the last reducing iteration."""
         rep = Report()

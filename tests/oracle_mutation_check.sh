@@ -15,10 +15,15 @@ muts=(
 's/if (s == 0 \&\& prm->fix_first) {/if (s == 1 \&\& prm->fix_first) {/'
 's/double v = 0.5 \* (x\[k\] + a\[k\] + z\[k\] + b\[k\]);/double v = x[k] + a[k];/'
 's/xn\[k\] = (y\[k\] + prm->rho \* (s\[k\] - a\[k\])) \/ (1.0 + prm->rho);/xn[k] = (y[k] + prm->rho * (s[k] + a[k])) \/ (1.0 + prm->rho);/'
+'s/s2 += Knew\[o + k\] \* Knew\[o + k\];/s2 += Kold[o + k] * Kold[o + k];/'
+'s/s3 += dmx \* dmx + dmy \* dmy + dr \* dr;/s3 += dmx * dmx + dmy * dmy;/'
+'s/s3 += dx \* dx;/s3 += 0.0 * dx;/'
+'s/res\[2 \* it + 1\] = prm->rho \* sqrt(du);/res[2 * it + 1] = sqrt(du);/'
+'s/pr += (xn\[q\] - s\[q\]) \* (xn\[q\] - s\[q\])/pr += (x[q] - s[q]) * (x[q] - s[q])/'
 )
 for m in "${muts[@]}"; do
   rm -rf w; mkdir w; cp -r /root/repo/oracle /root/repo/tests /root/repo/paper_1909_00149_b200 w/; rm -f w/oracle/liboracle.so
   sed -i "$m" w/oracle/uot_oracle.c
   if cmp -s w/oracle/uot_oracle.c /root/repo/oracle/uot_oracle.c; then echo "MUTATION DID NOT APPLY: $m"; continue; fi
-  (cd w && timeout 600 python -m pytest tests/test_oracle_pins.py -x -q -p no:cacheprovider 2>&1 | tail -1) | sed "s|^|[$m] |" | cut -c1-220
+  (cd w && timeout 600 python -m pytest tests/test_oracle_pins.py tests/test_oracle_residual_pins.py -x -q -p no:cacheprovider 2>&1 | tail -1) | sed "s|^|[$m] |" | cut -c1-220
 done

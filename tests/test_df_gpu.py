@@ -55,8 +55,23 @@ def test_df_parity(monkeypatch, shape, check, inner, path):
     inn = dfp.inner_state()
     for k, ok in (("mx", "mx"), ("my", "my"), ("r", "r"), ("ain", "ain"), ("z", "z")):
         _cmp(k, inn[k].double().cpu().numpy(), st[ok], max(scale, np.abs(st[ok]).max()))
-    assert rep["primal_res"] == pytest.approx(res[-1, 0], rel=2e-3, abs=1e-6)
-    assert rep["dual_res"] == pytest.approx(res[-1, 1], rel=2e-3, abs=1e-6)
+    # residuals (oracle reductions pinned by P23) within the bound the measured
+    # iterate errors e = v_gpu - v_ref imply by the triangle inequality:
+    #   primal |[x-s; z-s]|: <= |e_x| + |e_z| + 2|e_s|;  dual rho|[dx; dz]|: <= rho(|e^n| + |e^(n-1)|)
+    # (e^(n-1) from a separate (n-1)-iteration run), + 1e-4 relative for fp32 partial sums
+    g_n = {k: getattr(dfp, k).double().cpu().numpy() for k in ("s", "x")}
+    g_n["z"] = inn["z"].double().cpu().numpy()
+    en = {k: float(np.linalg.norm((g_n[k] - st[k]).ravel())) for k in ("s", "x", "z")}
+    dfq = DFProblem(torch.from_numpy(y).cuda(), torch.from_numpy(s0).cuda(), mu, kappa, rho, tau1=t, tau2=t,
+                    inner_iters=inner)
+    dfq.solve(n - 1, eps=0.0, check_every=check)
+    stq, _ = oracle.df_admm(y, s0, mu, kappa, rho, t, t, n - 1, inner_iters=inner)
+    eq = float(np.linalg.norm((dfq.x.double().cpu().numpy() - stq["x"]).ravel())) + \
+        float(np.linalg.norm((dfq.inner_state()["z"].double().cpu().numpy() - stq["z"]).ravel()))
+    bp = en["x"] + en["z"] + 2 * en["s"] + 1e-4 * res[-1, 0] + 1e-9
+    bd = rho * (en["x"] + en["z"] + eq) + 1e-4 * res[-1, 1] + 1e-9
+    assert abs(rep["primal_res"] - res[-1, 0]) <= bp, (rep["primal_res"], res[-1, 0], bp)
+    assert abs(rep["dual_res"] - res[-1, 1]) <= bd, (rep["dual_res"], res[-1, 1], bd)
     assert rep["data_term"] == pytest.approx(0.5 * ((y - st["s"]) ** 2).sum(), rel=1e-4)
     assert rep["iterations"] == n
 
@@ -76,18 +91,18 @@ def test_df_device_stop_matches_oracle_residuals(monkeypatch, wave):
     kc = rep["iterations"]
     st, res = oracle.df_admm(y, s0, 0.8, 0.5, 1.0, t, t, kc)
     assert res[-1, 0] < 1.05e-3 and res[-1, 1] < 1.05e-3
-    np.testing.assert_allclose(dfp.s.double().cpu().numpy(), st["s"], atol=2e-3 * max(y.max(), 1))
+    np.testing.assert_allclose(dfp.s.double().cpu().numpy(), st["s"], atol=1e-3 * max(y.max(), 1))
     inn = dfp.inner_state()
     scale = max(np.abs(y).max(), np.abs(s0).max())
     for k in ("mx", "my", "ain", "z"):
-        _cmp(k, inn[k].double().cpu().numpy(), st[k], max(scale, np.abs(st[k]).max()), tol=2e-3)
+        _cmp(k, inn[k].double().cpu().numpy(), st[k], max(scale, np.abs(st[k]).max()), tol=1e-3)
     for k in ("x", "a", "b"):
-        _cmp(k, getattr(dfp, k).double().cpu().numpy(), st[k], scale, tol=2e-3)
+        _cmp(k, getattr(dfp, k).double().cpu().numpy(), st[k], scale, tol=1e-3)
     # warm continuation from the recovered state matches a fresh run of kc + 7 iterations
     dfp.solve(7, eps=0.0, check_every=7)
     st2, _ = oracle.df_admm(y, s0, 0.8, 0.5, 1.0, t, t, kc + 7)
     for k in ("x", "a", "b", "s"):
-        _cmp(k, getattr(dfp, k).double().cpu().numpy(), st2[k], scale, tol=2e-3)
+        _cmp(k, getattr(dfp, k).double().cpu().numpy(), st2[k], scale, tol=1e-3)
 
 
 @pytest.mark.parametrize("wave", ["0", "1"])

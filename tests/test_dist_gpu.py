@@ -1,0 +1,120 @@
+"""World-2 multi-process runs of the frame-range sharding
+on real `Problem` contexts: `dist.ShardedChain.run` end to end in two processes.
+
+The round-end GPU tier has ONE device, so both ranks run on cuda:0 with a gloo group; the
+boundary frame, the per-iteration boundary duals (chain prox) and the 8-double stop sums go
+through host copies (`dist._staged`) -- the same calls NCCL makes device to device across
+GPUs.  No kernel waits on another rank's kernel (the waits are host-side), so sharing one
+GPU cannot deadlock.  The sharded run must be BITWISE equal to the unsharded chain (P16):
+every pair and frame is computed by the same kernel arithmetic from the same inputs.
+"""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+T, NY, NX = 9, 40, 64
+ALPHA = 1.3
+# the same per-pass kernels on both sides: the persistent kernels are chosen per call (a
+# sharded run issues one call per check interval) and the wavefront / SMEM-tile choice
+# depends on the pair count, and different kernels need not round identically
+PATH_ENV = {"UOT_TPERSIST": "0", "UOT_PERSIST": "0", "UOT_WAVE": "1"}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _frames():
+    from paper_1909_00149_b200 import inputs
+    return inputs.gen_random(1, T, NY, NX, seed=77, kind="sparse")
+
+
+def _tau(prox):
+    from paper_1909_00149_b200.uot import default_steps
+    return default_steps(NX, NY, n_frames=T, rho=10.0 if prox else math.inf)[0]
+
+
+def _worker(rank, world, port, mode, n, check, tol, out):
+    import torch.distributed as dist
+    from paper_1909_00149_b200 import dist as udist
+    from paper_1909_00149_b200.uot import Problem
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.update(PATH_ENV)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    prox = mode == "prox"
+    full = _frames()
+    p0, p1 = udist.shard_range(T - 1, world, rank)
+    own_hi = p1 if rank < world - 1 else p1 + 1
+    fr = torch.zeros((1, p1 - p0 + 1, NY, NX), dtype=torch.float32, device="cuda")
+    fr[:, : own_hi - p0].copy_(torch.from_numpy(full[:, p0:own_hi]))
+    udist.exchange_boundary_frame(fr, rank, world)            # frame p1 from the next rank
+    tau = _tau(prox)
+    prob = Problem(fr, ALPHA, rho=10.0 if prox else math.inf, tau1=tau, tau2=tau, halos=prox)
+    rep = udist.ShardedChain(prob, rank, world).run(n, check_every=check, tol=tol)
+    st = {k: v.cpu().numpy() for k, v in prob.state().items()}
+    out[rank] = (p0, p1, st, rep)
+    dist.destroy_process_group()
+
+
+def _sharded(mode, n, check, tol, world=2):
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), mode, n, check, tol, out), nprocs=world, join=True)
+    return [out[r] for r in range(world)]
+
+
+def _unsharded(mode, n, check, tol):
+    from paper_1909_00149_b200.uot import Problem
+    prox = mode == "prox"
+    tau = _tau(prox)
+    old = {k: os.environ.get(k) for k in PATH_ENV}
+    os.environ.update(PATH_ENV)
+    try:
+        prob = _make(Problem, prox, tau)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    prob.iterate(n, check_every=check, tol=tol)
+    rep = prob.report()
+    return {k: v.cpu().numpy() for k, v in prob.state().items()}, rep
+
+
+def _make(Problem, prox, tau):
+    return Problem(torch.from_numpy(_frames()).cuda(), ALPHA, rho=10.0 if prox else math.inf, tau1=tau, tau2=tau)
+
+
+@pytest.mark.parametrize("mode,n,check,tol", [("fixed", 37, 10, 0.0), ("prox", 23, 5, 0.0),
+                                              ("fixed", 4000, 10, 1e-3)])
+def test_sharded_chain_world2_bitwise(mode, n, check, tol):
+    full_st, full_rep = _unsharded(mode, n, check, tol)
+    shards = _sharded(mode, n, check, tol)
+    if tol > 0:
+        assert full_rep["converged"] and full_rep["iterations"] < n
+    for p0, p1, st, rep in shards:
+        # every rank reports the global sums and the same (global) stop iteration
+        assert rep["iterations"] == full_rep["iterations"]
+        assert rep["converged"] == full_rep["converged"]
+        for key in ("objective", "transport", "growth", "prox_term", "upper_bound", "primal_res", "dual_res",
+                    "f_norm"):
+            assert rep[key] == pytest.approx(full_rep[key], rel=1e-12, abs=1e-300), key
+        for key in ("mx", "my", "r", "a"):
+            assert np.array_equal(st[key][:, : p1 - p0], full_st[key][:, p0:p1]), key
+        if mode == "prox":
+            assert np.array_equal(st["x"], full_st["x"][:, p0:p1 + 1])
