@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: run the N>1 code path with ranks sharing the visible GPUs and host-staged "
+                         "exchanges (functional check on a 1-GPU box; not a performance number)")
     return ap.parse_args()
 
 
@@ -251,7 +254,7 @@ def relaunch_distributed(args):
     count of every communicator is visible in the log."""
     import socket
     import torch
-    if torch.cuda.device_count() < args.gpus:
+    if args.dist_backend == "nccl" and torch.cuda.device_count() < args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but only {torch.cuda.device_count()} CUDA devices are visible")
     sk = socket.socket()
     sk.bind(("127.0.0.1", 0))
@@ -289,9 +292,13 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 and args.dist_backend == "gloo":
+        dist.init_process_group("gloo")
+    elif world > 1:
         # communicator-init lines (rank counts) on stderr, also when a launcher started us
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
@@ -329,7 +336,8 @@ def main():
     from paper_1909_00149_b200.uot import default_steps
     tau, _ = default_steps(cfg.nx, cfg.ny, n_frames=cfg.n_frames, rho=rho)   # global chain length (L12)
     prob = Problem(frames, cfg.alpha, rho=rho, tau1=tau, tau2=tau, stream=stream,
-                   halos=(prox and world > 1 and cfg.n_chains == 1))
+                   halos=(prox and world > 1 and cfg.n_chains == 1 and rank > 0,
+                          prox and world > 1 and cfg.n_chains == 1 and rank < world - 1))
     driver = udist.ShardedChain(prob, rank, world)
     G = prob.G
     N = cfg.nx * cfg.ny
@@ -347,14 +355,14 @@ def main():
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 

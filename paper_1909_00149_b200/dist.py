@@ -137,8 +137,9 @@ class ShardedChain:
     def __init__(self, prob, rank: int = 0, world: int = 1, group=None, overlap: bool = True):
         self.prob, self.rank, self.world, self.group, self.overlap = prob, rank, world, group, overlap
         self.exchanging = prob.prox and world > 1
-        if self.exchanging and (prob.a_prev_halo is None or prob.a_next_halo is None):
-            raise ValueError("chain-prox shards need Problem(..., halos=True)")
+        if self.exchanging and ((rank > 0) != (prob.a_prev_halo is not None) or
+                                (rank < world - 1) != (prob.a_next_halo is not None)):
+            raise ValueError("chain-prox shards need Problem(..., halos=(rank > 0, rank < world - 1))")
         self._sums = None
 
     def _global_check(self, tol):

@@ -57,7 +57,7 @@ class Problem:
 
     def __init__(self, frames: torch.Tensor, alpha: float, rho: float = math.inf,
                  tau1: float | None = None, tau2: float | None = None, *, stream: torch.cuda.Stream | None = None,
-                 force_steps: bool = False, reset: bool = True, halos: bool = False,
+                 force_steps: bool = False, reset: bool = True, halos: bool | tuple = False,
                  p_norm: int = 1, fix_first: bool = False):
         if frames.dim() != 4:
             raise ValueError("frames must be [B][T][ny][nx]")
@@ -83,8 +83,11 @@ class Problem:
         self.a = [e(plane), e(plane)]
         self.x = [e(self.frames.shape), e(self.frames.shape)] if self.prox else [None, None]
         # chain-prox shard halos (L19): duals of the pairs just outside this shard, [B][ny][nx]
-        self.a_prev_halo = torch.zeros((B, ny, nx), dtype=torch.float32, device=dev) if halos else None
-        self.a_next_halo = torch.zeros((B, ny, nx), dtype=torch.float32, device=dev) if halos else None
+        # halos = (has_prev, has_next) or a bool for both: a shard with no neighbour on a side
+        # passes no halo there (the chain ends; its end frame is reduced by this shard)
+        hp, hn = (halos, halos) if isinstance(halos, bool) else (bool(halos[0]), bool(halos[1]))
+        self.a_prev_halo = torch.zeros((B, ny, nx), dtype=torch.float32, device=dev) if hp else None
+        self.a_next_halo = torch.zeros((B, ny, nx), dtype=torch.float32, device=dev) if hn else None
         flags = (_lib.UOT_FORCE_STEPS if force_steps else 0) | (_lib.UOT_RESIDUAL_L2 if p_norm == 2 else 0) | \
             (_lib.UOT_FIX_FIRST_FRAME if fix_first else 0)
         if p_norm not in (1, 2):

@@ -62,7 +62,8 @@ def _worker(rank, world, port, mode, n, check, tol, out):
     fr[:, : own_hi - p0].copy_(torch.from_numpy(full[:, p0:own_hi]))
     udist.exchange_boundary_frame(fr, rank, world)            # frame p1 from the next rank
     tau = _tau(prox)
-    prob = Problem(fr, ALPHA, rho=10.0 if prox else math.inf, tau1=tau, tau2=tau, halos=prox)
+    prob = Problem(fr, ALPHA, rho=10.0 if prox else math.inf, tau1=tau, tau2=tau,
+                   halos=(prox and rank > 0, prox and rank < world - 1))
     rep = udist.ShardedChain(prob, rank, world).run(n, check_every=check, tol=tol)
     st = {k: v.cpu().numpy() for k, v in prob.state().items()}
     out[rank] = (p0, p1, st, rep)

@@ -94,8 +94,8 @@ def _emulated_shards(fr, alpha, rho, tau, n, cut):
     """Chain frames [0..T-1] split into shards [0..cut] and [cut..T-1] (shared frame `cut`);
     per iteration the boundary duals are exchanged by device copies (what NCCL does across GPUs)."""
     t = torch.from_numpy(fr).cuda()
-    A = Problem(t[:, :cut + 1].contiguous(), alpha, rho=rho, tau1=tau, tau2=tau, halos=True)
-    Bp = Problem(t[:, cut:].contiguous(), alpha, rho=rho, tau1=tau, tau2=tau, halos=True)
+    A = Problem(t[:, :cut + 1].contiguous(), alpha, rho=rho, tau1=tau, tau2=tau, halos=(False, True))
+    Bp = Problem(t[:, cut:].contiguous(), alpha, rho=rho, tau1=tau, tau2=tau, halos=(True, False))
     for _ in range(n):
         sa, sb = A.slot, Bp.slot
         Bp.a_prev_halo.copy_(A.a[sa][:, -1])
@@ -120,6 +120,10 @@ def test_sharded_chain_bitwise(T, cut):
         assert torch.equal(fs[k][:, cut:], sb[k]), k
     assert torch.equal(fs["x"][:, :cut + 1], sa["x"])
     assert torch.equal(fs["x"][:, cut:], sb["x"])
+    # the shared frame is reduced once (by the shard that owns it): shard objectives add up
+    of, oa, ob = full.objective(), A.objective(), Bp.objective()
+    for key in ("objective", "prox_term", "transport", "upper_bound"):
+        assert oa[key] + ob[key] == pytest.approx(of[key], rel=1e-12), key
     ref, _ = oracle.iterate(fr, alpha, rho, tau, tau, n)
     _cmp(fr, full, ref)
 
@@ -199,8 +203,8 @@ def test_sharded_chain_driver_overlap_emulated():
     t = torch.from_numpy(fr).cuda()
     full = Problem(t, 1.3, rho=5.0, tau1=tau, tau2=tau)
     full.iterate(n)
-    A = Problem(t[:, :cut + 1].contiguous(), 1.3, rho=5.0, tau1=tau, tau2=tau, halos=True)
-    B = Problem(t[:, cut:].contiguous(), 1.3, rho=5.0, tau1=tau, tau2=tau, halos=True)
+    A = Problem(t[:, :cut + 1].contiguous(), 1.3, rho=5.0, tau1=tau, tau2=tau, halos=(False, True))
+    B = Problem(t[:, cut:].contiguous(), 1.3, rho=5.0, tau1=tau, tau2=tau, halos=(True, False))
     for _ in range(n):
         sa, sb = A.slot, B.slot
         A.iterate_part(_lib.UOT_PART_INTERIOR, False)
