@@ -355,7 +355,16 @@ typedef struct {
     double   tau1, tau2;           /* inner Alg.1 steps; 0 = Theorem-1 default (pair prox)       */
     int32_t  inner_iters;          /* Alg.1 iterations per ADMM iteration, >= 1      */
     uint32_t flags;                /* UOT_RESIDUAL_L2, UOT_FORCE_STEPS, UOT_RPCA_SIGNED          */
+    /* Frame-range shard of a video of n_frames_total frames (line 11's
+     * T-1 pair proxes, "simultaneously solved", split by frame range).  The
+     * context holds frames [frame0, frame0 + n_frames) of the video and their n_frames - 1
+     * pairs; with UOT_RPCA_HAS_NEXT its last frame is the next shard's first (a halo frame:
+     * updated here bit-identically, reduced by its owner).  0 / 0 = the whole video.        */
+    int32_t  frame0, n_frames_total;
+    uint32_t shard_flags;          /* UOT_RPCA_HAS_PREV | UOT_RPCA_HAS_NEXT                      */
 } uot_rpca_params;
+#define UOT_RPCA_HAS_PREV 1u
+#define UOT_RPCA_HAS_NEXT 2u
 
 typedef struct {                   /* caller-owned device buffers, fp32, 16-B aligned           */
     const float* y;                /* [T][ny][nx] observations                                   */
@@ -371,6 +380,12 @@ typedef struct {                   /* caller-owned device buffers, fp32, 16-B al
     float* r;                      /* [Q][ny][nx] inner residual                                 */
     float* ain[2];                 /* [Q][ny][nx] inner dual, ping-pong                          */
     double* scratch;               /* uot_rpca_scratch_doubles(&params) doubles                  */
+    /* sharded contexts only (else NULL):                                                        */
+    float* mgather;                /* [n_frames_total][ny][nx]: M = L + D of EVERY frame (line 10); uot_rpca_iterate_pre
+                                    * writes this shard's owned frames and zeros the others, the caller sums the
+                                    * buffers of all shards (all-reduce: exactly one nonzero term per element)  */
+    float* halo_prev;              /* [chains][2][ny][nx] (w, c) of the pair left of frame0 (HAS_PREV), received */
+    float* halo_next;              /* [chains][2][ny][nx] (z, b) of the pair right of the last frame (HAS_NEXT)   */
 } uot_rpca_buffers;
 
 typedef struct {
@@ -398,6 +413,27 @@ int uot_rpca_solve(uot_rpca_ctx* ctx, int32_t max_iters, double eps, int32_t che
 int uot_rpca_set_timing(uot_rpca_ctx* ctx, int enable);
 int uot_rpca_get_timing(uot_rpca_ctx* ctx, double* ms_by_kernel /*[6]: pre, gram, eig, apply, prox, post*/,
                         int64_t* n_iters);
+/* Sharded ADMM iteration, split where the shards exchange (DESIGN.md 6a "Sharded"); the caller
+ * owns the collectives (NCCL over NVLink, same stream order):
+ *   uot_rpca_stop_external(ctx)          arm the device stop, local test disabled
+ *   loop: uot_rpca_iterate_pre(ctx, red) lines 5-9, 12, line-11 centres; mgather <- own M
+ *         (caller) all-reduce(sum) mgather over the shards
+ *         uot_rpca_iterate_post(ctx, red) lines 10 (Gram of all frames, eigen, T for this
+ *                                       shard's frames), 11, 13-15; residual partial sums
+ *         (caller) send (z, b) of the first pair to the previous shard's halo_next and
+ *                  (w, c) of the last pair to the next shard's halo_prev
+ *         if red: uot_rpca_stop_pack(ctx, sums8) -> (caller) all-reduce(sum) ->
+ *                 uot_rpca_stop_apply(ctx, sums8, eps)
+ *   uot_rpca_get_report(ctx, out)        sync; this shard's sums (nuclear norm is global);
+ *                                        iteration count rewound to a device stop
+ * sums8 = [primal^2, dual^2/rho^2, data, l1, transport, growth, nonfinite, 0] (device doubles).
+ * An unsharded context may use the same calls (mgather then unused). */
+int uot_rpca_iterate_pre(uot_rpca_ctx* ctx, int32_t reduce);
+int uot_rpca_iterate_post(uot_rpca_ctx* ctx, int32_t reduce);
+int uot_rpca_stop_external(uot_rpca_ctx* ctx);
+int uot_rpca_stop_pack(uot_rpca_ctx* ctx, double* sums8);
+int uot_rpca_stop_apply(uot_rpca_ctx* ctx, const double* sums8, double eps);
+int uot_rpca_get_report(uot_rpca_ctx* ctx, uot_rpca_report* out);
 int uot_rpca_state_slot(const uot_rpca_ctx* ctx);   /* ping-pong slot of zw/mx/my/ain holding the iterate */
 int64_t uot_rpca_launch_count(const uot_rpca_ctx* ctx);
 void uot_rpca_destroy(uot_rpca_ctx* ctx);

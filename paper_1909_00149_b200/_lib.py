@@ -33,7 +33,8 @@ EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset
             "uot_df_get_timing", "uot_df_launch_count", "uot_df_destroy", "uot_df_last_error",
             "uot_rpca_scratch_doubles", "uot_rpca_create", "uot_rpca_reset", "uot_rpca_solve",
             "uot_rpca_set_timing", "uot_rpca_get_timing", "uot_rpca_state_slot", "uot_rpca_launch_count",
-            "uot_rpca_destroy", "uot_rpca_last_error")
+            "uot_rpca_destroy", "uot_rpca_last_error", "uot_rpca_iterate_pre", "uot_rpca_iterate_post",
+            "uot_rpca_stop_external", "uot_rpca_stop_pack", "uot_rpca_stop_apply", "uot_rpca_get_report")
 UOT_N_PATHS = 10
 UOT_RPCA_MAX_T = 128
 UOT_RPCA_SIGNED = 8
@@ -90,13 +91,18 @@ class RpcaParams(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("n_frames", ctypes.c_int32),
                 ("lam", ctypes.c_double), ("gamma", ctypes.c_double), ("kappa", ctypes.c_double),
                 ("mu", ctypes.c_double), ("rho", ctypes.c_double), ("tau1", ctypes.c_double),
-                ("tau2", ctypes.c_double), ("inner_iters", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+                ("tau2", ctypes.c_double), ("inner_iters", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("frame0", ctypes.c_int32), ("n_frames_total", ctypes.c_int32), ("shard_flags", ctypes.c_uint32)]
+
+
+UOT_RPCA_HAS_PREV, UOT_RPCA_HAS_NEXT = 1, 2
 
 
 class RpcaBuffers(ctypes.Structure):
     _fields_ = [("y", _fp), ("phi", _fp), ("S", _fp), ("L", _fp), ("X", _fp), ("Tm", _fp), ("A", _fp), ("D", _fp),
                 ("Sm", _fp), ("pc", _fp), ("zw", _fp * 2), ("bc", _fp), ("zprev", _fp), ("mx", _fp * 2), ("my", _fp * 2),
-                ("r", _fp), ("ain", _fp * 2), ("scratch", _fp)]
+                ("r", _fp), ("ain", _fp * 2), ("scratch", _fp), ("mgather", _fp), ("halo_prev", _fp),
+                ("halo_next", _fp)]
 
 
 class RpcaReport(ctypes.Structure):
@@ -184,6 +190,13 @@ def lib():
     L.uot_rpca_get_timing.restype = ctypes.c_int
     L.uot_rpca_state_slot.argtypes = [ctypes.c_void_p]; L.uot_rpca_state_slot.restype = ctypes.c_int
     L.uot_rpca_launch_count.argtypes = [ctypes.c_void_p]; L.uot_rpca_launch_count.restype = ctypes.c_int64
+    for fn in ("uot_rpca_iterate_pre", "uot_rpca_iterate_post"):
+        getattr(L, fn).argtypes = [ctypes.c_void_p, ctypes.c_int32]; getattr(L, fn).restype = ctypes.c_int
+    L.uot_rpca_stop_external.argtypes = [ctypes.c_void_p]; L.uot_rpca_stop_external.restype = ctypes.c_int
+    L.uot_rpca_stop_pack.argtypes = [ctypes.c_void_p, ctypes.c_void_p]; L.uot_rpca_stop_pack.restype = ctypes.c_int
+    L.uot_rpca_stop_apply.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double]
+    L.uot_rpca_stop_apply.restype = ctypes.c_int
+    L.uot_rpca_get_report.argtypes = [ctypes.c_void_p, RR]; L.uot_rpca_get_report.restype = ctypes.c_int
     L.uot_rpca_destroy.argtypes = [ctypes.c_void_p]; L.uot_rpca_destroy.restype = None
     L.uot_rpca_last_error.argtypes = [ctypes.c_void_p]; L.uot_rpca_last_error.restype = ctypes.c_char_p
     _lib = L

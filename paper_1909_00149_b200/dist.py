@@ -181,3 +181,78 @@ class ShardedChain:
                 if red:
                     self._global_check(tol)
         return all_reduce_report(p.report(), p.frames.device, group=self.group)
+
+
+class ShardedRPCA:
+    """Drive one rank's frame-range shard of Algorithm 3 (RPCA+UOT-DF; a
+    `uot.RPCAProblem(..., shard=(frame0, T_total))`), SURVEY 8(f) NEXT(3).
+
+    Per ADMM iteration (stream-ordered, no host synchronisation; NCCL over NVLink):
+      uot_rpca_iterate_pre   lines 5-9, 12 and line 11's centres on this shard's frames
+                             (the halo frame too); M = L + D of its OWNED frames into mgather
+      all-reduce(mgather)    line 10 needs the Gram matrix of every frame: the shards' disjoint
+                             rows sum exactly (Tg x N floats)
+      uot_rpca_iterate_post  line 10 (Gram + eigen-decomposition of all Tg frames, redundant per
+                             rank; T = M W for this shard's frames), line 11 (T-1 independent pair
+                             proxes), lines 13-15
+      boundary exchange      (z, b) of the first pair -> previous rank, (w, c) of the last pair ->
+                             next rank: the only per-iteration coupling of line 11's pairs
+                             (lines 5-7 of the shared frame read both neighbours' pairs)
+      at checked iterations  8 partial sums all-reduced, L28 test on the global sums (every rank
+                             stops at the same iteration)
+    run() returns the report with the additive terms summed over ranks.
+    """
+
+    def __init__(self, prob, rank: int = 0, world: int = 1, group=None):
+        if (rank > 0) != prob.has_prev or (rank < world - 1) != prob.has_next:
+            raise ValueError("RPCAProblem shard does not match the rank's position")
+        self.prob, self.rank, self.world, self.group = prob, rank, world, group
+        self._sums = None
+
+    def _exchange(self):
+        p = self.prob
+        first, last = p.boundary_planes()
+        sends, recvs = [], []
+        chains = len(first)
+        if self.rank > 0:
+            for c in range(chains):
+                sends += [(first[c][0], self.rank - 1), (first[c][1], self.rank - 1)]
+                recvs += [(p.halo_prev[c, 0], self.rank - 1), (p.halo_prev[c, 1], self.rank - 1)]
+        if self.rank < self.world - 1:
+            for c in range(chains):
+                sends += [(last[c][0], self.rank + 1), (last[c][1], self.rank + 1)]
+                recvs += [(p.halo_next[c, 0], self.rank + 1), (p.halo_next[c, 1], self.rank + 1)]
+        for w in _p2p(sends, recvs, self.group):
+            w.wait()
+
+    def run(self, n_iters: int, check_every: int = 10, eps: float = 0.0) -> dict:
+        p = self.prob
+        if self.world == 1 and p.mgather is None:
+            return p.solve(n_iters, eps=eps, check_every=check_every)
+        if self._sums is None:
+            self._sums = torch.zeros(8, dtype=torch.float64, device=p.Y.device)
+        p.stop_external()
+        ce = max(int(check_every), 1)
+        for k in range(n_iters):
+            red = (k + 1) % ce == 0 or k == n_iters - 1
+            p.iterate_pre(red)
+            all_reduce_sum_(p.mgather, self.group)
+            p.iterate_post(red)
+            if self.world > 1:
+                self._exchange()
+            if red:
+                p.stop_pack(self._sums)
+                all_reduce_sum_(self._sums, self.group)
+                p.stop_apply(self._sums, eps)
+        rep = p.get_report()
+        if self.world > 1:
+            keys = ("data_term", "l1_term", "transport", "growth")
+            t = torch.tensor([rep[k] for k in keys] + [rep["primal_res"] ** 2, rep["dual_res"] ** 2],
+                             dtype=torch.float64, device=p.Y.device)
+            all_reduce_sum_(t, self.group)
+            for i, k in enumerate(keys):
+                rep[k] = float(t[i])
+            rep["primal_res"], rep["dual_res"] = float(t[4].sqrt()), float(t[5].sqrt())
+            rep["objective"] = rep["data_term"] + rep["l1_term"] + p._p.gamma * rep["nuclear"] + \
+                p._p.kappa * (rep["transport"] + rep["growth"])
+        return rep

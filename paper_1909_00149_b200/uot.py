@@ -378,7 +378,10 @@ class RPCAProblem:
     def __init__(self, Y: torch.Tensor, lam: float, gamma: float, kappa: float, mu: float, rho: float = 1.0,
                  phi: torch.Tensor | None = None, tau1: float | None = None, tau2: float | None = None,
                  inner_iters: int = 1, p_norm: int = 1, signed: bool = False, *,
-                 stream: torch.cuda.Stream | None = None, reset: bool = True):
+                 stream: torch.cuda.Stream | None = None, reset: bool = True, shard: tuple | None = None):
+        """shard = (frame0, T_total): Y holds frames [frame0, frame0 + T) of a T_total-frame
+        video (a frame-range shard; the last frame is the next shard's first when
+        frame0 + T < T_total); driven by dist.ShardedRPCA."""
         if Y.dim() != 3:
             raise ValueError("Y must be [T][ny][nx]")
         if not Y.is_cuda or Y.dtype != torch.float32:
@@ -404,8 +407,17 @@ class RPCAProblem:
         self.mx, self.my, self.ain = [e(Q, ny, nx), e(Q, ny, nx)], [e(Q, ny, nx), e(Q, ny, nx)], [e(Q, ny, nx), e(Q, ny, nx)]
         self.r = e(Q, ny, nx)
         flags = (_lib.UOT_RESIDUAL_L2 if p_norm == 2 else 0) | (_lib.UOT_RPCA_SIGNED if self.signed else 0)
+        f0, Tt = (0, T) if shard is None else (int(shard[0]), int(shard[1]))
+        self.frame0, self.T_total = f0, Tt
+        self.has_prev, self.has_next = f0 > 0, f0 + T < Tt
+        sflags = (_lib.UOT_RPCA_HAS_PREV if self.has_prev else 0) | (_lib.UOT_RPCA_HAS_NEXT if self.has_next else 0)
+        chains = 2 if self.signed else 1
+        self.mgather = e(Tt, ny, nx) if Tt > T else None
+        self.halo_prev = e(chains, 2, ny, nx) if self.has_prev else None     # (w, c) of pair frame0 - 1
+        self.halo_next = e(chains, 2, ny, nx) if self.has_next else None     # (z, b) of the pair after the last frame
         self._p = RpcaParams(nx, ny, T, float(lam), float(gamma), float(kappa), float(mu), float(rho),
-                             float(tau1 or 0.0), float(tau2 or 0.0), int(inner_iters), flags)
+                             float(tau1 or 0.0), float(tau2 or 0.0), int(inner_iters), flags, f0,
+                             Tt if Tt > T else 0, sflags)
         nsc = int(lib().uot_rpca_scratch_doubles(ctypes.byref(self._p)))
         if nsc == 0:
             raise ValueError(f"unsupported shape (2 <= T <= {_lib.UOT_RPCA_MAX_T})")
@@ -425,6 +437,9 @@ class RPCAProblem:
             bf.ain[k] = self.ain[k].data_ptr()
         bf.r = self.r.data_ptr()
         bf.scratch = self.scratch.data_ptr()
+        bf.mgather = self.mgather.data_ptr() if self.mgather is not None else None
+        bf.halo_prev = self.halo_prev.data_ptr() if self.halo_prev is not None else None
+        bf.halo_next = self.halo_next.data_ptr() if self.halo_next is not None else None
         self._bufs = bf
         ctx = ctypes.c_void_p()
         check(lib().uot_rpca_create(ctypes.byref(self._p), ctypes.byref(bf), ctypes.c_void_p(self.stream.cuda_stream),
@@ -453,6 +468,41 @@ class RPCAProblem:
         d["status"] = rc
         self.iterations = d["iterations"]
         return d
+
+    # ---- sharded iteration (include/uot.h "Sharded ADMM iteration"); see dist.ShardedRPCA
+    def iterate_pre(self, reduce: bool = False):
+        check(lib().uot_rpca_iterate_pre(self._ctx, int(bool(reduce))), self._ctx, rpca=True)
+
+    def iterate_post(self, reduce: bool = False):
+        check(lib().uot_rpca_iterate_post(self._ctx, int(bool(reduce))), self._ctx, rpca=True)
+        self.iterations += 1
+
+    def stop_external(self):
+        check(lib().uot_rpca_stop_external(self._ctx), self._ctx, rpca=True)
+
+    def stop_pack(self, sums8: torch.Tensor):
+        check(lib().uot_rpca_stop_pack(self._ctx, ctypes.c_void_p(sums8.data_ptr())), self._ctx, rpca=True)
+
+    def stop_apply(self, sums8: torch.Tensor, eps: float):
+        check(lib().uot_rpca_stop_apply(self._ctx, ctypes.c_void_p(sums8.data_ptr()), float(eps)), self._ctx, rpca=True)
+
+    def get_report(self) -> dict:
+        rep = RpcaReport()
+        check(lib().uot_rpca_get_report(self._ctx, ctypes.byref(rep)), self._ctx, rpca=True)
+        d = rep.as_dict()
+        self.iterations = d["iterations"]
+        return d
+
+    def boundary_planes(self):
+        """Planes this shard sends after an iteration: (z, b) of its first pair (to the previous
+        shard's halo_next) and (w, c) of its last pair (to the next shard's halo_prev), one
+        [2][ny][nx] pair per sign chain (views; z/w from the current ping-pong slot)."""
+        s = int(lib().uot_rpca_state_slot(self._ctx))
+        P = self.T - 1
+        chains = [0, P] if self.signed else [0]
+        first = [(self.zw[s][c0, 0], self.bc[c0, 0]) for c0 in chains]
+        last = [(self.zw[s][c0 + P - 1, 1], self.bc[c0 + P - 1, 1]) for c0 in chains]
+        return first, last
 
     def state(self) -> dict:
         """Current iterate: S, L, X, Tm, A, D [T][ny][nx]; Z, W, Bd, Cd [T-1][ny][nx] (z_t, w_{t+1},

@@ -29,14 +29,21 @@ def test_exports_every_declared_symbol(L):
         assert hasattr(L, name), name
 
 
-def test_struct_sizes_match_header():
-    # uot_params: 4 int32 + 4 double + uint32 (+pad); uot_buffers: 15 pointers (r_alt last)
-    assert ctypes.sizeof(_lib.Params) == 56
-    assert ctypes.sizeof(_lib.Buffers) == 15 * 8
-    # uot_rpca_params: 3 int32 (+pad) + 7 double + int32 + uint32; uot_rpca_buffers: 22 pointers
-    assert ctypes.sizeof(_lib.RpcaParams) == 16 + 7 * 8 + 8
-    assert ctypes.sizeof(_lib.RpcaBuffers) == 22 * 8
-    assert ctypes.sizeof(_lib.Report) == 9 * 8 + 8 + 4 + 4
+def test_struct_sizes_match_header(tmp_path):
+    """The ctypes mirrors have the sizes the C compiler gives the structs of include/uot.h."""
+    import subprocess
+    names = ["uot_params", "uot_buffers", "uot_report", "uot_df_params", "uot_df_buffers", "uot_df_report",
+             "uot_rpca_params", "uot_rpca_buffers", "uot_rpca_report"]
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include "uot.h"\nint main(void) {\n' +
+                   "".join(f'  printf("%zu\\n", sizeof({n}));\n' for n in names) + "  return 0;\n}\n")
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    sizes = [int(v) for v in subprocess.check_output([str(exe)], text=True).split()]
+    mirrors = [_lib.Params, _lib.Buffers, _lib.Report, _lib.DfParams, _lib.DfBuffers, _lib.DfReport,
+               _lib.RpcaParams, _lib.RpcaBuffers, _lib.RpcaReport]
+    for n, m, c in zip(names, mirrors, sizes):
+        assert ctypes.sizeof(m) == c, (n, ctypes.sizeof(m), c)
 
 
 @pytest.mark.parametrize("nx,ny,T,rho", [(64, 64, 2, math.inf), (3, 5, 2, 1.0), (6, 6, 4, 2.0), (1, 2, 2, math.inf)])

@@ -119,3 +119,66 @@ def test_sharded_chain_world2_bitwise(mode, n, check, tol):
             assert np.array_equal(st[key][:, : p1 - p0], full_st[key][:, p0:p1]), key
         if mode == "prox":
             assert np.array_equal(st["x"], full_st["x"][:, p0:p1 + 1])
+
+
+# ----------------------------------------------------------------------------- Algorithm 3 shards
+def _rpca_video():
+    g = np.random.default_rng(4)
+    Y = (g.random((9, 16, 16)) * 0.3).astype(np.float32)
+    Y[:, 4:8, 3:7] += 1.0
+    return Y
+
+
+RP = dict(lam=0.05, gamma=0.4, kappa=0.3, mu=1.5, rho=2.0)
+
+
+def _rpca_make(Y, shard=None):
+    from paper_1909_00149_b200.uot import RPCAProblem
+    import oracle
+    t = oracle.default_steps(Y.shape[2], Y.shape[1], prox=True)[0]
+    return RPCAProblem(torch.from_numpy(np.ascontiguousarray(Y)).cuda(), RP["lam"], RP["gamma"], RP["kappa"], RP["mu"],
+                       RP["rho"], tau1=t, tau2=t, shard=shard)
+
+
+def _rpca_worker(rank, world, port, n, check, eps, out):
+    import torch.distributed as dist
+    from paper_1909_00149_b200 import dist as udist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["UOT_PERSIST"] = "0"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    Y = _rpca_video()
+    T = Y.shape[0]
+    p0, p1 = udist.shard_range(T - 1, world, rank)                 # pairs [p0, p1) -> frames [p0, p1]
+    prob = _rpca_make(Y[p0:p1 + 1], shard=(p0, T))
+    rep = udist.ShardedRPCA(prob, rank, world).run(n, check_every=check, eps=eps)
+    out[rank] = (p0, p1, {k: v.cpu().numpy() for k, v in prob.state().items()}, rep)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,check,eps", [(20, 5, 0.0), (3000, 10, 1e-3)])
+def test_sharded_rpca_world2_bitwise(n, check, eps):
+    old = os.environ.get("UOT_PERSIST")
+    os.environ["UOT_PERSIST"] = "0"
+    try:
+        full = _rpca_make(_rpca_video())
+    finally:
+        if old is None:
+            os.environ.pop("UOT_PERSIST", None)
+        else:
+            os.environ["UOT_PERSIST"] = old
+    rf = full.solve(n, eps, check)
+    fs = {k: v.cpu().numpy() for k, v in full.state().items()}
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.spawn(_rpca_worker, args=(2, _free_port(), n, check, eps, out), nprocs=2, join=True)
+    for r in range(2):
+        p0, p1, st, rep = out[r]
+        assert rep["iterations"] == rf["iterations"] and rep["converged"] == rf["converged"]
+        for key in ("objective", "data_term", "l1_term", "nuclear", "transport", "growth", "primal_res", "dual_res"):
+            assert rep[key] == pytest.approx(rf[key], rel=1e-12, abs=1e-300), key
+        for key in ("S", "L", "X", "Tm", "A", "D"):
+            assert np.array_equal(st[key], fs[key][p0:p1 + 1]), key
+        for key in ("Z", "W", "Bd", "Cd", "mx", "my", "r", "ain"):
+            assert np.array_equal(st[key], fs[key][p0:p1]), key
