@@ -198,9 +198,9 @@ int uot_set_timing(uot_ctx* ctx, int enable);
 int uot_get_timing(uot_ctx* ctx, double* ms_total, int64_t* n_launches);
 /* As uot_get_timing, split by kernel: ms[k], n[k] for k = uot_kernel_path codes (0 k_iter,
  * 1 / 3 two- / four-iteration k_iter2 pass, 2 k_persist, 5 / 7 / 6 / 9 two- / three- / four- /
- * five-iteration k_wave pass, 8 k_tpersist) and 4 = the UOT-DF ADMM kernel; both arrays hold
- * UOT_N_PATHS entries.  Clears the record. */
-#define UOT_N_PATHS 10
+ * five-iteration k_wave pass, 8 k_tpersist, 10 k_single) and 4 = the UOT-DF ADMM kernel; both
+ * arrays hold UOT_N_PATHS entries.  Clears the record. */
+#define UOT_N_PATHS 11
 int uot_get_timing_paths(uot_ctx* ctx, double* ms, int64_t* n);
 
 /* Which ping-pong slot (0/1) of mx/my/a/x holds the current iterate. */
@@ -217,7 +217,9 @@ int uot_set_temporal(uot_ctx* ctx, int enable);
  * four-iteration passes, 5 / 6 / 9 = k_wave (register wavefront, 16-byte-aligned planes
  * with nx % 4 == 0) with two / four / five iterations per pass, 8 = k_tpersist (small grids: all
  * iterations of a call in one cooperative launch of SMEM-tile passes, when every run up to a
- * check has even length; otherwise the per-pass kernels).  Four-iteration contexts fill in
+ * check has even length; otherwise the per-pass kernels), 10 = k_single (one small pair with
+ * nx % 4 == 0 and nx/4 * ny <= 1024, fixed marginals: every iteration of a call in ONE CTA with the
+ * state in registers, reductions and stopping test in-kernel; UOT_SINGLE=0 disables it).  Four-iteration contexts fill in
  * with two-iteration passes / k_iter where a reduction falls inside four iterations. */
 int uot_kernel_path(const uot_ctx* ctx);
 

@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(256) k_pair_reduce(const ReduceArgs R) {
 
 }  // namespace uotk (k_pair_reduce)
 #include "uot_tpersist.inc"
+#include "uot_single.cuh"
 namespace uotk {
 
 // prox cold start (L8): x^0 = 0, or max(p, 0) with UOT_RESET_X_FROM_P
@@ -434,6 +435,8 @@ struct uot_ctx {
         CUtensorMap mx[2][2], my[2][2], a[2][2], r[2][2], f[2];   // [S = 4, 2][slot / r buffer]
     } tp;
     bool t4on;           // four-iteration passes enabled (UOT_T4)
+    bool single_on;      // one-CTA k_single for single small pairs (UOT_SINGLE)
+    int single_v;        // its pixels per thread: 8 (nx % 8 == 0) or 4 (UOT_SINGLE_V=4 forces 4)
     struct LogE { int64_t iter; int slot, rcur; };
     std::vector<LogE> log;           // launches since the stop was armed (device-stop correction)
     std::vector<LogE> persist_base;  // state at the start of each persistent launch since arming
@@ -727,6 +730,8 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     c->t2vec = (p.nx % 4 == 0) && al16(b.f) && al16(b.mx[0]) && al16(b.mx[1]) && al16(b.my[0]) && al16(b.my[1]) &&
                al16(b.a[0]) && al16(b.a[1]) && al16(b.r) && al16(b.r_alt);
     c->t4on = env_int("UOT_T4", 1) != 0;
+    c->single_on = env_int("UOT_SINGLE", 1) != 0;
+    c->single_v = env_int("UOT_SINGLE_V", 8);
     c->pdl = env_int("UOT_PDL", 1) != 0;
     if (c->t2ok) {
         const int wenv = env_int("UOT_T2_WIDE", -1);
@@ -1052,6 +1057,56 @@ static int launch_persist(uot_ctx* c, int n, int reduce_every, bool reduce_last,
     return UOT_OK;
 }
 
+// Small single-pair fixed-marginal grids (C1): all n iterations in ONE CTA (k_single,
+// uot_single.cuh), reductions and stopping test in-kernel.
+static bool use_single(const uot_ctx* c) {
+    return !c->prox && c->G == 1 && c->t2vec && c->single_on && (c->nx / 4) * c->ny <= kSingleThreads;
+}
+
+static int launch_single(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
+    SingleArgs A{};
+    A.nx = c->nx; A.ny = c->ny; A.f = c->b.f;
+    A.slot0 = c->slot;
+    A.mx_in = c->b.mx[c->slot]; A.my_in = c->b.my[c->slot]; A.a_in = c->b.a[c->slot];
+    for (int q = 0; q < 2; ++q) { A.mxb[q] = c->b.mx[q]; A.myb[q] = c->b.my[q]; A.ab[q] = c->b.a[q]; }
+    A.r = rbuf(c);
+    A.tau1 = c->tau1f; A.tau2 = c->tau2f; A.atau1 = (float)(c->p.alpha * c->tau1); A.r_scale = c->r_scale;
+    A.n_iters = n; A.red_every = reduce_every; A.red_last = reduce_last ? 1 : 0;
+    A.iter0 = c->iter;
+    A.pair_out = c->pair_it; A.glob = c->glob;
+    A.stop = const_cast<int*>(stop); A.tol = tol; A.tau1d = c->tau1;
+    void* args[1] = {(void*)&A};
+    cudaEvent_t e1 = nullptr;
+    if (c->timing) {
+        while (c->ev_used + 2 > c->ev.size()) {
+            cudaEvent_t ev;
+            if (cudaEventCreate(&ev) != cudaSuccess) return fail(c, UOT_E_CUDA, "cudaEventCreate");
+            c->ev.push_back(ev);
+        }
+        cudaEventRecord(c->ev[c->ev_used], c->s);
+        e1 = c->ev[c->ev_used + 1];
+        c->ev_used += 2;
+        c->ev_kind.push_back(10);
+    }
+    const bool v8 = c->nx % 8 == 0 && c->single_v != 4;
+    const void* fn = v8 ? (c->r_mode == 0 ? (const void*)k_single<0, 8>
+                                          : (c->r_mode == 1 ? (const void*)k_single<1, 8> : (const void*)k_single<2, 8>))
+                        : (c->r_mode == 0 ? (const void*)k_single<0, 4>
+                                          : (c->r_mode == 1 ? (const void*)k_single<1, 4> : (const void*)k_single<2, 4>));
+    const int V = v8 ? 8 : 4;
+    const int threads = ((c->nx / V) * c->ny + 31) / 32 * 32;
+    launch_k(c, fn, dim3(1), dim3(threads), 0, args);
+    if (e1) cudaEventRecord(e1, c->s);
+    int rc = check_launch(c, "k_single");
+    if (rc) return rc;
+    const int slot0 = c->slot;
+    c->slot = slot0 ^ (n & 1);            // iterate iter0 + done is written to slot slot0 ^ (done & 1)
+    if (c->stop_armed) c->persist_base.push_back({c->iter, slot0, c->rcur});   // (device-stop correction)
+    c->iter += n;
+    c->persist_launches++;
+    return UOT_OK;
+}
+
 // All n iterations in one cooperative launch of k_tpersist (uot_tpersist.inc): passes of 4 (2
 // before a checked iteration) on SMEM tiles, one grid barrier per pass.  Requires every run up
 // to a check to be even (use_tpersist).  The host replays the pass plan for the slot / r-buffer
@@ -1242,6 +1297,7 @@ static int pick_pass(const uot_ctx* c, int d) {
 }
 
 static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, const int* stop, double tol) {
+    if (n >= 1 && use_single(c)) return launch_single(c, n, reduce_every, reduce_last, stop, tol);
     if (use_tpersist(c, n, reduce_every)) return launch_tpersist(c, n, reduce_every, reduce_last, stop, tol);
     if (use_persist(c) && n >= 2) return launch_persist(c, n, reduce_every, reduce_last, stop, tol);
     const bool poll = stop != nullptr && n > 2 * kPollChunk && c->poll.init();
@@ -1559,6 +1615,7 @@ int uot_r_slot(const uot_ctx* c) { return c ? c->rcur : -1; }
 
 int uot_kernel_path(const uot_ctx* c) {
     if (!c) return -1;
+    if (use_single(c)) return 10;
     if (c->tp.ok && c->t2ok && c->t2on) return 8;
     if (use_persist(c)) return 2;
     if (!(c->t2ok && c->t2on)) return 0;

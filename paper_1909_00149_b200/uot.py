@@ -204,7 +204,7 @@ class Problem:
         check(lib().uot_get_timing(self._ctx, ctypes.byref(ms), ctypes.byref(n)), self._ctx)
         return ms.value, n.value
 
-    PATH_NAMES = ("k_iter", "k_iter2", "k_persist", "k_iter4", "k_df", "k_wave2", "k_wave4", "k_wave3", "k_tpersist", "k_wave5")
+    PATH_NAMES = ("k_iter", "k_iter2", "k_persist", "k_iter4", "k_df", "k_wave2", "k_wave4", "k_wave3", "k_tpersist", "k_wave5", "k_single")
 
     def get_timing_paths(self):
         """{kernel: (summed device ms, launches)} of the timed launches, split by kernel

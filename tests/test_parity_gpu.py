@@ -115,15 +115,16 @@ CASES = [
 # (UOT_PERSIST=0, UOT_TEMPORAL=0), the two-iterations-per-pass SMEM-tiled kernel k_iter2
 # (UOT_TEMPORAL=1; odd tails run the streaming kernel), or the SMEM-resident persistent
 # kernel (UOT_PERSIST=1, used when the grid fits)
-PATHS = [dict(UOT_VEC=1, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
-         dict(UOT_VEC=1, UOT_SEG_H=4, UOT_PERSIST=0, UOT_TEMPORAL=0),
-         dict(UOT_VEC=4, UOT_SEG_H=7, UOT_PERSIST=0, UOT_TEMPORAL=0),
-         dict(UOT_VEC=4, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
-         dict(UOT_VEC=2, UOT_SEG_H=5, UOT_PERSIST=0, UOT_TEMPORAL=0),
-         dict(UOT_PERSIST=0, UOT_TEMPORAL=1), dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=1),
-         dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=1, UOT_T4=0),
-         dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=0),
-         dict(UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=0, UOT_T4_TH=32, UOT_T2_WIDE=0), dict(UOT_PERSIST=1)]
+PATHS = [dict(UOT_SINGLE=0, UOT_VEC=1, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
+         dict(UOT_SINGLE=0, UOT_VEC=1, UOT_SEG_H=4, UOT_PERSIST=0, UOT_TEMPORAL=0),
+         dict(UOT_SINGLE=0, UOT_VEC=4, UOT_SEG_H=7, UOT_PERSIST=0, UOT_TEMPORAL=0),
+         dict(UOT_SINGLE=0, UOT_VEC=4, UOT_SEG_H=0, UOT_PERSIST=0, UOT_TEMPORAL=0),
+         dict(UOT_SINGLE=0, UOT_VEC=2, UOT_SEG_H=5, UOT_PERSIST=0, UOT_TEMPORAL=0),
+         dict(UOT_SINGLE=0, UOT_PERSIST=0, UOT_TEMPORAL=1), dict(UOT_SINGLE=0, UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=1),
+         dict(UOT_SINGLE=0, UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=1, UOT_T4=0),
+         dict(UOT_SINGLE=0, UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=0),
+         dict(UOT_SINGLE=0, UOT_PERSIST=0, UOT_TEMPORAL=1, UOT_WAVE=0, UOT_T4_TH=32, UOT_T2_WIDE=0), dict(UOT_SINGLE=0, UOT_PERSIST=1),
+         dict(UOT_SINGLE=1)]
 
 
 @pytest.mark.parametrize("env", PATHS, ids=lambda e: "-".join(f"{k[4:]}{v}" for k, v in e.items()))
@@ -502,7 +503,7 @@ def test_tpersist_matches_oracle(shape, n, check):
     fr = inputs.gen_random(B, T, ny, nx, seed=7 + nx, kind="sparse")
     tau = tau_for(ny, nx)
     _, st_s, rep_s = gpu_run(fr, 1.1, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 0}, check_every=check)
-    prob, st_t, rep_t = gpu_run(fr, 1.1, n, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 1, "UOT_TPERSIST": 1,
+    prob, st_t, rep_t = gpu_run(fr, 1.1, n, tau, env={"UOT_SINGLE": 0, "UOT_PERSIST": 0, "UOT_TEMPORAL": 1, "UOT_TPERSIST": 1,
                                                      "UOT_WAVE": 0}, check_every=check)
     assert prob.kernel_path == "k_tpersist"
     l0 = prob.launches
@@ -517,7 +518,7 @@ def test_tpersist_matches_oracle(shape, n, check):
     compare(fr, st_t, ref)
     assert rep_t["iterations"] == n
     assert rep_t["objective"] == pytest.approx(rrep[:, 0].sum() + 1.1 * rrep[:, 1].sum(), rel=OBJ_RTOL)
-    _, st_q, _ = gpu_run(fr, 1.1, n - 1, tau, env={"UOT_PERSIST": 0, "UOT_TEMPORAL": 1, "UOT_TPERSIST": 1,
+    _, st_q, _ = gpu_run(fr, 1.1, n - 1, tau, env={"UOT_SINGLE": 0, "UOT_PERSIST": 0, "UOT_TEMPORAL": 1, "UOT_TPERSIST": 1,
                                                   "UOT_WAVE": 0}, check_every=check)
     check_residuals(fr, st_t, ref, rep_t, rrep, tau, st_q, oracle.iterate(fr, 1.1, math.inf, tau, tau, n - 1)[0])
     assert rep_t["dual_res"] == pytest.approx(rep_s["dual_res"], rel=1e-3, abs=1e-6)
@@ -598,7 +599,7 @@ def test_wave_edge_shapes(shape, costs):
     fr = inputs.gen_random(B, T, ny, nx, seed=3 + ny + nx, kind="uniform")
     tau = tau_for(ny, nx)
     for n, check in ((30, 10), (23, 7)):
-        prob, st, rep = gpu_run(fr, 1.2, n, tau, env={"UOT_WAVE": 1, "UOT_TPERSIST": 0, "UOT_PERSIST": 0,
+        prob, st, rep = gpu_run(fr, 1.2, n, tau, env={"UOT_SINGLE": 0, "UOT_WAVE": 1, "UOT_TPERSIST": 0, "UOT_PERSIST": 0,
                                                      "UOT_WAVE_H": 16, "UOT_PASS_COST": costs}, check_every=check)
         assert prob.kernel_path.startswith("k_wave")
         ref, rrep = oracle.iterate(fr, 1.2, math.inf, tau, tau, n)

@@ -15,11 +15,12 @@ from paper_1909_00149_b200.uot import Problem
 pytestmark = pytest.mark.gpu
 # one-pass k_iter ("stream"), register-wavefront passes (four / two iterations per pass;
 # prox contexts run k_iter there), SMEM-tile passes, SMEM-resident persistent kernel
-PATHS = ["stream", "temporal", "temporal2", "tiles", "persist"]
+PATHS = ["stream", "temporal", "temporal2", "tiles", "persist", "single"]
 
 
 def _run(monkeypatch, path, fr, alpha, rho, tau, n, **kw):
     monkeypatch.setenv("UOT_PERSIST", "1" if path == "persist" else "0")
+    monkeypatch.setenv("UOT_SINGLE", "1" if path == "single" else "0")      # one-CTA k_single (G = 1)
     monkeypatch.setenv("UOT_TEMPORAL", "0" if path == "stream" else "1")
     monkeypatch.setenv("UOT_T4", "0" if path == "temporal2" else "1")
     monkeypatch.setenv("UOT_WAVE", "0" if path == "tiles" else "1")
