@@ -411,7 +411,7 @@ def main():
     alg_bytes_launch = bytes_iter
     dom = max(by_path, key=lambda k: by_path[k][0])
     dom_ms, dom_n = by_path[dom]
-    if prox or dom in ("k_persist", "k_tpersist"):
+    if prox or dom in ("k_persist", "k_tpersist", "k_single"):
         avg_launch_s = (dom_ms / max(iters_timed, 1)) / 1e3
     else:
         avg_launch_s = (dom_ms / max(dom_n, 1)) / 1e3
@@ -425,7 +425,9 @@ def main():
                    "k_iter4": "k_iter2<36, S=4> (four fused Alg.1 iterations per HBM pass, SMEM tiles)",
                    "k_iter2": "k_iter2<32, S=2> (two fused Alg.1 iterations per HBM pass, SMEM tiles)",
                    "k_persist": "k_persist (all iterations in one cooperative launch, SMEM-resident)",
-                   "k_tpersist": "k_tpersist (all passes of a call in one cooperative launch, SMEM tiles)"}.get(
+                   "k_tpersist": "k_tpersist (all passes of a call in one cooperative launch, SMEM tiles)",
+                   "k_single": "k_single (every iteration of a call in ONE CTA, state in registers; "
+                               "SMEM/latency-bound on one SM: the HBM fraction is not meaningful)"}.get(
         dom, f"k_iter<{'prox' if prox else 'fixed'}> (fused Alg.1 iteration)")
     shares = {k: {"ms": v[0], "launches": v[1], "share": v[0] / max(kern_ms, 1e-30)} for k, v in by_path.items()}
 
