@@ -15,6 +15,8 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: named ranges for nsys / ncu --nvtx (no-ops without a tool)
+
 #include "uot.h"
 #include "uot_kernels.cuh"
 #include "uot_persist.cuh"
@@ -852,6 +854,12 @@ static int launch_setup(uot_ctx* c) {
     return check_launch(c, "k_pair_reduce(setup)");
 }
 
+// NVTX range over one C-ABI call (host-side enqueue time; the device work it enqueues follows)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 static int resolve_pending(uot_ctx* c);
 
 int uot_reset(uot_ctx* c, uint32_t flags) {
@@ -1353,6 +1361,7 @@ static void fill_report(const uot_ctx* c, const double* h, uot_report* out) {
 }
 
 int uot_iterate(uot_ctx* c, int32_t n, int32_t check_every, double tol) {
+    NvtxRange nvtx_("uot_iterate");
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     if (n < 0 || check_every < 0) return fail(c, UOT_E_INVALID, "n_iters and check_every must be >= 0");
     if (c->ext_stop) {                   // one chunk of a cross-rank stopped run: no local test
@@ -1376,6 +1385,7 @@ int uot_iterate(uot_ctx* c, int32_t n, int32_t check_every, double tol) {
 }
 
 int uot_iterate_part(uot_ctx* c, int32_t part, int32_t reduce) {
+    NvtxRange nvtx_("uot_iterate_part");
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     if (part != UOT_PART_ALL && part != UOT_PART_INTERIOR && part != UOT_PART_BOUNDARY)
         return fail(c, UOT_E_INVALID, "bad part %d", part);
@@ -1443,6 +1453,7 @@ int uot_get_report(uot_ctx* c, uot_report* out) {
 }
 
 int uot_prox_step(uot_ctx* c, int32_t n, uot_report* out) {
+    NvtxRange nvtx_("uot_prox_step");
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     if (n < 0) return fail(c, UOT_E_INVALID, "n_iters < 0");
     const bool cap = capturing(c);
@@ -1476,6 +1487,7 @@ int uot_prox_step(uot_ctx* c, int32_t n, uot_report* out) {
 }
 
 int uot_solve(uot_ctx* c, int32_t max_iters, double tol, int32_t check_every, uot_report* out) {
+    NvtxRange nvtx_("uot_solve");
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     if (max_iters < 0 || check_every < 1) return fail(c, UOT_E_INVALID, "max_iters >= 0 and check_every >= 1 required");
     int prc = resolve_pending(c);
@@ -1499,6 +1511,7 @@ int uot_solve(uot_ctx* c, int32_t max_iters, double tol, int32_t check_every, uo
 }
 
 int uot_objective(uot_ctx* c, double* per_pair, uot_report* out) {
+    NvtxRange nvtx_("uot_objective");
     if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
     int prc = resolve_pending(c);
     if (prc) return prc;

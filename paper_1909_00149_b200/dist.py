@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import torch
 import torch.distributed as dist
+from torch.cuda import nvtx
 
 
 def shard_range(n_pairs: int, world: int, rank: int):
@@ -143,6 +144,11 @@ class ShardedChain:
         self._sums = None
 
     def _global_check(self, tol):
+        nvtx.range_push("global_stop_check")
+        self._global_check_(tol)
+        nvtx.range_pop()
+
+    def _global_check_(self, tol):
         p = self.prob
         if self._sums is None:
             self._sums = torch.zeros(8, dtype=torch.float64, device=p.frames.device)
@@ -169,8 +175,10 @@ class ShardedChain:
             for k in range(n_iters):
                 red = (k + 1) % ce == 0 or k == n_iters - 1
                 s = p.slot
+                nvtx.range_push("exchange_boundary_duals")
                 works = exchange_boundary_duals(p.a[s][:, 0], p.a[s][:, -1], p.a_prev_halo, p.a_next_halo,
                                                 self.rank, self.world, self.group, wait=not self.overlap)
+                nvtx.range_pop()
                 if self.overlap:
                     p.iterate_part(UOT_PART_INTERIOR, red)
                     for w in works:
@@ -236,10 +244,14 @@ class ShardedRPCA:
         for k in range(n_iters):
             red = (k + 1) % ce == 0 or k == n_iters - 1
             p.iterate_pre(red)
+            nvtx.range_push("allreduce_mgather")
             all_reduce_sum_(p.mgather, self.group)
+            nvtx.range_pop()
             p.iterate_post(red)
             if self.world > 1:
+                nvtx.range_push("exchange_boundary_pairs")
                 self._exchange()
+                nvtx.range_pop()
             if red:
                 p.stop_pack(self._sums)
                 all_reduce_sum_(self._sums, self.group)
