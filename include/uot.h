@@ -338,9 +338,14 @@ const char* uot_df_last_error(const uot_df_ctx* ctx);
  *   lines 14-15    : b_t <- b_t + z_t - s_t, c_{t+1} <- c_{t+1} + w_{t+1} - s_{t+1}
  * Residuals (L28): primal ||[X-S-L; L-T; z-s; w-s]||, dual rho||[dX; dT; dz; dw]||;
  * stop when both < eps, tested on the device every check_every iterations.
- * Limits: 2 <= T <= UOT_RPCA_MAX_T.
+ * Line 10 for T > 128 (the T x T Jacobi solver no longer fits one CTA): the partial SVD of P:861
+ * by subspace iteration -- Gram matrix in 128-frame blocks, one CholeskyQR2-orthonormalised step
+ * of width k = min(T, 64) (UOT_RPCA_K, <= 128) per ADMM iteration, warm-started from the previous Ritz vectors, the
+ * k x k Rayleigh quotient by the same Jacobi solver; exact when the k Ritz vectors span every
+ * eigenvector of G with lambda > (gamma/rho)^2 (UOT_RPCA_SVT=1 forces it at any T, UOT_RPCA_K
+ * sets k).  Limits: 2 <= T <= UOT_RPCA_MAX_T.
  * ======================================================================== */
-#define UOT_RPCA_MAX_T 128
+#define UOT_RPCA_MAX_T 512
 /* Signed split eq:RPCA_UOTDF_PN: S = S+ - S-, S+/- >= 0,
  * each with its own l1 term and its own chain of UOT terms (reading L30: the split of
  * Algorithm 3 extended with z+/-, w+/-, b+/-, c+/-; s+ and s- updated jointly, exactly, per
@@ -400,6 +405,9 @@ typedef struct {
     int64_t iterations;            /* ADMM iterations since uot_rpca_reset                      */
     int32_t converged, nonfinite;
     int32_t jacobi_sweeps;         /* sweeps of the last eigen-decomposition                     */
+    double svt_min_ritz;           /* T > 128 (partial SVD): smallest Ritz value of the k-wide subspace; the
+                                    * SVT is exact only while it is < (gamma/rho)^2 (else raise UOT_RPCA_K);
+                                    * -1 on the exact T <= 128 path                                */
 } uot_rpca_report;
 
 size_t uot_rpca_scratch_doubles(const uot_rpca_params* params);

@@ -36,7 +36,7 @@ EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset
             "uot_rpca_destroy", "uot_rpca_last_error", "uot_rpca_iterate_pre", "uot_rpca_iterate_post",
             "uot_rpca_stop_external", "uot_rpca_stop_pack", "uot_rpca_stop_apply", "uot_rpca_get_report")
 UOT_N_PATHS = 11
-UOT_RPCA_MAX_T = 128
+UOT_RPCA_MAX_T = 512
 UOT_RPCA_SIGNED = 8
 
 
@@ -109,7 +109,8 @@ class RpcaReport(ctypes.Structure):
     _fields_ = [("primal_res", ctypes.c_double), ("dual_res", ctypes.c_double), ("data_term", ctypes.c_double),
                 ("l1_term", ctypes.c_double), ("nuclear", ctypes.c_double), ("transport", ctypes.c_double),
                 ("growth", ctypes.c_double), ("objective", ctypes.c_double), ("iterations", ctypes.c_int64),
-                ("converged", ctypes.c_int32), ("nonfinite", ctypes.c_int32), ("jacobi_sweeps", ctypes.c_int32)]
+                ("converged", ctypes.c_int32), ("nonfinite", ctypes.c_int32), ("jacobi_sweeps", ctypes.c_int32),
+                ("svt_min_ritz", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -174,7 +174,7 @@ def test_rpca_invalid_arguments():
     with pytest.raises(UotError):
         RPCAProblem(Y, 1.0, 1.0, 0.0, 1.0)
     with pytest.raises(ValueError):
-        RPCAProblem(torch.zeros(200, 4, 4, device="cuda"), 1.0, 1.0, 1.0, 1.0)
+        RPCAProblem(torch.zeros(600, 4, 4, device="cuda"), 1.0, 1.0, 1.0, 1.0)
     with pytest.raises(ValueError):
         RPCAProblem(torch.zeros(1, 4, 4, device="cuda"), 1.0, 1.0, 1.0, 1.0)
 
