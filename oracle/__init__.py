@@ -7,7 +7,9 @@ neither imports the other.  The C source is ``oracle/uot_oracle.c``; this
 module only compiles it (gcc) and marshals numpy arrays.
 
 Parity status: every function here is pinned by ``tests/test_oracle_pins.py``
-(P1..P17, DESIGN.md section "Oracle pins"); none is "parity unpinned".
+(P1..P20, DF1..DF4) and ``tests/test_oracle_residual_pins.py`` (P21..P23, the
+stopping-rule reductions), DESIGN.md section "Oracle and its pins"; none is
+"parity unpinned".
 """
 from __future__ import annotations
 

@@ -23,8 +23,10 @@
  *     value is K(M, r, x) = div(M) - r - x_{t+1} + x_t  (P:276 with A = [I,-I]);
  *   - p = 1; rho = +inf means fixed marginals x == frames (L2).
  *
- * Parity of this file is pinned by tests/test_oracle_pins.py (P1..P17 of
- * DESIGN.md) -- closed forms, invariants, brute-force LPs, duality bounds.
+ * Parity of this file is pinned by tests/test_oracle_pins.py (P1..P20, DF1..DF4
+ * of DESIGN.md) -- closed forms, invariants, brute-force LPs, duality bounds --
+ * and its stopping-rule / report reductions by tests/test_oracle_residual_pins.py
+ * (P21..P23: recomputed from consecutive states).
  */
 #include <math.h>
 #include <stdlib.h>

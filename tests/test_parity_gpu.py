@@ -647,3 +647,33 @@ def test_random_pass_schedules_match_one_pass_kernel():
             assert rep_t["objective"] == pytest.approx(rep_s["objective"], rel=1e-5, abs=1e-7), (case, path, env)
         assert rep_t["primal_res"] == pytest.approx(rep_s["primal_res"], rel=1e-4, abs=1e-7), (case, path, env)
     print(f"random pass schedules: {case + 1} cases")
+
+
+def test_external_stop_contract():
+    """uot_stop_external / _pack / _apply (include/uot.h): apply without arming and a local
+    tol while armed are refused; an armed run honours a stop set from outside (the sums of
+    another 'rank' are added) at exactly the checked iteration, and uot_get_report rewinds to it."""
+    from paper_1909_00149_b200._lib import UotError
+    fr = inputs.gen_random(1, 3, 40, 64, seed=12, kind="uniform")
+    tau = tau_for(40, 64)
+    prob = Problem(torch.from_numpy(fr).cuda(), 0.8, tau1=tau, tau2=tau)
+    sums = torch.zeros(8, dtype=torch.float64, device="cuda")
+    with pytest.raises(UotError) as e:
+        prob.stop_apply(sums, 1e-3)
+    assert e.value.code == 2
+    prob.stop_external()
+    with pytest.raises(UotError) as e:
+        prob.iterate(10, check_every=10, tol=1e-3)
+    assert e.value.code == 2
+    # chunks of 10 with the global test; a huge tol makes the first check stop the run
+    for k in range(5):
+        prob.iterate(10, check_every=10, tol=0.0)
+        prob.stop_pack(sums)
+        sums.mul_(2.0)                                  # "all-reduce" over two identical shards
+        prob.stop_apply(sums, 1e30)
+    rep = prob.report()
+    assert rep["converged"] == 1 and rep["iterations"] == 10
+    ref, _ = oracle.iterate(fr, 0.8, math.inf, tau, tau, 10)
+    compare(fr, {k: v.double().cpu().numpy() for k, v in prob.state().items()}, ref)
+    rep2 = prob.solve(7, tol=0.0, check_every=7)           # disarmed: an ordinary solve continues
+    assert rep2["iterations"] == 17
