@@ -25,6 +25,9 @@ ALPHA = 1.3
 # sharded run issues one call per check interval) and the wavefront / SMEM-tile choice
 # depends on the pair count, and different kernels need not round identically
 PATH_ENV = {"UOT_TPERSIST": "0", "UOT_PERSIST": "0", "UOT_WAVE": "1"}
+# the persistent SMEM-tile passes (one cooperative launch per call): the same 4 + 4 + 2 pass plan
+# per check interval on both sides, so also bitwise
+PATH_ENV_TP = {"UOT_TPERSIST": "1", "UOT_PERSIST": "0", "UOT_WAVE": "0", "UOT_SINGLE": "0"}
 
 
 def _free_port():
@@ -45,13 +48,13 @@ def _tau(prox):
     return default_steps(NX, NY, n_frames=T, rho=10.0 if prox else math.inf)[0]
 
 
-def _worker(rank, world, port, mode, n, check, tol, out):
+def _worker(rank, world, port, mode, n, check, tol, out, env=None):
     import torch.distributed as dist
     from paper_1909_00149_b200 import dist as udist
     from paper_1909_00149_b200.uot import Problem
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    os.environ.update(PATH_ENV)
+    os.environ.update(env or PATH_ENV)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     prox = mode == "prox"
@@ -70,20 +73,21 @@ def _worker(rank, world, port, mode, n, check, tol, out):
     dist.destroy_process_group()
 
 
-def _sharded(mode, n, check, tol, world=2):
+def _sharded(mode, n, check, tol, world=2, env=None):
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), mode, n, check, tol, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), mode, n, check, tol, out, env), nprocs=world, join=True)
     return [out[r] for r in range(world)]
 
 
-def _unsharded(mode, n, check, tol):
+def _unsharded(mode, n, check, tol, env=None):
     from paper_1909_00149_b200.uot import Problem
     prox = mode == "prox"
     tau = _tau(prox)
-    old = {k: os.environ.get(k) for k in PATH_ENV}
-    os.environ.update(PATH_ENV)
+    env = env or PATH_ENV
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         prob = _make(Problem, prox, tau)
     finally:
@@ -101,11 +105,12 @@ def _make(Problem, prox, tau):
     return Problem(torch.from_numpy(_frames()).cuda(), ALPHA, rho=10.0 if prox else math.inf, tau1=tau, tau2=tau)
 
 
-@pytest.mark.parametrize("mode,n,check,tol", [("fixed", 37, 10, 0.0), ("prox", 23, 5, 0.0),
-                                              ("fixed", 4000, 10, 1e-3)])
-def test_sharded_chain_world2_bitwise(mode, n, check, tol):
-    full_st, full_rep = _unsharded(mode, n, check, tol)
-    shards = _sharded(mode, n, check, tol)
+@pytest.mark.parametrize("mode,n,check,tol,tp", [("fixed", 37, 10, 0.0, False), ("prox", 23, 5, 0.0, False),
+                                                 ("fixed", 4000, 10, 1e-3, False), ("fixed", 4000, 10, 1e-3, True)])
+def test_sharded_chain_world2_bitwise(mode, n, check, tol, tp):
+    env = PATH_ENV_TP if tp else PATH_ENV
+    full_st, full_rep = _unsharded(mode, n, check, tol, env)
+    shards = _sharded(mode, n, check, tol, env=env)
     if tol > 0:
         assert full_rep["converged"] and full_rep["iterations"] < n
     for p0, p1, st, rep in shards:
