@@ -453,6 +453,7 @@ def main():
                     "unit": "GB/s", "frac": a1 / peak, "px_it_per_s": sum_over_ranks(float(G) * N * n1) / (ms1 / 1e3),
                     "iterations": n1}
     traffic = None
+    ncu_dram_gbs = None
     prof_sum = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof_sum):
         try:
@@ -460,6 +461,10 @@ def main():
             d = json.load(open(prof_sum)).get(key)
             if d:
                 traffic = d.get("dram_bytes_per_launch")
+                m = d.get("metrics", {}).get("gpu__time_duration.sum", {})
+                ncu_ms = float(m.get("value", "nan")) * {"ms": 1.0, "us": 1e-3, "usecond": 1e-3, "ns": 1e-6}.get(
+                    m.get("unit", "ms"), 1.0)
+                ncu_dram_gbs = traffic / (ncu_ms / 1e3) / 1e9 if traffic and ncu_ms > 0 else None
         except Exception:
             traffic = None
 
@@ -553,6 +558,10 @@ def main():
             "config": config_dict(cfg, world, args.mode),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         # SURVEY 8(d)'s three numbers: px-it/s (value), algorithmic GB/s (achieved), and
+                         # ncu DRAM GB/s of the stored capture (cold, serialised launch at ncu's clock)
+                         "ncu_dram_gbs": ncu_dram_gbs,
+                         "frac_of_spec_8tbs": achieved / 8000.0,
                          "kernel": kernel_name,
                          "alg_bytes_per_launch": alg_bytes_launch, "avg_launch_ms": avg_launch_s * 1e3,
                          "launches_timed": dom_n, "kernels_in_step": shares, "peak_source": peak_src,
