@@ -248,6 +248,17 @@ class Problem:
         d["iterations"] = self.iterations
         return d
 
+    def load_state_dict(self, d: dict):
+        """Resume from a checkpoint (a state_dict of a problem with the same frames, shape and
+        parameters): copies the iterate into the current buffers.  Algorithm 1 recomputes K^k
+        from the state at the start of every call (L8), so continuing after a load equals
+        continuing the original run; the iteration count restarts at this problem's own."""
+        cur = self.state()
+        for k, v in cur.items():
+            if k not in d or tuple(d[k].shape) != tuple(v.shape):
+                raise ValueError(f"checkpoint lacks {k} or has the wrong shape")
+            v.copy_(d[k])
+
     @property
     def iterations(self) -> int:
         return int(self.report()["iterations"])

@@ -677,3 +677,32 @@ def test_external_stop_contract():
     compare(fr, {k: v.double().cpu().numpy() for k, v in prob.state().items()}, ref)
     rep2 = prob.solve(7, tol=0.0, check_every=7)           # disarmed: an ordinary solve continues
     assert rep2["iterations"] == 17
+
+
+@pytest.mark.parametrize("env", [dict(UOT_SINGLE=0), dict(UOT_SINGLE=0, UOT_TEMPORAL=0), dict(UOT_SINGLE=1)],
+                         ids=["default", "k_iter", "k_single"])
+def test_checkpoint_resume_bitwise(env):
+    """state_dict() after 23 iterations, load_state_dict() into a fresh problem, 17 more
+    iterations == 40 uninterrupted iterations, bitwise (K^k is recomputed from the state at
+    the start of every call, L8)."""
+    fr = inputs.gen_random(1, 2, 48, 64, seed=41, kind="sparse")
+    tau = tau_for(48, 64)
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
+    try:
+        a = Problem(torch.from_numpy(fr).cuda(), 1.2, tau1=tau, tau2=tau)
+        b = Problem(torch.from_numpy(fr).cuda(), 1.2, tau1=tau, tau2=tau)
+        c = Problem(torch.from_numpy(fr).cuda(), 1.2, tau1=tau, tau2=tau)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    a.step(40)
+    b.step(23)
+    ck = b.state_dict()
+    c.load_state_dict(ck)
+    c.step(17)
+    for k in ("mx", "my", "r", "a"):
+        assert torch.equal(a.state()[k], c.state()[k]), k
