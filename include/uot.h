@@ -10,7 +10,7 @@
  * entry point returns UOT_E_CUDA.
  *
  * Readings of the paper (sign of the constraint, rho convention, boundary,
- * stopping rule, ...) are DESIGN.md L1..L21 and are cited as "Lnn".
+ * stopping rule, ...) are DESIGN.md L1..L30 and are cited as "Lnn".
  *
  * ---------------------------------------------------------------------------
  * Problem.  A context holds B independent chains of T frames x_t (fp32,
@@ -90,7 +90,9 @@ typedef struct {
     float*  a[2];          /* [B][P][ny][nx] ping-pong dual                                      */
     float*  x[2];          /* [B][T][ny][nx] ping-pong frames (prox mode), NULL when rho = inf  */
     const float* a_prev_halo; /* [B][ny][nx] dual of the pair preceding frame 0 (chain prox shard), or NULL = 0 */
-    const float* a_next_halo; /* [B][ny][nx] dual of the pair following frame T-1, or NULL = 0          */
+    const float* a_next_halo; /* [B][ny][nx] dual of the pair following frame T-1, or NULL = 0; non-NULL
+                                 also means frame T-1 is the next shard's first frame: it is updated
+                                 here bit-identically but its terms are reduced by its owner       */
     double* scratch;       /* uot_scratch_doubles(&params) doubles (reduction partials, flags)  */
     float*  r_alt;         /* [B][P][ny][nx] second r buffer, or NULL.  Fixed marginals only:
                               enables the temporally blocked kernel (two iterations per HBM pass,
