@@ -544,7 +544,7 @@ def main():
             r1, s1 = cpu_oracle_rate_1thread(cfg, max(2.0, args.cpu_seconds / 3), rho)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
                    "one_thread": {"value": r1, "unit": UNIT, "cores": 1, "sample": s1},
-                   "host": lscpu_info()}
+                   "host": lscpu_info(), "gpu_over_cpu": value / rate if rate else None}
         except Exception as ex:   # the oracle is a reported baseline, not the product
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {ex}"}
 

@@ -39,7 +39,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *SOURCES]
+    extra = os.environ.get("UOT_NVCC_EXTRA", "").split()      # A/B experiments, e.g. -DUOT_PROX_MIN_BLOCKS=3
+    cmd = [NVCC, *FLAGS, *extra, "-o", tmp, *SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
