@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_single_gpu.py tests/test_dist_gpu.py -q -x -m gpu -k "stop or tpersist or external or sharded" > gpurun_out/quick.log 2>&1; echo EXIT $? >> gpurun_out/quick.log
+timeout 1200 python -m pytest tests/test_dist_gpu.py -q -x -m gpu -k "bench" > gpurun_out/quick.log 2>&1; echo EXIT $? >> gpurun_out/quick.log

@@ -187,3 +187,28 @@ def test_sharded_rpca_world2_bitwise(n, check, eps):
             assert np.array_equal(st[key], fs[key][p0:p1 + 1]), key
         for key in ("Z", "W", "Bd", "Cd", "mx", "my", "r", "ain"):
             assert np.array_equal(st[key], fs[key][p0:p1]), key
+
+
+@pytest.mark.parametrize("mode", ["fixed", "prox"])
+def test_bench_two_ranks_functional(mode):
+    """`bench.py --gpus 2` without a launcher re-launches itself as 2 ranks (torch.distributed.run);
+    with --dist-backend gloo both share this GPU (functional check of the N > 1 bench path: frame
+    shards, boundary-frame exchange, global stop, report all-reduce; not a timing).  The job's
+    objective equals the one-rank run's."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    base = [sys.executable, os.path.join(root, "bench.py"), "--config", "C3", "--iters", "20", "--steps", "1",
+            "--warmup", "3", "--no-cpu", "--no-e2e", "--mode", mode]
+    env = dict(os.environ, UOT_TPERSIST="0", UOT_PERSIST="0")
+    one = subprocess.run(base, capture_output=True, text=True, timeout=600, env=env)
+    two = subprocess.run(base + ["--gpus", "2", "--dist-backend", "gloo"], capture_output=True, text=True,
+                         timeout=600, env=env)
+    assert one.returncode == 0, one.stderr[-2000:]
+    assert two.returncode == 0, two.stderr[-2000:]
+    l1 = json.loads([ln for ln in one.stdout.splitlines() if ln.startswith("{")][-1])
+    l2 = json.loads([ln for ln in two.stdout.splitlines() if ln.startswith("{")][-1])
+    assert l2["n_gpus"] == 2 and l2["iterations_per_step"] == 20
+    # (the shards may select other pass kernels than the whole chain: fp32 rounding order only)
+    assert l2["objective"] == pytest.approx(l1["objective"], rel=1e-5)
