@@ -461,6 +461,30 @@ static int fail(uot_ctx* c, int code, const char* fmt, ...) {
 
 static const int kSMs = 148;
 
+// Segment height of the register wavefront: a warp marches H + 2S rows for H output rows, and
+// the G x strips x ceil(ny / H) warps run in waves of kSMs x (resident warps per SM).  Time is
+// modelled as (waves, rounded up) x (H + 2S): the smallest H that fits one fewer wave wins.
+// Measured (C3, 63 x 256^2, S = 5): H = 16 -> 2.55 waves, 2.88e11 px-it/s; H = 43 -> 0.96 wave,
+// 4.12e11; H = 37 -> 1.12 waves, 2.52e11.  C4 / C5 keep 512-row segments (the model's pick is
+// within 2% there); segments are capped at 512 rows (the measured C4 optimum of round 1).
+// UOT_WAVE_H overrides.
+static int wave_height(long long G, int strips, int ny, int S) {
+    const int resident = S >= 4 ? 8 : 10;                      // warps per SM (WaveCfg: registers)
+    const long long wave = (long long)kSMs * resident;
+    int bestH = 16;
+    double best = 1e300;
+    for (int n = (ny + 511) / 512; n <= (ny + 15) / 16; ++n) {  // n segments of H = ceil(ny / n) rows
+        const int H = (ny + n - 1) / n;
+        if (H < 16) break;
+        const long long units = G * strips * n;
+        const long long waves = (units + wave - 1) / wave;
+        const double t = (double)waves * (H + 2 * S) * (1.0 + 1e-9 * n);   // ties: fewer segments
+        if (t < best * (1.0 - 1e-12)) { best = t; bestH = H; }
+    }
+    return std::max(16, bestH);
+}
+
+
 static int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
     return v && *v ? atoi(v) : dflt;
@@ -690,12 +714,8 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     // Enough independent strips to fill the GPU: segment height 512 (halved down to 16 for
     // smaller problems, >= 2 waves of 8 warps per SM); below one wave at 16 rows the SMEM tiles.
     const long long strips = wave_strips(p.nx, 4);
-    int wave_h = env_int("UOT_WAVE_H", 0);
-    if (wave_h <= 0) {                  // fewer segments = less row halo (C4: 512 rows 6.29e11, 128: 6.18e11)
-        wave_h = 512;
-        while (wave_h > 16 && (long long)c->G * strips * ((p.ny + wave_h - 1) / wave_h) < 2LL * kSMs * 8) wave_h /= 2;
-    }
-    wave_h = std::max(16, wave_h);                              // >= 16: records within uot_scratch_doubles
+    const int wave_h_env = env_int("UOT_WAVE_H", 0);
+    int wave_h = wave_h_env > 0 ? std::max(16, wave_h_env) : 16;   // >= 16: records within uot_scratch_doubles
     const int wenv_wave = env_int("UOT_WAVE", -1);
     const bool wave = (p.nx % 4 == 0) &&
                       (wenv_wave >= 0 ? wenv_wave != 0
@@ -705,8 +725,8 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
         TVar& v = c->tv[k];
         v.wave = wave;
         if (wave) {
-            v.th = wave_h;
             v.tx = wave_strips(p.nx, kVarS[k]);
+            v.th = wave_h_env > 0 ? wave_h : wave_height(c->G, v.tx, p.ny, kVarS[k]);
         } else {
             v.tx = (p.nx + kTW - 1) / kTW;
         }
