@@ -468,8 +468,8 @@ static const int kSMs = 148;
 // 4.12e11; H = 37 -> 1.12 waves, 2.52e11.  C4 / C5 keep 512-row segments (the model's pick is
 // within 2% there); segments are capped at 512 rows (the measured C4 optimum of round 1).
 // UOT_WAVE_H overrides.
-static int wave_height(long long G, int strips, int ny, int S) {
-    const int resident = S >= 4 ? 8 : 10;                      // warps per SM (WaveCfg: registers)
+static int wave_height(long long G, int strips, int ny, int S, int resident = 0) {
+    if (resident <= 0) resident = S >= 4 ? 8 : 10;             // k_wave warps per SM (WaveCfg: registers)
     const long long wave = (long long)kSMs * resident;
     int bestH = 16;
     double best = 1e300;
