@@ -22,6 +22,7 @@
 #include "uot_persist.cuh"
 #include "uot_temporal.cuh"
 #include "uot_wave.cuh"
+#include "uot_wave_pk.cuh"
 
 using namespace uotk;
 
@@ -80,23 +81,24 @@ static bool tvar_fill(TVar& v, bool wide) {
     return ok;
 }
 
+// pk: the packed fp32x2 instruction stream (k_wave_pk, default) or the scalar k_wave (UOT_WAVE_PK=0)
 template <int S, int RM>
-static bool wvar_fill(TVar& v) {
+static bool wvar_fill(TVar& v, bool pk) {
     using namespace uotk;
     v.S = S; v.wave = true; v.tma = false; v.threads = kWaveWarps * 32; v.smem = kWaveSmem;
-    v.fn[0] = (const void*)k_wave<S, RM, false>;
-    v.fn[1] = (const void*)k_wave<S, RM, true>;
+    v.fn[0] = pk ? (const void*)k_wave_pk<S, RM, false> : (const void*)k_wave<S, RM, false>;
+    v.fn[1] = pk ? (const void*)k_wave_pk<S, RM, true> : (const void*)k_wave<S, RM, true>;
     bool ok = true;
     for (const void* f : v.fn)
         ok = ok && cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem) == cudaSuccess;
     return ok;
 }
 
-static bool wvar_select(TVar& v, int S, int rm) {
-    if (S == 5) return rm == 1 ? wvar_fill<5, 1>(v) : (rm == 2 ? wvar_fill<5, 2>(v) : wvar_fill<5, 0>(v));
-    if (S == 4) return rm == 1 ? wvar_fill<4, 1>(v) : (rm == 2 ? wvar_fill<4, 2>(v) : wvar_fill<4, 0>(v));
-    if (S == 3) return rm == 1 ? wvar_fill<3, 1>(v) : (rm == 2 ? wvar_fill<3, 2>(v) : wvar_fill<3, 0>(v));
-    return rm == 1 ? wvar_fill<2, 1>(v) : (rm == 2 ? wvar_fill<2, 2>(v) : wvar_fill<2, 0>(v));
+static bool wvar_select(TVar& v, int S, int rm, bool pk) {
+    if (S == 5) return rm == 1 ? wvar_fill<5, 1>(v, pk) : (rm == 2 ? wvar_fill<5, 2>(v, pk) : wvar_fill<5, 0>(v, pk));
+    if (S == 4) return rm == 1 ? wvar_fill<4, 1>(v, pk) : (rm == 2 ? wvar_fill<4, 2>(v, pk) : wvar_fill<4, 0>(v, pk));
+    if (S == 3) return rm == 1 ? wvar_fill<3, 1>(v, pk) : (rm == 2 ? wvar_fill<3, 2>(v, pk) : wvar_fill<3, 0>(v, pk));
+    return rm == 1 ? wvar_fill<2, 1>(v, pk) : (rm == 2 ? wvar_fill<2, 2>(v, pk) : wvar_fill<2, 0>(v, pk));
 }
 
 template <int TH, int S>
@@ -767,7 +769,7 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
                 v.tx = (p.nx + kTW - 1) / kTW;
                 v.ty = (p.ny + v.th - 1) / v.th;
             }
-            v.ok = v.wave ? wvar_select(v, S, c->r_mode) : tvar_select(v, S, v.th, wide, c->r_mode);
+            v.ok = v.wave ? wvar_select(v, S, c->r_mode, env_int("UOT_WAVE_PK", 1) != 0) : tvar_select(v, S, v.th, wide, c->r_mode);
             if (!v.ok) {
                 cudaGetLastError();
                 continue;

@@ -591,16 +591,19 @@ def test_graph_capture_replays_iterations(env):
 @pytest.mark.parametrize("shape", [(1, 2, 1, 8), (1, 2, 3, 4), (2, 3, 5, 116), (1, 2, 130, 228), (3, 2, 17, 240)],
                          ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("costs", ["1.155,1.15,1.137,1.35", "9,9,9,0.1"], ids=["default", "S5"])
-def test_wave_edge_shapes(shape, costs):
+@pytest.mark.parametrize("pk", [1, 0], ids=["packed", "scalar"])
+def test_wave_edge_shapes(shape, costs, pk):
     """The register wavefront on degenerate / ragged grids: one row, rows < S, one quad per
     row, widths just under / over one 112- or 120-column strip, with 16-row segments and
-    reductions every 10 and 7 iterations."""
+    reductions every 10 and 7 iterations; the packed fp32x2 kernel (k_wave_pk, default) and
+    the scalar k_wave."""
     B, T, ny, nx = shape
     fr = inputs.gen_random(B, T, ny, nx, seed=3 + ny + nx, kind="uniform")
     tau = tau_for(ny, nx)
     for n, check in ((30, 10), (23, 7)):
         prob, st, rep = gpu_run(fr, 1.2, n, tau, env={"UOT_SINGLE": 0, "UOT_WAVE": 1, "UOT_TPERSIST": 0, "UOT_PERSIST": 0,
-                                                     "UOT_WAVE_H": 16, "UOT_PASS_COST": costs}, check_every=check)
+                                                     "UOT_WAVE_H": 16, "UOT_PASS_COST": costs, "UOT_WAVE_PK": pk},
+                                check_every=check)
         assert prob.kernel_path.startswith("k_wave")
         ref, rrep = oracle.iterate(fr, 1.2, math.inf, tau, tau, n)
         compare(fr, st, ref)
