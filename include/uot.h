@@ -94,10 +94,11 @@ typedef struct {
                                  also means frame T-1 is the next shard's first frame: it is updated
                                  here bit-identically but its terms are reduced by its owner       */
     double* scratch;       /* uot_scratch_doubles(&params) doubles (reduction partials, flags)  */
-    float*  r_alt;         /* [B][P][ny][nx] second r buffer, or NULL.  Fixed marginals only:
-                              enables the temporally blocked kernel (two iterations per HBM pass,
-                              DESIGN.md "k_iter2"), which cannot update r in place.  Which of
-                              r / r_alt holds the current r: uot_r_slot().                     */
+    float*  r_alt;         /* [B][P][ny][nx] second r buffer, or NULL.  Enables the temporally
+                              blocked kernels (several iterations per HBM pass: k_wave / k_iter2
+                              with fixed marginals, k_wave_prox in chain prox without halos),
+                              which cannot update r in place.  Which of r / r_alt holds the
+                              current r: uot_r_slot().                                         */
 } uot_buffers;
 
 /* Reductions (fp64) summed over this context's pairs, DESIGN.md "Reductions". */
@@ -200,9 +201,9 @@ int uot_set_timing(uot_ctx* ctx, int enable);
 int uot_get_timing(uot_ctx* ctx, double* ms_total, int64_t* n_launches);
 /* As uot_get_timing, split by kernel: ms[k], n[k] for k = uot_kernel_path codes (0 k_iter,
  * 1 / 3 two- / four-iteration k_iter2 pass, 2 k_persist, 5 / 7 / 6 / 9 two- / three- / four- /
- * five-iteration k_wave pass, 8 k_tpersist, 10 k_single) and 4 = the UOT-DF ADMM kernel; both
- * arrays hold UOT_N_PATHS entries.  Clears the record. */
-#define UOT_N_PATHS 11
+ * five-iteration k_wave pass, 8 k_tpersist, 10 k_single, 11 chain-prox k_wave_prox pass) and 4 =
+ * the UOT-DF ADMM kernel; both arrays hold UOT_N_PATHS entries.  Clears the record. */
+#define UOT_N_PATHS 12
 int uot_get_timing_paths(uot_ctx* ctx, double* ms, int64_t* n);
 
 /* Which ping-pong slot (0/1) of mx/my/a/x holds the current iterate. */
@@ -221,7 +222,10 @@ int uot_set_temporal(uot_ctx* ctx, int enable);
  * iterations of a call in one cooperative launch of SMEM-tile passes, when every run up to a
  * check has even length; otherwise the per-pass kernels), 10 = k_single (one small pair with
  * nx % 4 == 0 and nx/4 * ny <= 1024, fixed marginals: every iteration of a call in ONE CTA with the
- * state in registers, reductions and stopping test in-kernel; UOT_SINGLE=0 disables it).  Four-iteration contexts fill in
+ * state in registers, reductions and stopping test in-kernel; UOT_SINGLE=0 disables it), 11 =
+ * k_wave_prox (chain prox, rho < inf, with buffers.r_alt, aligned planes, nx % 4 == 0 and no
+ * shard halos: four (two) iterations per pass, pairs in lockstep groups of clusters of CTAs;
+ * UOT_PROX_WAVE=0 disables it).  Four-iteration contexts fill in
  * with two-iteration passes / k_iter where a reduction falls inside four iterations. */
 int uot_kernel_path(const uot_ctx* ctx);
 

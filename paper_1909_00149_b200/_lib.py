@@ -35,7 +35,7 @@ EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset
             "uot_rpca_set_timing", "uot_rpca_get_timing", "uot_rpca_state_slot", "uot_rpca_launch_count",
             "uot_rpca_destroy", "uot_rpca_last_error", "uot_rpca_iterate_pre", "uot_rpca_iterate_post",
             "uot_rpca_stop_external", "uot_rpca_stop_pack", "uot_rpca_stop_apply", "uot_rpca_get_report")
-UOT_N_PATHS = 11
+UOT_N_PATHS = 12
 UOT_RPCA_MAX_T = 512
 UOT_RPCA_SIGNED = 8
 

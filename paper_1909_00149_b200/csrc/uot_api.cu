@@ -23,6 +23,7 @@
 #include "uot_temporal.cuh"
 #include "uot_wave.cuh"
 #include "uot_wave_pk.cuh"
+#include "uot_wave_prox.cuh"
 
 using namespace uotk;
 
@@ -439,6 +440,13 @@ struct uot_ctx {
         CUtensorMap mx[2][2], my[2][2], a[2][2], r[2][2], f[2];   // [S = 4, 2][slot / r buffer]
     } tp;
     bool t4on;           // four-iteration passes enabled (UOT_T4)
+    struct {             // chain prox: register wavefront with pair groups (k_wave_prox)
+        bool ok;
+        int S;               // iterations of the long pass (3); short pass: 2
+        int cl, groups;      // CTAs per cluster, pair groups per chain
+        int strips, segs, H;
+        const void* fn[2][2];  // [long / two-iteration pass][red]
+    } pw;
     bool single_on;      // one-CTA k_single for single small pairs (UOT_SINGLE)
     int single_v;        // its pixels per thread: 8 (nx % 8 == 0) or 4 (UOT_SINGLE_V=4 forces 4)
     struct LogE { int64_t iter; int slot, rcur; };
@@ -490,6 +498,82 @@ static int wave_height(long long G, int strips, int ny, int S, int resident = 0)
 static int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
     return v && *v ? atoi(v) : dflt;
+}
+
+// Chain prox (rho < inf) without shard halos: k_wave_prox passes of 3 (and 2) iterations.  A pair
+// group is a cluster of cl CTAs x kWpWarps pairs writing the middle cl*8 - 2*3 of them; cl
+// (1, 2, 4, 8) minimises the CTAs per (strip, segment), the segment height follows the
+// wave-quantisation model with the co-resident clusters the occupancy API reports.
+// (l1 growth term only: the p = 2 / balanced variants of chain prox run k_iter.)
+static void plan_prox_wave(uot_ctx* c) {
+    using namespace uotk;
+    memset(&c->pw, 0, sizeof(c->pw));
+    if (c->r_mode != 0) return;
+    c->pw.S = 3;                         // C4 chain prox: S = 3 1.81e11 px-it/s, S = 4 0.97e11 (255 registers, spills)
+    c->pw.fn[0][0] = (const void*)k_wave_prox<3, 0, false>;
+    c->pw.fn[0][1] = (const void*)k_wave_prox<3, 0, true>;
+    c->pw.fn[1][0] = (const void*)k_wave_prox<2, 0, false>;
+    c->pw.fn[1][1] = (const void*)k_wave_prox<2, 0, true>;
+    const size_t sm[2] = {WpCfg<3>::smem, WpCfg<2>::smem};
+    for (int k = 0; k < 2; ++k)
+        for (int red = 0; red < 2; ++red)
+            if (cudaFuncSetAttribute(c->pw.fn[k][red], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm[k]) != cudaSuccess) {
+                cudaGetLastError();
+                return;
+            }
+    const int S = c->pw.S;
+    int best_cl = 0;
+    long long best = 1LL << 62;
+    const int clenv = env_int("UOT_PROX_CL", 0);
+    for (int cl = 1; cl <= 8; cl *= 2) {
+        if (clenv > 0 && cl != clenv) continue;
+        const int V = cl * kWpWarps - 2 * S;
+        if (V <= 0) continue;
+        const long long ctas = (long long)c->B * ((c->P + V - 1) / V) * cl;
+        if (ctas < best) { best = ctas; best_cl = cl; }
+    }
+    if (!best_cl) return;
+    c->pw.cl = best_cl;
+    c->pw.groups = (c->P + best_cl * kWpWarps - 2 * S - 1) / (best_cl * kWpWarps - 2 * S);
+    c->pw.strips = wave_strips(c->nx, S);
+    // co-resident clusters (one 256-thread CTA per SM; cluster placement may strand SMs)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(best_cl * 64, 1);
+    cfg.blockDim = dim3(kWpWarps * 32);
+    cfg.dynamicSmemBytes = sm[0];
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = best_cl; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclus = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclus, c->pw.fn[0][0], &cfg) != cudaSuccess || nclus <= 0) {
+        cudaGetLastError();
+        return;
+    }
+    const long long G = (long long)c->B * c->pw.groups * best_cl;     // CTAs per (strip, segment)
+    const int hset = env_int("UOT_PROX_WAVE_H", 0);
+    // wave_height with its wave = kSMs x resident: resident = co-resident CTAs / kSMs (rounded)
+    int H = 16;
+    {
+        const long long wave = (long long)nclus * best_cl;
+        double bt = 1e300;
+        for (int n = (c->ny + 511) / 512; n <= (c->ny + 15) / 16; ++n) {
+            const int h = (c->ny + n - 1) / n;
+            if (h < 16) break;
+            const long long units = G * c->pw.strips * n;
+            const double t = (double)((units + wave - 1) / wave) * (h + 2 * S) * (1.0 + 1e-9 * n);
+            if (t < bt * (1.0 - 1e-12)) { bt = t; H = h; }
+        }
+    }
+    if (hset > 0) H = std::max(16, hset);               // >= 16: records within uot_scratch_doubles
+    if (H > c->ny) H = c->ny;
+    c->pw.H = H;
+    c->pw.segs = (c->ny + H - 1) / H;
+    c->pw.ok = true;
+    if (env_int("UOT_DEBUG", 0))
+        fprintf(stderr, "k_wave_prox plan: S %d cl %d groups %d strips %d segs %d H %d, %d co-resident clusters\n",
+                c->pw.S, c->pw.cl, c->pw.groups, c->pw.strips, c->pw.segs, c->pw.H, nclus);
 }
 
 // Work decomposition of k_iter: strips of
@@ -734,9 +818,15 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
         }
         v.ty = (p.ny + v.th - 1) / v.th;
     }
+    memset(&c->pw, 0, sizeof(c->pw));
+    if (prox && b.r_alt && !b.a_prev_halo && !b.a_next_halo && p.nx % 4 == 0 && env_int("UOT_PROX_WAVE", 1) != 0 &&
+        al16(b.frames) && al16(b.mx[0]) && al16(b.mx[1]) && al16(b.my[0]) && al16(b.my[1]) && al16(b.a[0]) &&
+        al16(b.a[1]) && al16(b.r) && al16(b.r_alt) && al16(b.x[0]) && al16(b.x[1]))
+        plan_prox_wave(c);
     size_t recs = part_records(c->geo, c->G, c->bpp);
     for (const TVar& v : c->tv)
         if ((size_t)c->G * v.tx * v.ty > recs) recs = (size_t)c->G * v.tx * v.ty;
+    if (c->pw.ok && (size_t)c->G * c->pw.strips * c->pw.segs > recs) recs = (size_t)c->G * c->pw.strips * c->pw.segs;
     c->part = b.scratch;
     c->pair_it = c->part + recs * kRec;
     c->pair_obj = c->pair_it + (size_t)c->G * kRec;
@@ -1279,6 +1369,72 @@ static int launch_pass(uot_ctx* c, int vi, bool red, const int* stop, double tol
     return UOT_OK;
 }
 
+// Chain prox: S (4 or 2) iterations in one pass of k_wave_prox (uot_wave_prox.cuh), launched as
+// clusters of pw.cl CTAs; iterations iter+1 .. iter+S, reductions (red) for iteration iter+S.
+static int launch_prox_pass(uot_ctx* c, int S, bool red, const int* stop, double tol) {
+    const int in = c->slot, o = in ^ 1;
+    uotk::WaveProxArgs W{};
+    W.nx = c->nx; W.ny = c->ny; W.strips = c->pw.strips; W.segs = c->pw.segs; W.H = c->pw.H;
+    W.B = c->B; W.T = c->T; W.P = c->P; W.groups = c->pw.groups; W.cl = c->pw.cl; W.N = c->N;
+    W.p = c->b.frames;
+    W.mx_in = c->b.mx[in]; W.my_in = c->b.my[in]; W.a_in = c->b.a[in]; W.r_in = rbuf(c); W.x_in = c->b.x[in];
+    W.mx_out = c->b.mx[o]; W.my_out = c->b.my[o]; W.a_out = c->b.a[o];
+    W.r_out = c->rcur ? c->b.r : c->b.r_alt; W.x_out = c->b.x[o];
+    const double rt = c->p.rho * c->tau1;
+    W.tau1 = c->tau1f; W.tau2 = c->tau2f; W.atau1 = (float)(c->p.alpha * c->tau1); W.r_scale = c->r_scale;
+    W.c1 = (float)(rt / (1.0 + rt)); W.c2 = (float)(1.0 / (1.0 + rt)); W.c3 = (float)(c->tau1 / (1.0 + rt));
+    W.fix_first = c->fix_first;
+    W.partials = c->part; W.stop = stop;
+    cudaEvent_t e1 = nullptr;
+    if (c->timing) {
+        while (c->ev_used + 2 > c->ev.size()) {
+            cudaEvent_t ev;
+            if (cudaEventCreate(&ev) != cudaSuccess) return fail(c, UOT_E_CUDA, "cudaEventCreate");
+            c->ev.push_back(ev);
+        }
+        cudaEventRecord(c->ev[c->ev_used], c->s);
+        e1 = c->ev[c->ev_used + 1];
+        c->ev_used += 2;
+        c->ev_kind.push_back(11);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(c->B * c->pw.groups * c->pw.cl), (unsigned)(c->pw.strips * c->pw.segs));
+    cfg.blockDim = dim3(uotk::kWpWarps * 32);
+    cfg.dynamicSmemBytes = S == 3 ? uotk::WpCfg<3>::smem : uotk::WpCfg<2>::smem;
+    cfg.stream = c->s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c->pw.cl; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = c->pdl ? 2 : 1;
+    void* kargs[1] = {(void*)&W};
+    cudaError_t e = cudaLaunchKernelExC(&cfg, c->pw.fn[S == 2 ? 1 : 0][red ? 1 : 0], kargs);
+    if (e1) cudaEventRecord(e1, c->s);
+    if (e != cudaSuccess) return fail(c, UOT_E_CUDA, "k_wave_prox launch: %s", cudaGetErrorString(e));
+    int rc = check_launch(c, "k_wave_prox");
+    if (rc) return rc;
+    c->iter += S;
+    c->slot ^= 1;
+    c->rcur ^= 1;
+    log_launch(c);
+    if (red) {
+        ReduceArgs R{};
+        R.partials = c->part; R.recs_per_pair = c->pw.strips * c->pw.segs; R.G = c->G;
+        R.pair_out = c->pair_it; R.glob = c->glob; R.counter = c->counter;
+        R.stop = const_cast<int*>(stop); R.max_mask = 0u; R.is_iteration = 1; R.is_setup = 0;
+        R.iteration = c->iter; R.tol = tol; R.tau1 = c->tau1;
+        {
+            void* rargs[1] = {(void*)&R};
+            launch_k(c, (const void*)k_pair_reduce, dim3(c->G), dim3(256), 0, rargs);
+        }
+        rc = check_launch(c, "k_pair_reduce(prox wave)");
+        if (rc) return rc;
+    }
+    return UOT_OK;
+}
+
 // Small grids: the SMEM-resident persistent kernel, unless k_iter2 serves the fixed-
 // marginal problem and it has more than kPersistMaxPx pair-pixels (measured: C2, 512^2,
 // 5.5 us/iteration with k_iter2 vs 8.8 with k_persist; C1, 64^2: k_persist 2x faster).
@@ -1348,6 +1504,15 @@ static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, c
         // iterations up to and including the next reduction (or the end of the call)
         int d = n - k;
         if (reduce_every > 0) d = std::min(d, reduce_every - (k % reduce_every));
+        if (c->pw.ok) {                 // chain prox: passes of 3, then 2, then one k_iter
+            const int L = c->pw.S;
+            const int S = d >= L ? L : (d >= 2 ? 2 : 1);
+            const int rc = S == 1 ? launch_one(c, UOT_PART_ALL, need_red(k), stop, tol)
+                                  : launch_prox_pass(c, S, need_red(k + S - 1), stop, tol);
+            k += S;
+            if (rc) return rc;
+            continue;
+        }
         const int S = pick_pass(c, d);
         const int rc = S == 1 ? launch_one(c, UOT_PART_ALL, need_red(k), stop, tol)
                               : launch_pass(c, pass_variant(c, S), need_red(k + S - 1), stop, tol);
@@ -1653,6 +1818,7 @@ int uot_kernel_path(const uot_ctx* c) {
     if (use_single(c)) return 10;
     if (c->tp.ok && c->t2ok && c->t2on) return 8;
     if (use_persist(c)) return 2;
+    if (c->pw.ok) return 11;
     if (!(c->t2ok && c->t2on)) return 0;
     const bool four = c->t4on && c->tv[1].ok;
     const TVar& v = c->tv[four ? 1 : 0];

@@ -119,6 +119,10 @@ __device__ __forceinline__ void zero(float (&d)[V]) {
 
 // shrink^{l2}_{tau1} factor: max(||q|| - tau1, 0)/||q||, 0 at q = 0 (L7).
 // rsqrt(0) = +inf -> 1 - tau1*inf = -inf -> 0.
+// |q|^2 of the flux-prox argument in ONE association, fma(qy, qy, qx * qx), in every kernel (the
+// packed-fp32x2 wavefronts compute it the same way): paths that must agree bitwise do
+__device__ __forceinline__ float norm2(float qx, float qy) { return __fmaf_rn(qy, qy, __fmul_rn(qx, qx)); }
+
 __device__ __forceinline__ float shrink_factor(float n2, float inv, float t1) {
     return fmaxf(fmaf(-t1, inv, 1.f), 0.f);
 }
@@ -264,9 +268,9 @@ k_iter(const IterArgs A) {
             const float ar = (v < V - 1) ? a_p[(v + 1) % V] : (lane == 31 ? aR_p : nb);
             const float gx = colx[v] ? a_p[v] - ar : 0.f;
             const float gy = a_p[v] - a_c[v];            // row j0-1 < ny-1
-            const float qx = (colx[v] ? mxp[v] : 0.f) - t1 * gx;
-            const float qy = myp[v] - t1 * gy;
-            const float n2 = qx * qx + qy * qy;
+            const float qx = __fmaf_rn(-t1, gx, (colx[v] ? mxp[v] : 0.f));
+            const float qy = __fmaf_rn(-t1, gy, myp[v]);
+            const float n2 = norm2(qx, qy);
             const float s = shrink_factor(n2, rsqrtf(n2), t1);
             myp_n[v] = s * qy;
             myp_o[v] = myp[v];
@@ -347,9 +351,9 @@ k_iter(const IterArgs A) {
             const float gy = lastrow ? 0.f : a_c[v] - c_a[v];
             mxk[v] = colx[v] ? c_mx[v] : 0.f;           // pinned components read as 0 (L3)
             myk[v] = lastrow ? 0.f : c_my[v];
-            const float qx = mxk[v] - t1 * gx;
-            const float qy = myk[v] - t1 * gy;
-            const float n2 = qx * qx + qy * qy;
+            const float qx = __fmaf_rn(-t1, gx, mxk[v]);
+            const float qy = __fmaf_rn(-t1, gy, myk[v]);
+            const float n2 = norm2(qx, qy);
             const float inv = rsqrtf(n2);
             const float s = shrink_factor(n2, inv, t1);
             mxn[v] = s * qx;
@@ -397,9 +401,9 @@ k_iter(const IterArgs A) {
                 const float gxL = aL_c - a_c[0];
                 const float gyL = lastrow ? 0.f : aL_c - c_aL;
                 const float kyL = lastrow ? 0.f : c_myL;
-                const float qx = c_mxL - t1 * gxL;
-                const float qy = kyL - t1 * gyL;
-                const float n2 = qx * qx + qy * qy;
+                const float qx = __fmaf_rn(-t1, gxL, c_mxL);
+                const float qy = __fmaf_rn(-t1, gyL, kyL);
+                const float n2 = norm2(qx, qy);
                 lmn0 = shrink_factor(n2, rsqrtf(n2), t1) * qx;
                 lmk0 = c_mxL;
             } else {

@@ -176,9 +176,9 @@ k_persist(const PersistArgs A) {
                 const float ac = sA[ka];
                 const float gx = (gi < nx - 1) ? ac - sA[ka + 1] : 0.f;
                 const float gy = (gj < ny - 1) ? ac - sA[ka + L.wa] : 0.f;
-                const float qx = MXk[e] - t1 * gx;
-                const float qy = MYk[e] - t1 * gy;
-                const float n2 = qx * qx + qy * qy;
+                const float qx = __fmaf_rn(-t1, gx, MXk[e]);
+                const float qy = __fmaf_rn(-t1, gy, MYk[e]);
+                const float n2 = norm2(qx, qy);
                 const float s = shrink_factor(n2, rsqrtf(n2), t1);
                 mxn = s * qx;
                 myn = s * qy;

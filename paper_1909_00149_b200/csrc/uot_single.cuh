@@ -112,9 +112,9 @@ __global__ void __launch_bounds__(V == 8 ? kSingleThreads / 2 : kSingleThreads, 
         for (int v = 0; v < V; ++v) {
             const float gx = a[v] - (v < V - 1 ? a[v + 1] : aR);
             const float gy = a[v] - ad[v];
-            const float qx = mx[v] - (v == V - 1 ? t1xl : t1) * gx;
-            const float qy = my[v] - t1y * gy;
-            const float n2 = qx * qx + qy * qy;
+            const float qx = __fmaf_rn(-(v == V - 1 ? t1xl : t1), gx, mx[v]);
+            const float qy = __fmaf_rn(-t1y, gy, my[v]);
+            const float n2 = norm2(qx, qy);
             const float inv = rsqrt_ftz(n2);
             const float sf = shrink_factor(n2, inv, t1);
             nmx[v] = sf * qx;

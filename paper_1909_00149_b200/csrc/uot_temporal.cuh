@@ -212,9 +212,9 @@ __device__ __forceinline__ void iter_tile(const Iter2Args& A, float* sm, double*
             for (int v = 0; v < 4; ++v) {
                 const float gx = colx(r, c + v) ? av[v] - av[v + 1] : 0.f;
                 const float gy = rowy(r, c + v) ? av[v] - adv[v] : 0.f;
-                const float qx = mxv[v] - t1 * gx;   // M is 0 on pinned / outside
-                const float qy = myv[v] - t1 * gy;
-                const float n2 = qx * qx + qy * qy;
+                const float qx = __fmaf_rn(-t1, gx, mxv[v]);   // M is 0 on pinned / outside
+                const float qy = __fmaf_rn(-t1, gy, myv[v]);
+                const float n2 = norm2(qx, qy);
                 const float sf = shrink_factor(n2, rsqrtf(n2), t1);
                 ox[v] = sf * qx;
                 oy[v] = sf * qy;

@@ -165,9 +165,9 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S, RED>::minb) k_wave
             for (int v = 0; v < 4; ++v) {
                 const float gx = av[v] - av[v + 1];
                 const float gy = av[v] - f4c(cA, v);
-                const float qx = f4c(qmx, v) - (v == 3 ? t1x3 : t1) * gx;
-                const float qy = f4c(qmy, v) - t1y * gy;
-                const float n2 = qx * qx + qy * qy;
+                const float qx = __fmaf_rn(-(v == 3 ? t1x3 : t1), gx, f4c(qmx, v));
+                const float qy = __fmaf_rn(-t1y, gy, f4c(qmy, v));
+                const float n2 = norm2(qx, qy);
                 const float inv = rsqrt_ftz(n2);
                 const float sf = shrink_factor(n2, inv, t1);
                 nmx[v] = sf * qx;
@@ -372,9 +372,9 @@ __global__ void __launch_bounds__(kWaveDfWarps * 32, 8 / kWaveDfWarps) k_wave_df
             for (int v = 0; v < 4; ++v) {
                 const float gx = av[v] - av[v + 1];
                 const float gy = av[v] - f4c(cA, v);
-                const float qx = f4c(q.mx, v) - (v == 3 ? t1x3 : t1) * gx;
-                const float qy = f4c(q.my, v) - t1y * gy;
-                const float n2 = qx * qx + qy * qy;
+                const float qx = __fmaf_rn(-(v == 3 ? t1x3 : t1), gx, f4c(q.mx, v));
+                const float qy = __fmaf_rn(-t1y, gy, f4c(q.my, v));
+                const float n2 = norm2(qx, qy);
                 const float inv = rsqrt_ftz(n2);
                 const float sf = shrink_factor(n2, inv, t1);
                 nmx[v] = sf * qx;

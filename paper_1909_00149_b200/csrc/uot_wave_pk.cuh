@@ -16,7 +16,8 @@
 // contraction across intrinsics); the previous K is carried negated (nK = -K, computed as
 // (r - div M) + f, an exact negation) so line 7's 2K' - K is one fma(-2, nK', nK); the
 // l1 soft threshold is evaluated as q - clamp(q, -s, s), equal to sign(q) max(|q| - s, 0)
-// in round-to-nearest.  The one reassociation is n2 = qx^2 + qy^2's product order.
+// in round-to-nearest; |q|^2 is fma(qy, qy, qx * qx) as in every kernel (norm2).  So the
+// iterates equal k_wave's value for value (zeros may differ in sign).
 #pragma once
 #include "uot_wave.cuh"
 
@@ -170,18 +171,33 @@ __global__ void __launch_bounds__(kWaveWarps * 32, WaveCfg<S, RED>::minb) k_wave
             const Quad nkn = qadd(qsub(rn, divn), Fr);
             const Quad an = qfma(pk_dup(t2), qfma(pk_dup(-2.f), nkn, p.nk), p.a);
             if (RED && j == S) {                                 // branch-free: weight 0 off the output
+                // per-quad partial sums (packed where the terms are), then one weighted add per
+                // sum and row; the five a6 sums of k_wave in a different association order
                 const float wr = (writer && rho >= y0 && rho < y1) ? 1.f : 0.f;
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const float n2v = qc(n2, v), invv = qc(inv, v), rv = qc(rn, v), kv = qc(nkn, v);
-                    const float nrm = fmaxf(fmaf(n2v, fminf(invv, 1e30f), -t1), 0.f);   // |M^j| (k_wave)
-                    const float dmx = qc(nmx, v) - qc(p.mx, v), dmy = qc(nmy, v) - qc(p.my, v), dr = rv - qc(p.r, v);
-                    s_tr = fmaf(wr, nrm, s_tr);
-                    s_gr = fmaf(wr, pw(rv, RM), s_gr);
-                    s_k2 = fmaf(wr * kv, kv, s_k2);
-                    s_dz = fmaf(wr, dmx * dmx + dmy * dmy + dr * dr, s_dz);
-                    s_ub = fmaf(wr, pw(qc(divn, v) - qc(Fr, v), RM), s_ub);
+                const Quad ic = {make_float2(fminf(inv.l.x, 1e30f), fminf(inv.l.y, 1e30f)),
+                                 make_float2(fminf(inv.h.x, 1e30f), fminf(inv.h.y, 1e30f))};
+                Quad nrm = qfma(n2, ic, qd(make_float4(-t1, -t1, -t1, -t1)));          // |M^j| (k_wave)
+                nrm = {make_float2(fmaxf(nrm.l.x, 0.f), fmaxf(nrm.l.y, 0.f)), make_float2(fmaxf(nrm.h.x, 0.f), fmaxf(nrm.h.y, 0.f))};
+                const float2 tr = pk_add(nrm.l, nrm.h);
+                const float2 k2 = pk_fma(nkn.h, nkn.h, pk_mul(nkn.l, nkn.l));
+                const Quad dmx = qsub(nmx, p.mx), dmy = qsub(nmy, p.my), dr = qsub(rn, p.r);
+                float2 dz = pk_fma(dmx.h, dmx.h, pk_mul(dmx.l, dmx.l));
+                dz = pk_fma(dmy.l, dmy.l, dz); dz = pk_fma(dmy.h, dmy.h, dz);
+                dz = pk_fma(dr.l, dr.l, dz); dz = pk_fma(dr.h, dr.h, dz);
+                const Quad ub = qsub(divn, Fr);
+                float gr, ubs;
+                if constexpr (RM == 1) {
+                    const float2 g2 = pk_fma(rn.h, rn.h, pk_mul(rn.l, rn.l)), u2 = pk_fma(ub.h, ub.h, pk_mul(ub.l, ub.l));
+                    gr = g2.x + g2.y; ubs = u2.x + u2.y;
+                } else {
+                    gr = (fabsf(rn.l.x) + fabsf(rn.l.y)) + (fabsf(rn.h.x) + fabsf(rn.h.y));
+                    ubs = (fabsf(ub.l.x) + fabsf(ub.l.y)) + (fabsf(ub.h.x) + fabsf(ub.h.y));
                 }
+                s_tr = fmaf(wr, tr.x + tr.y, s_tr);
+                s_gr = fmaf(wr, gr, s_gr);
+                s_k2 = fmaf(wr, k2.x + k2.y, s_k2);
+                s_dz = fmaf(wr, dz.x + dz.y, s_dz);
+                s_ub = fmaf(wr, ubs, s_ub);
             }
             upY[j] = nmy;
             if (j < S) {

@@ -78,8 +78,8 @@ class Problem:
         self.mx = [e(plane), e(plane)]
         self.my = [e(plane), e(plane)]
         self.r = e(plane)
-        # fixed marginals: second r buffer for the two-iterations-per-pass kernel (k_iter2)
-        self.r_alt = e(plane) if not self.prox else None
+        # second r buffer for the multi-iteration passes (k_wave / k_iter2; chain prox: k_wave_prox)
+        self.r_alt = e(plane)
         self.a = [e(plane), e(plane)]
         self.x = [e(self.frames.shape), e(self.frames.shape)] if self.prox else [None, None]
         # chain-prox shard halos (L19): duals of the pairs just outside this shard, [B][ny][nx]
@@ -204,7 +204,8 @@ class Problem:
         check(lib().uot_get_timing(self._ctx, ctypes.byref(ms), ctypes.byref(n)), self._ctx)
         return ms.value, n.value
 
-    PATH_NAMES = ("k_iter", "k_iter2", "k_persist", "k_iter4", "k_df", "k_wave2", "k_wave4", "k_wave3", "k_tpersist", "k_wave5", "k_single")
+    PATH_NAMES = ("k_iter", "k_iter2", "k_persist", "k_iter4", "k_df", "k_wave2", "k_wave4", "k_wave3", "k_tpersist", "k_wave5", "k_single",
+                  "k_wave_prox")
 
     def get_timing_paths(self):
         """{kernel: (summed device ms, launches)} of the timed launches, split by kernel

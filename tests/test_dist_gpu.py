@@ -24,7 +24,7 @@ ALPHA = 1.3
 # the same per-pass kernels on both sides: the persistent kernels are chosen per call (a
 # sharded run issues one call per check interval) and the wavefront / SMEM-tile choice
 # depends on the pair count, and different kernels need not round identically
-PATH_ENV = {"UOT_TPERSIST": "0", "UOT_PERSIST": "0", "UOT_WAVE": "1"}
+PATH_ENV = {"UOT_TPERSIST": "0", "UOT_PERSIST": "0", "UOT_WAVE": "1", "UOT_PROX_WAVE": "0"}
 # the persistent SMEM-tile passes (one cooperative launch per call): the same 4 + 4 + 2 pass plan
 # per check interval on both sides, so also bitwise
 PATH_ENV_TP = {"UOT_TPERSIST": "1", "UOT_PERSIST": "0", "UOT_WAVE": "0", "UOT_SINGLE": "0"}

@@ -106,11 +106,14 @@ def _emulated_shards(fr, alpha, rho, tau, n, cut):
 
 
 @pytest.mark.parametrize("T,cut", [(4, 2), (6, 1), (6, 4)])
-def test_sharded_chain_bitwise(T, cut):
+def test_sharded_chain_bitwise(T, cut, monkeypatch):
     fr = inputs.gen_random(2, T, 24, 64, seed=11, kind="sparse")
     alpha, rho = 1.1, 4.0
     tau = oracle.default_steps(64, 24, prox=True, n_frames=T, safety=0.95)[0]
     n = 40
+    # the unsharded chain on the shards' kernel (one pass per iteration; shards with halos never
+    # take the multi-iteration k_wave_prox, which agrees with it to rounding: test_prox_wave_gpu)
+    monkeypatch.setenv("UOT_PROX_WAVE", "0")
     full = Problem(torch.from_numpy(fr).cuda(), alpha, rho=rho, tau1=tau, tau2=tau)
     full.step(n)
     A, Bp = _emulated_shards(fr, alpha, rho, tau, n, cut)
@@ -193,14 +196,15 @@ def test_interior_boundary_parts_equal_full_iteration(T):
     assert ra["objective"] == rb["objective"] and ra["iterations"] == rb["iterations"] == 12
 
 
-def test_sharded_chain_driver_overlap_emulated():
+def test_sharded_chain_driver_overlap_emulated(monkeypatch):
     """ShardedChain-style overlapped schedule (interior pairs, halo copy, boundary pairs) on
-    two shards of one chain equals the unsharded chain bitwise."""
+    two shards of one chain equals the unsharded chain (one pass per iteration) bitwise."""
     from paper_1909_00149_b200 import _lib
     T, cut, n = 9, 4, 30
     fr = inputs.gen_random(1, T, 16, 64, seed=5, kind="sparse")
     tau = oracle.default_steps(64, 16, prox=True, n_frames=T, safety=0.95)[0]
     t = torch.from_numpy(fr).cuda()
+    monkeypatch.setenv("UOT_PROX_WAVE", "0")
     full = Problem(t, 1.3, rho=5.0, tau1=tau, tau2=tau)
     full.iterate(n)
     A = Problem(t[:, :cut + 1].contiguous(), 1.3, rho=5.0, tau1=tau, tau2=tau, halos=(False, True))
