@@ -406,12 +406,13 @@ def main():
     # ---- roofline of the dominant kernel (largest share of the timed launches).  Fixed
     #      marginals: one launch = one HBM pass of the state (k_iter4: four fused iterations,
     #      k_iter2: two, k_iter: one), algorithmic 36 B per pair-pixel per pass.  k_persist:
-    #      per iteration.  Chain prox: per iteration (1 launch, or interior + boundary launches).
+    #      per iteration.  Chain prox: per iteration (1 launch, or interior + boundary launches);
+    #      k_wave_prox: per pass of 3 (2) iterations, algorithmic 44 B per pair-pixel per pass.
     peak, peak_src = load_peaks()
     alg_bytes_launch = bytes_iter
     dom = max(by_path, key=lambda k: by_path[k][0])
     dom_ms, dom_n = by_path[dom]
-    if prox or dom in ("k_persist", "k_tpersist", "k_single"):
+    if (prox and dom != "k_wave_prox") or dom in ("k_persist", "k_tpersist", "k_single"):
         avg_launch_s = (dom_ms / max(iters_timed, 1)) / 1e3
     else:
         avg_launch_s = (dom_ms / max(dom_n, 1)) / 1e3
@@ -427,7 +428,9 @@ def main():
                    "k_persist": "k_persist (all iterations in one cooperative launch, SMEM-resident)",
                    "k_tpersist": "k_tpersist (all passes of a call in one cooperative launch, SMEM tiles)",
                    "k_single": "k_single (every iteration of a call in ONE CTA, state in registers; "
-                               "SMEM/latency-bound on one SM: the HBM fraction is not meaningful)"}.get(
+                               "SMEM/latency-bound on one SM: the HBM fraction is not meaningful)",
+                   "k_wave_prox": "k_wave_prox<S=3> (chain prox: three fused Alg.1 iterations per HBM pass, "
+                                  "pair groups in clusters exchanging duals by st.async)"}.get(
         dom, f"k_iter<{'prox' if prox else 'fixed'}> (fused Alg.1 iteration)")
     shares = {k: {"ms": v[0], "launches": v[1], "share": v[0] / max(kern_ms, 1e-30)} for k, v in by_path.items()}
 
@@ -457,7 +460,8 @@ def main():
     prof_sum = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof_sum):
         try:
-            key = cfg.name + ("-prox" if prox else (f"-{dom}" if temporal else ""))
+            key = cfg.name + (("-k_wave_prox" if dom == "k_wave_prox" else "-prox") if prox
+                              else (f"-{dom}" if temporal else ""))
             d = json.load(open(prof_sum)).get(key)
             if d:
                 traffic = d.get("dram_bytes_per_launch")

@@ -224,8 +224,9 @@ int uot_set_temporal(uot_ctx* ctx, int enable);
  * nx % 4 == 0 and nx/4 * ny <= 1024, fixed marginals: every iteration of a call in ONE CTA with the
  * state in registers, reductions and stopping test in-kernel; UOT_SINGLE=0 disables it), 11 =
  * k_wave_prox (chain prox, rho < inf, with buffers.r_alt, aligned planes, nx % 4 == 0 and no
- * shard halos: four (two) iterations per pass, pairs in lockstep groups of clusters of CTAs;
- * UOT_PROX_WAVE=0 disables it).  Four-iteration contexts fill in
+ * shard halos, when its pair groups waste at most 1.34 pair slots per pair: three (two)
+ * iterations per pass, pairs of a group in clusters of CTAs exchanging duals by st.async;
+ * UOT_PROX_WAVE=0 disables it, =2 forces it).  Four-iteration contexts fill in
  * with two-iteration passes / k_iter where a reduction falls inside four iterations. */
 int uot_kernel_path(const uot_ctx* ctx);
 

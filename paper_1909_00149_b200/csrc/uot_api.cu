@@ -533,6 +533,10 @@ static void plan_prox_wave(uot_ctx* c) {
         if (ctas < best) { best = ctas; best_cl = cl; }
     }
     if (!best_cl) return;
+    // pair slots per pair (halo pairs + idle slots): C4 320 / 255 = 1.25 runs the wave (1.54e11 vs
+    // k_iter 1.29e11 px-it/s); C3 96 / 63 = 1.52 is slower than one pass per iteration (0.87e11 vs
+    // 1.08e11), so above 1.34 chain prox stays on k_iter (UOT_PROX_WAVE=2 forces the wave)
+    if ((double)best * kWpWarps / ((double)c->B * c->P) > 1.34 && env_int("UOT_PROX_WAVE", 1) != 2) return;
     c->pw.cl = best_cl;
     c->pw.groups = (c->P + best_cl * kWpWarps - 2 * S - 1) / (best_cl * kWpWarps - 2 * S);
     c->pw.strips = wave_strips(c->nx, S);

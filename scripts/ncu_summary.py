@@ -1,5 +1,6 @@
 #!/usr/bin/env python
 """Summarise ncu outputs into profiles/ (run here, on the CPU box).
+(`full` also reads the raw-page CSV export of a report made on the GPU box.)
 
   python scripts/ncu_summary.py launches <launches.csv> <out.md>
   python scripts/ncu_summary.py full <report.ncu-rep> <config> <alg_bytes_per_launch> <out.json> [kernel-substring]
@@ -13,7 +14,11 @@ import sys
 
 
 def launches(path, out):
-    lines = open(path).read().splitlines()
+    if path.endswith(".gz"):
+        import gzip
+        lines = gzip.open(path, "rt").read().splitlines()
+    else:
+        lines = open(path).read().splitlines()
     start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
     rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
     tot = collections.defaultdict(float)
@@ -47,12 +52,21 @@ METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.
 
 
 def full(rep, config, alg_bytes, out, pick=None):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """rep: an .ncu-rep, or its `ncu -i ... --page raw --csv` export (.csv / .csv.gz, summarised on the box)."""
+    if rep.endswith(".csv.gz"):
+        import gzip
+        raw = gzip.open(rep, "rt").read()
+    elif rep.endswith(".csv"):
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     res = {}
     for vals in rows[2:]:
         kname = vals[hdr.index("Kernel Name")]
+        if kname in res:
+            continue                  # several launches of one kernel: the first
         d = {}
         for m in METRICS:
             if m in hdr:

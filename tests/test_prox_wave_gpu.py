@@ -17,6 +17,7 @@ from paper_1909_00149_b200.uot import Problem
 pytestmark = pytest.mark.gpu
 
 NO_WAVE = {"UOT_PROX_WAVE": "0"}
+WAVE = {"UOT_PROX_WAVE": "2"}       # force the wave (small test chains waste more pair slots than the size rule allows)
 
 
 def _run(fr, alpha, rho, tau, n, env, monkeypatch, check=0, fix_first=False, x_from_p=False):
@@ -60,7 +61,7 @@ def test_prox_wave_matches_k_iter_and_oracle(case, n, check, monkeypatch):
     B, T, ny, nx, alpha, rho, env = case
     fr = inputs.gen_random(B, T, ny, nx, seed=T * 13 + nx, kind="sparse")
     tau = oracle.default_steps(nx, ny, prox=True, n_frames=T, safety=0.95)[0]
-    pw, rw = _run(fr, alpha, rho, tau, n, env, monkeypatch, check)
+    pw, rw = _run(fr, alpha, rho, tau, n, {**WAVE, **env}, monkeypatch, check)
     assert pw.kernel_path == "k_wave_prox"
     pi, ri = _run(fr, alpha, rho, tau, n, {**NO_WAVE, "UOT_PERSIST": 0}, monkeypatch, check)
     assert pi.kernel_path == "k_iter"
@@ -83,7 +84,7 @@ def test_prox_wave_fix_first_and_warm_x(T, monkeypatch):
     """Constant first frame and the x^0 = max(p, 0) warm start (L8)."""
     fr = inputs.gen_random(1, T, 21, 64, seed=T, kind="uniform")
     tau = oracle.default_steps(64, 21, prox=True, n_frames=T, safety=0.95, fix_first=True)[0]
-    pw, rw = _run(fr, 1.3, 2.5, tau, 26, {"UOT_PROX_CL": 2}, monkeypatch, 10, fix_first=True, x_from_p=True)
+    pw, rw = _run(fr, 1.3, 2.5, tau, 26, {**WAVE, "UOT_PROX_CL": 2}, monkeypatch, 10, fix_first=True, x_from_p=True)
     pi, ri = _run(fr, 1.3, 2.5, tau, 26, NO_WAVE, monkeypatch, 10, fix_first=True, x_from_p=True)
     for k in ("mx", "my", "r", "a", "x"):
         scale = max(float(pi.state()[k].abs().max()), 1e-30)
@@ -101,6 +102,7 @@ def test_prox_wave_device_stop(monkeypatch):
     tau = oracle.default_steps(32, 12, prox=True, n_frames=4, safety=0.95)[0]
     with monkeypatch.context() as m:
         m.setenv("UOT_PROX_CL", "2")
+        m.setenv("UOT_PROX_WAVE", "2")
         prob = Problem(torch.from_numpy(fr).cuda(), 0.9, rho=3.0, tau1=tau, tau2=tau)
     assert prob.kernel_path == "k_wave_prox"
     rep = prob.solve(20000, tol=1e-4, check_every=10)
@@ -120,6 +122,7 @@ def test_prox_wave_graph_capture(monkeypatch):
     s = torch.cuda.Stream()
     with monkeypatch.context() as m:
         m.setenv("UOT_PROX_CL", "2")
+        m.setenv("UOT_PROX_WAVE", "2")
         prob = Problem(torch.from_numpy(fr).cuda(), 1.0, rho=4.0, tau1=tau, tau2=tau, stream=s)
     assert prob.kernel_path == "k_wave_prox"
     torch.cuda.synchronize()
