@@ -448,7 +448,7 @@ struct uot_ctx {
         const void* fn[2][2];  // [long / two-iteration pass][red]
     } pw;
     bool single_on;      // one-CTA k_single for single small pairs (UOT_SINGLE)
-    int single_v;        // its pixels per thread: 8 (nx % 8 == 0) or 4 (UOT_SINGLE_V=4 forces 4)
+    int single_v;        // its pixels per thread: 8 (nx % 8 == 0) or 4 (UOT_SINGLE_V=4 forces 4, =16 tries 16)
     struct LogE { int64_t iter; int slot, rcur; };
     std::vector<LogE> log;           // launches since the stop was armed (device-stop correction)
     std::vector<LogE> persist_base;  // state at the start of each persistent launch since arming
@@ -1212,12 +1212,14 @@ static int launch_single(uot_ctx* c, int n, int reduce_every, bool reduce_last, 
         c->ev_used += 2;
         c->ev_kind.push_back(10);
     }
-    const bool v8 = c->nx % 8 == 0 && c->single_v != 4;
-    const void* fn = v8 ? (c->r_mode == 0 ? (const void*)k_single<0, 8>
-                                          : (c->r_mode == 1 ? (const void*)k_single<1, 8> : (const void*)k_single<2, 8>))
-                        : (c->r_mode == 0 ? (const void*)k_single<0, 4>
-                                          : (c->r_mode == 1 ? (const void*)k_single<1, 4> : (const void*)k_single<2, 4>));
-    const int V = v8 ? 8 : 4;
+    // pixels per thread: 16 (UOT_SINGLE_V=16, nx % 16 == 0), 8 (nx % 8 == 0, default) or 4
+    const int V = (c->single_v == 16 && c->nx % 16 == 0) ? 16 : ((c->nx % 8 == 0 && c->single_v != 4) ? 8 : 4);
+    const void* fn = V == 16 ? (c->r_mode == 0 ? (const void*)k_single<0, 16>
+                                               : (c->r_mode == 1 ? (const void*)k_single<1, 16> : (const void*)k_single<2, 16>))
+                   : V == 8 ? (c->r_mode == 0 ? (const void*)k_single<0, 8>
+                                              : (c->r_mode == 1 ? (const void*)k_single<1, 8> : (const void*)k_single<2, 8>))
+                            : (c->r_mode == 0 ? (const void*)k_single<0, 4>
+                                              : (c->r_mode == 1 ? (const void*)k_single<1, 4> : (const void*)k_single<2, 4>));
     const int threads = ((c->nx / V) * c->ny + 31) / 32 * 32;
     launch_k(c, fn, dim3(1), dim3(threads), 0, args);
     if (e1) cudaEventRecord(e1, c->s);

@@ -11,6 +11,7 @@
 // Included by uot_api.cu after the report-slot enum (GL_*).
 #pragma once
 #include <type_traits>
+#include "uot_wave_pk.cuh"
 
 namespace uotk {
 
@@ -49,8 +50,10 @@ __device__ __forceinline__ void st4v(float* p, const float (&d)[V]) {
     for (int u = 0; u < V; u += 4) *reinterpret_cast<float4*>(p + u) = make_float4(d[u], d[u + 1], d[u + 2], d[u + 3]);
 }
 
-template <int RM, int V>
-__global__ void __launch_bounds__(V == 8 ? kSingleThreads / 2 : kSingleThreads, 1) k_single(const SingleArgs A) {
+// PK: the pointwise arithmetic as packed fp32x2 (FFMA2 / FADD2 / FMUL2, uot_wave_pk.cuh: same
+// values as the scalar form; the two horizontal differences stay scalar).
+template <int RM, int V, bool PK = true>
+__global__ void __launch_bounds__(kSingleThreads * 4 / V, 1) k_single(const SingleArgs A) {
     __shared__ __align__(16) float As[kSingleThreads * 4];      // a^k, [ny][nx]
     __shared__ __align__(16) float Mys[kSingleThreads * 4];     // M'_y, [ny][nx]
     __shared__ float Mxw[kSingleThreads];                        // M'_x of each thread's last column
@@ -108,6 +111,28 @@ __global__ void __launch_bounds__(V == 8 ? kSingleThreads / 2 : kSingleThreads, 
 #pragma unroll
             for (int v = 0; v < V; ++v) ad[v] = 0.f;
         float nmx[V], nmy[V], nrm[V], rn[V];
+        if constexpr (PK && !RD) {
+            const float2 nt1 = pk_dup(-t1), nt1y2 = pk_dup(-t1y), one = pk_dup(1.f), tt1 = pk_dup(t1);
+#pragma unroll
+            for (int v = 0; v < V; v += 2) {
+                const float2 gx = make_float2(a[v] - a[v + 1], a[v + 1] - (v + 2 < V ? a[v + 2] : aR));
+                const float2 av = make_float2(a[v], a[v + 1]);
+                const float2 gy = pk_sub(av, make_float2(ad[v], ad[v + 1]));
+                const float2 qx = pk_fma(v + 2 < V ? nt1 : make_float2(-t1, -t1xl), gx, make_float2(mx[v], mx[v + 1]));
+                const float2 qy = pk_fma(nt1y2, gy, make_float2(my[v], my[v + 1]));
+                const float2 n2 = pk_fma(qy, qy, pk_mul(qx, qx));
+                float2 sf = pk_fma(nt1, make_float2(rsqrt_ftz(n2.x), rsqrt_ftz(n2.y)), one);
+                sf = make_float2(fmaxf(sf.x, 0.f), fmaxf(sf.y, 0.f));
+                const float2 m1 = pk_mul(sf, qx), m2 = pk_mul(sf, qy);
+                nmx[v] = m1.x; nmx[v + 1] = m1.y; nmy[v] = m2.x; nmy[v + 1] = m2.y;
+                const float2 q5 = pk_fma(tt1, av, make_float2(r[v], r[v + 1]));
+                float2 r5;
+                if constexpr (RM == 0) r5 = pk_sub(q5, make_float2(fminf(fmaxf(q5.x, -at1), at1), fminf(fmaxf(q5.y, -at1), at1)));
+                else if constexpr (RM == 1) r5 = pk_mul(q5, pk_dup(rsc));
+                else r5 = make_float2(0.f, 0.f);
+                rn[v] = r5.x; rn[v + 1] = r5.y;
+            }
+        } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const float gx = a[v] - (v < V - 1 ? a[v + 1] : aR);
@@ -123,6 +148,7 @@ __global__ void __launch_bounds__(V == 8 ? kSingleThreads / 2 : kSingleThreads, 
             // line 5: r^{k+1} = shrink_{alpha tau1}(r^k + tau1 a^k) (p = 2: averaging, L24)
             rn[v] = r_update(fmaf(t1, a[v], r[v]), RM, at1, rsc);
         }
+        }
         Mxw[q] = nmx[V - 1];
         if (act) st4v<V>(Mys + g, nmy);
         __syncthreads();
@@ -133,6 +159,20 @@ __global__ void __launch_bounds__(V == 8 ? kSingleThreads / 2 : kSingleThreads, 
         else
 #pragma unroll
             for (int v = 0; v < V; ++v) mu[v] = 0.f;
+        if constexpr (PK && !RD) {
+            const float2 tt2 = pk_dup(t2), m2 = pk_dup(-2.f);
+#pragma unroll
+            for (int v = 0; v < V; v += 2) {
+                const float2 dmx = make_float2(nmx[v] - (v ? nmx[v - 1] : ml), nmx[v + 1] - nmx[v]);
+                const float2 divn = pk_add(dmx, pk_sub(make_float2(nmy[v], nmy[v + 1]), make_float2(mu[v], mu[v + 1])));
+                // -K^{k+1} = (r - div M) + f (exact negation); a += tau2 (2K^{k+1} - K^k)
+                const float2 nk = pk_add(pk_sub(make_float2(rn[v], rn[v + 1]), divn), make_float2(f[v], f[v + 1]));
+                const float2 an = pk_fma(tt2, pk_fma(m2, nk, make_float2(-K[v], -K[v + 1])), make_float2(a[v], a[v + 1]));
+                mx[v] = nmx[v]; mx[v + 1] = nmx[v + 1]; my[v] = nmy[v]; my[v + 1] = nmy[v + 1];
+                r[v] = rn[v]; r[v + 1] = rn[v + 1]; a[v] = an.x; a[v + 1] = an.y;
+                K[v] = -nk.x; K[v + 1] = -nk.y;
+            }
+        } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const float divn = (nmx[v] - (v ? nmx[v - 1] : ml)) + (nmy[v] - mu[v]);
@@ -148,6 +188,7 @@ __global__ void __launch_bounds__(V == 8 ? kSingleThreads / 2 : kSingleThreads, 
                 sums[4] = fmaf(w, pw(divn - f[v], RM), sums[4]);
             }
             mx[v] = nmx[v]; my[v] = nmy[v]; r[v] = rn[v]; a[v] = an; K[v] = kn;
+        }
         }
     };
     int done = 0;
