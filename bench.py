@@ -61,6 +61,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--prox-shard", default="ghost", choices=["ghost", "halo"],
+                    help="chain prox at N > 1: ghost pairs (k_wave_prox passes, boundary pairs' state swapped "
+                         "every 3 / 2 iterations; dist.GhostChain) or one boundary dual per iteration "
+                         "(k_iter passes; dist.ShardedChain)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: run the N>1 code path with ranks sharing the visible GPUs and host-staged "
                          "exchanges (functional check on a 1-GPU box; not a performance number)")
@@ -307,7 +311,14 @@ def main():
 
     # ---- this rank's shard: pairs [p0, p1) -> frames [p0, p1] (last = shared boundary frame)
     p0, p1 = udist.shard_range(cfg.n_pairs, world, rank)
-    if cfg.n_chains == 1:
+    ghost = args.mode == "prox" and args.prox_shard == "ghost" and world > 1 and cfg.n_chains == 1
+    if ghost:
+        # chain prox with ghost pairs: frames [q0, q1] of the ghost range, all loaded from the host
+        _, _, q0, q1 = udist.ghost_range(cfg.n_pairs, world, rank)
+        own = make_frames(cfg, q0, q1 + 1)
+        host = torch.from_numpy(np.ascontiguousarray(own))
+        shape = tuple(own.shape)
+    elif cfg.n_chains == 1:
         own = make_frames(cfg, p0, p1 if rank < world - 1 else p1 + 1)      # owned frames
         host = torch.from_numpy(np.ascontiguousarray(own))
         shape = (1, p1 - p0 + 1, cfg.ny, cfg.nx)
@@ -322,7 +333,9 @@ def main():
     def upload(src_pinned):
         """H2D of the owned frames + boundary frame from the next rank (NCCL)."""
         n_own = src_pinned.shape[1] if cfg.n_chains == 1 else src_pinned.shape[0]
-        if cfg.n_chains == 1:
+        if ghost:
+            frames.copy_(src_pinned, non_blocking=True)
+        elif cfg.n_chains == 1:
             frames[:, :n_own].copy_(src_pinned, non_blocking=True)
             if world > 1:
                 udist.exchange_boundary_frame(frames, rank, world)
@@ -335,17 +348,20 @@ def main():
     rho = PROX_RHO if prox else math.inf
     from paper_1909_00149_b200.uot import default_steps
     tau, _ = default_steps(cfg.nx, cfg.ny, n_frames=cfg.n_frames, rho=rho)   # global chain length (L12)
+    halo = prox and world > 1 and cfg.n_chains == 1 and not ghost
+    if ghost:
+        os.environ.setdefault("UOT_PROX_WAVE", "2")    # ghost pairs need k_wave_prox whatever the pair-slot rule says
     prob = Problem(frames, cfg.alpha, rho=rho, tau1=tau, tau2=tau, stream=stream,
-                   halos=(prox and world > 1 and cfg.n_chains == 1 and rank > 0,
-                          prox and world > 1 and cfg.n_chains == 1 and rank < world - 1))
-    driver = udist.ShardedChain(prob, rank, world)
-    G = prob.G
+                   halos=(halo and rank > 0, halo and rank < world - 1))
+    driver = udist.GhostChain(prob, cfg.n_pairs, rank, world) if ghost else udist.ShardedChain(prob, rank, world)
+    G = (p1 - p0) if ghost else prob.G          # pairs this rank owns (ghost pairs are copies)
     N = cfg.nx * cfg.ny
-    bytes_iter = alg_bytes_per_iter(args.mode, G, prob.B, prob.T, N)
+    bytes_iter = alg_bytes_per_iter(args.mode, G, prob.B, G + 1 if ghost else prob.T, N)
 
     def step():
         prob.reset()
-        return driver.run(cfg.iters, check_every=args.check_every, tol=1e-12)
+        # (ghost pairs: fixed iteration counts, tol = 0)
+        return driver.run(cfg.iters, check_every=args.check_every, tol=0.0 if ghost else 1e-12)
 
     def barrier():
         if world > 1:

@@ -230,6 +230,19 @@ int uot_set_temporal(uot_ctx* ctx, int enable);
  * with two-iteration passes / k_iter where a reduction falls inside four iterations. */
 int uot_kernel_path(const uot_ctx* ctx);
 
+/* Ghost pairs of a chain-prox shard: only pairs [lo, hi) of each chain are written
+ * and reduced by k_wave_prox passes; pairs outside are read-only copies of the neighbouring
+ * shards' pairs (with their frames), which the caller refreshes after every pass -- S
+ * iterations per exchange instead of one.  The context's first / last pair is treated as a
+ * chain end (a = 0 beyond it), so a side whose ghost pairs do not reach the chain's end needs
+ * >= S = 3 of them (the dependency cone of one pass; dist.ghost_range).  Requires
+ * uot_kernel_path == 11; afterwards every run between checks must be >= 2 iterations (passes
+ * of 3 and 2; UOT_E_INVALID for a single iteration, which would be a k_iter pass updating the
+ * ghosts); the iteration reports sum the own pairs
+ * only (uot_objective still covers every pair of the context: use its per-pair rows).
+ * lo = 0, hi = P restores the whole chain. */
+int uot_set_own_pairs(uot_ctx* ctx, int32_t lo, int32_t hi);
+
 /* Cross-rank stopping test for a chain sharded over ranks: the
  * L13 test must use the residuals and ||f|| summed over ALL shards, so no rank may stop on
  * its own sums.  Stream-ordered, no host synchronisation:

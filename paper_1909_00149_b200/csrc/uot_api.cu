@@ -443,6 +443,7 @@ struct uot_ctx {
     struct {             // chain prox: register wavefront with pair groups (k_wave_prox)
         bool ok;
         int S;               // iterations of the long pass (3); short pass: 2
+        int own_lo, own_hi;  // written pairs (uot_set_own_pairs: a shard's own pairs between ghost pairs)
         int cl, groups;      // CTAs per cluster, pair groups per chain
         int strips, segs, H;
         const void* fn[2][2];  // [long / two-iteration pass][red]
@@ -500,6 +501,8 @@ static int env_int(const char* name, int dflt) {
     return v && *v ? atoi(v) : dflt;
 }
 
+static bool pw_regroup(uot_ctx* c);
+
 // Chain prox (rho < inf) without shard halos: k_wave_prox passes of 3 (and 2) iterations.  A pair
 // group is a cluster of cl CTAs x kWpWarps pairs writing the middle cl*8 - 2*3 of them; cl
 // (1, 2, 4, 8) minimises the CTAs per (strip, segment), the segment height follows the
@@ -533,18 +536,33 @@ static void plan_prox_wave(uot_ctx* c) {
         if (ctas < best) { best = ctas; best_cl = cl; }
     }
     if (!best_cl) return;
+    c->pw.own_lo = 0;
+    c->pw.own_hi = c->P;
     // pair slots per pair (halo pairs + idle slots): C4 320 / 255 = 1.25 runs the wave (1.54e11 vs
     // k_iter 1.29e11 px-it/s); C3 96 / 63 = 1.52 is slower than one pass per iteration (0.87e11 vs
     // 1.08e11), so above 1.34 chain prox stays on k_iter (UOT_PROX_WAVE=2 forces the wave)
     if ((double)best * kWpWarps / ((double)c->B * c->P) > 1.34 && env_int("UOT_PROX_WAVE", 1) != 2) return;
     c->pw.cl = best_cl;
-    c->pw.groups = (c->P + best_cl * kWpWarps - 2 * S - 1) / (best_cl * kWpWarps - 2 * S);
     c->pw.strips = wave_strips(c->nx, S);
+    if (!pw_regroup(c)) return;
+    c->pw.ok = true;
+    if (env_int("UOT_DEBUG", 0))
+        fprintf(stderr, "k_wave_prox plan: S %d cl %d groups %d strips %d segs %d H %d\n",
+                c->pw.S, c->pw.cl, c->pw.groups, c->pw.strips, c->pw.segs, c->pw.H);
+}
+
+// Pair groups over the own pairs [own_lo, own_hi) and the segment height (the wave model with the
+// co-resident clusters the occupancy API reports).
+static bool pw_regroup(uot_ctx* c) {
+    using namespace uotk;
+    const int S = c->pw.S, best_cl = c->pw.cl;
+    const int own = c->pw.own_hi - c->pw.own_lo;
+    c->pw.groups = (own + best_cl * kWpWarps - 2 * S - 1) / (best_cl * kWpWarps - 2 * S);
     // co-resident clusters (one 256-thread CTA per SM; cluster placement may strand SMs)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(best_cl * 64, 1);
     cfg.blockDim = dim3(kWpWarps * 32);
-    cfg.dynamicSmemBytes = sm[0];
+    cfg.dynamicSmemBytes = WpCfg<3>::smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = best_cl; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
@@ -553,7 +571,7 @@ static void plan_prox_wave(uot_ctx* c) {
     int nclus = 0;
     if (cudaOccupancyMaxActiveClusters(&nclus, c->pw.fn[0][0], &cfg) != cudaSuccess || nclus <= 0) {
         cudaGetLastError();
-        return;
+        return false;
     }
     const long long G = (long long)c->B * c->pw.groups * best_cl;     // CTAs per (strip, segment)
     const int hset = env_int("UOT_PROX_WAVE_H", 0);
@@ -574,10 +592,7 @@ static void plan_prox_wave(uot_ctx* c) {
     if (H > c->ny) H = c->ny;
     c->pw.H = H;
     c->pw.segs = (c->ny + H - 1) / H;
-    c->pw.ok = true;
-    if (env_int("UOT_DEBUG", 0))
-        fprintf(stderr, "k_wave_prox plan: S %d cl %d groups %d strips %d segs %d H %d, %d co-resident clusters\n",
-                c->pw.S, c->pw.cl, c->pw.groups, c->pw.strips, c->pw.segs, c->pw.H, nclus);
+    return true;
 }
 
 // Work decomposition of k_iter: strips of
@@ -830,7 +845,8 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
     size_t recs = part_records(c->geo, c->G, c->bpp);
     for (const TVar& v : c->tv)
         if ((size_t)c->G * v.tx * v.ty > recs) recs = (size_t)c->G * v.tx * v.ty;
-    if (c->pw.ok && (size_t)c->G * c->pw.strips * c->pw.segs > recs) recs = (size_t)c->G * c->pw.strips * c->pw.segs;
+    // (16-row segments at most: uot_set_own_pairs may regroup the pairs and re-choose the height)
+    if (c->pw.ok && (size_t)c->G * c->pw.strips * ((p.ny + 15) / 16) > recs) recs = (size_t)c->G * c->pw.strips * ((p.ny + 15) / 16);
     c->part = b.scratch;
     c->pair_it = c->part + recs * kRec;
     c->pair_obj = c->pair_it + (size_t)c->G * kRec;
@@ -1382,6 +1398,7 @@ static int launch_prox_pass(uot_ctx* c, int S, bool red, const int* stop, double
     uotk::WaveProxArgs W{};
     W.nx = c->nx; W.ny = c->ny; W.strips = c->pw.strips; W.segs = c->pw.segs; W.H = c->pw.H;
     W.B = c->B; W.T = c->T; W.P = c->P; W.groups = c->pw.groups; W.cl = c->pw.cl; W.N = c->N;
+    W.own_lo = c->pw.own_lo; W.own_hi = c->pw.own_hi;
     W.p = c->b.frames;
     W.mx_in = c->b.mx[in]; W.my_in = c->b.my[in]; W.a_in = c->b.a[in]; W.r_in = rbuf(c); W.x_in = c->b.x[in];
     W.mx_out = c->b.mx[o]; W.my_out = c->b.my[o]; W.a_out = c->b.a[o];
@@ -1402,6 +1419,20 @@ static int launch_prox_pass(uot_ctx* c, int S, bool red, const int* stop, double
         e1 = c->ev[c->ev_used + 1];
         c->ev_used += 2;
         c->ev_kind.push_back(11);
+    }
+    if (red && (c->pw.own_lo > 0 || c->pw.own_hi < c->P)) {
+        // ghost pairs are not reduced: zero their records ([pair][strips * segs][kRec], contiguous
+        // per pair), which the kernel leaves untouched
+        const size_t per = (size_t)c->pw.strips * c->pw.segs * kRec * sizeof(double);
+        for (int b = 0; b < c->B; ++b) {
+            double* base = c->part + (size_t)b * c->P * c->pw.strips * c->pw.segs * kRec;
+            cudaError_t me = cudaSuccess;
+            if (c->pw.own_lo > 0) me = cudaMemsetAsync(base, 0, per * c->pw.own_lo, c->s);
+            if (me == cudaSuccess && c->pw.own_hi < c->P)
+                me = cudaMemsetAsync(base + (size_t)c->pw.own_hi * c->pw.strips * c->pw.segs * kRec, 0,
+                                     per * (c->P - c->pw.own_hi), c->s);
+            if (me != cudaSuccess) return fail(c, UOT_E_CUDA, "ghost records: %s", cudaGetErrorString(me));
+        }
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(c->B * c->pw.groups * c->pw.cl), (unsigned)(c->pw.strips * c->pw.segs));
@@ -1510,9 +1541,11 @@ static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, c
         // iterations up to and including the next reduction (or the end of the call)
         int d = n - k;
         if (reduce_every > 0) d = std::min(d, reduce_every - (k % reduce_every));
-        if (c->pw.ok) {                 // chain prox: passes of 3, then 2, then one k_iter
-            const int L = c->pw.S;
-            const int S = d >= L ? L : (d >= 2 ? 2 : 1);
+        if (c->pw.ok) {                 // chain prox: passes of 3 and 2 (one k_iter only for a single iteration)
+            const int L = c->pw.S;         // (3k + 1 ends in 2 + 2: no one-iteration pass)
+            const int S = d == L + 1 ? 2 : (d >= L ? L : (d >= 2 ? 2 : 1));
+            if (S == 1 && (c->pw.own_lo > 0 || c->pw.own_hi < c->P))   // k_iter would update the ghost pairs
+                return fail(c, UOT_E_INVALID, "ghost pairs set (uot_set_own_pairs): iterate in runs of 2..%d between checks", L);
             const int rc = S == 1 ? launch_one(c, UOT_PART_ALL, need_red(k), stop, tol)
                                   : launch_prox_pass(c, S, need_red(k + S - 1), stop, tol);
             k += S;
@@ -1830,6 +1863,23 @@ int uot_kernel_path(const uot_ctx* c) {
     const TVar& v = c->tv[four ? 1 : 0];
     if (v.wave && four && c->tv[3].ok) return 9;        // the pass kind of long runs: five per pass
     return v.wave ? (four ? 6 : 5) : (four ? 3 : 1);
+}
+
+int uot_set_own_pairs(uot_ctx* c, int32_t lo, int32_t hi) {
+    if (!c) return fail(nullptr, UOT_E_INVALID, "ctx is NULL");
+    if (!c->pw.ok) return fail(c, UOT_E_INVALID, "ghost pairs need the chain-prox wave path (uot_kernel_path 11)");
+    if (!(0 <= lo && lo < hi && hi <= c->P)) return fail(c, UOT_E_INVALID, "own pairs [%d, %d) outside [0, %d)", lo, hi, c->P);
+    int prc = resolve_pending(c);
+    if (prc) return prc;
+    const int olo = c->pw.own_lo, ohi = c->pw.own_hi;
+    c->pw.own_lo = lo;
+    c->pw.own_hi = hi;
+    if (!pw_regroup(c)) {
+        c->pw.own_lo = olo; c->pw.own_hi = ohi;
+        pw_regroup(c);
+        return fail(c, UOT_E_CUDA, "k_wave_prox regroup failed");
+    }
+    return UOT_OK;
 }
 
 int uot_set_temporal(uot_ctx* c, int enable) {

@@ -54,6 +54,8 @@ struct WaveProxArgs {
     int nx, ny, strips, segs, H;
     int B, T, P;                    // chains, frames and pairs per chain
     int groups, cl;                 // pair groups per chain, CTAs per cluster
+    int own_lo, own_hi;             // pairs [own_lo, own_hi) of each chain are written; the others are
+                                    // ghost pairs (a sharded chain's copies of its neighbours' pairs)
     long long N;
     const float* p;                 // [B][T][N] prox centres
     const float* mx_in; const float* my_in; const float* a_in; const float* r_in; const float* x_in;
@@ -114,7 +116,8 @@ __global__ void __launch_bounds__(kWpWarps * 32, 1) k_wave_prox(const WaveProxAr
     const int b = grp / A.groups, g = grp - b * A.groups;
     const int u = blockIdx.y, sy = u / A.strips, sx = u - sy * A.strips;
     const int Pc = A.P;
-    const int lo = (int)((long long)g * Pc / A.groups), hi = (int)((long long)(g + 1) * Pc / A.groups);
+    const int own = A.own_hi - A.own_lo;
+    const int lo = A.own_lo + (int)((long long)g * own / A.groups), hi = A.own_lo + (int)((long long)(g + 1) * own / A.groups);
     const int q = rank * kWpWarps + w;                            // slot in the group
     const int t = lo - S + q;                                     // pair of this warp
     const bool exists = t >= 0 && t < Pc && t < hi + S;
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 1) k_wave_prox(const WaveProxAr
     const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1, rsc = A.r_scale;
     const float2 c1 = pk_dup(A.c1), c2 = pk_dup(A.c2), nc3 = pk_dup(-A.c3);
     const bool fix0 = A.fix_first && t == 0;                      // constant first frame
-    const bool own_last = t == Pc - 1;                            // also owns frame T-1 (writes, reductions)
+    const bool own_last = t == Pc - 1 && A.own_hi == Pc;          // also owns frame T-1 (writes, reductions)
     const float2 nt1 = pk_dup(-t1), nt1h = make_float2(-t1, last_q ? 0.f : -t1);
 
     float4* sring = wpsm + (size_t)w * (C::warp_floats / 4) + lane;        // [slot][6][lane]

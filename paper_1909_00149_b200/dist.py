@@ -268,3 +268,100 @@ class ShardedRPCA:
             rep["objective"] = rep["data_term"] + rep["l1_term"] + p._p.gamma * rep["nuclear"] + \
                 p._p.kappa * (rep["transport"] + rep["growth"])
         return rep
+
+
+# ----------------------------------------------------------------------------- ghost pairs
+def ghost_range(n_pairs: int, world: int, rank: int, S: int = 3):
+    """Chain prox with ghost pairs: rank owns pairs [p0, p1) (shard_range) and holds pairs
+    [q0, q1) = [p0 - S, p1 + S) clipped to the chain (frames q0 .. q1) in its context."""
+    p0, p1 = shard_range(n_pairs, world, rank)
+    return p0, p1, max(0, p0 - S), min(n_pairs, p1 + S)
+
+
+def ghost_planes(prob):
+    """The current state planes of a Problem: [mx, my, r, a] ([B][P][ny][nx]) and x ([B][T][ny][nx])."""
+    st = prob.state()
+    return [st["mx"], st["my"], st["r"], st["a"]], st["x"]
+
+
+class GhostChain:
+    """Chain prox (rho < inf) over frame-range shards with S GHOST pairs per shared side, on the
+    temporally blocked kernel (k_wave_prox, DESIGN.md §6/§8).
+
+    Rank r owns pairs [p0, p1) and keeps copies of the S pairs (and S + 1 frames) on each side
+    that a pass of S iterations reads (the dependency cone: after S iterations a pair is exact
+    iff its S neighbours on both sides were); `uot_set_own_pairs` makes the kernel write and
+    reduce only the own pairs.  After every pass the shards swap their S boundary pairs' full
+    state (M, r, a and the frames x): 4 S planes + S (+1) frames per side every S iterations,
+    instead of one dual plane per iteration (ShardedChain).  NCCL P2P (gloo through host copies
+    in the CPU tests); the reports of checked passes are summed over ranks.  tol = 0 only.
+    """
+
+    def __init__(self, prob, n_pairs: int, rank: int = 0, world: int = 1, group=None, S: int = 3):
+        self.prob, self.rank, self.world, self.group, self.S = prob, rank, world, group, S
+        self.p0, self.p1, self.q0, self.q1 = ghost_range(n_pairs, world, rank, S)
+        if prob.P != self.q1 - self.q0:
+            raise ValueError(f"context holds {prob.P} pairs, the ghost range [{self.q0}, {self.q1}) needs "
+                             f"{self.q1 - self.q0}")
+        if world > 1:
+            prob.set_own_pairs(self.p0 - self.q0, self.p1 - self.q0)
+
+    def exchange(self):
+        """Swap the boundary pairs' state with the neighbours (after a pass)."""
+        if self.world == 1:
+            return
+        S, lo, hi = self.S, self.p0 - self.q0, self.p1 - self.q0
+        planes, x = ghost_planes(self.prob)
+        sends, recvs = [], []
+        if self.rank > 0:       # own pairs [lo, lo+S) and frames [lo, lo+S] -> left; ghosts [0, S), frames [0, S) <- left
+            for t in planes:
+                sends.append((t[:, lo:lo + S].contiguous(), self.rank - 1))
+                recvs.append((t[:, 0:S], self.rank - 1))
+            sends.append((x[:, lo:lo + S + 1].contiguous(), self.rank - 1))
+            recvs.append((x[:, 0:S], self.rank - 1))
+        if self.rank < self.world - 1:   # own pairs [hi-S, hi), frames [hi-S, hi) -> right; ghosts, frames [hi, hi+S] <- right
+            for t in planes:
+                sends.append((t[:, hi - S:hi].contiguous(), self.rank + 1))
+                recvs.append((t[:, hi:hi + S], self.rank + 1))
+            sends.append((x[:, hi - S:hi].contiguous(), self.rank + 1))
+            recvs.append((x[:, hi:hi + S + 1], self.rank + 1))
+        bufs = [(torch.empty_like(dst), dst) for dst, _ in recvs]
+        works = _p2p(sends, [(b, peer) for (b, _), (_, peer) in zip(bufs, recvs)], self.group)
+        for w in works:
+            w.wait()
+        for b, dst in bufs:
+            dst.copy_(b)
+
+    def passes(self, n_iters: int, check_every: int = 0):
+        """The pass lengths of a run: each stretch up to a checked iteration split into passes of
+        S = 3 and 2 (a one-iteration stretch cannot be run on ghost pairs)."""
+        out, k = [], 0
+        while k < n_iters:
+            d = n_iters - k
+            if check_every:
+                d = min(d, check_every - k % check_every)
+            if d == 1:
+                raise ValueError("ghost-pair runs need stretches of >= 2 iterations between checks")
+            n3, r = divmod(d, 3)
+            seg = [3] * n3 + ([2] if r == 2 else [])
+            if r == 1:                                  # 3k + 1 = 3(k - 1) + 2 + 2
+                seg = [3] * (n3 - 1) + [2, 2]
+            out += [(s, i == len(seg) - 1) for i, s in enumerate(seg)]
+            k += d
+        return out
+
+    def run(self, n_iters: int, check_every: int = 0, tol: float = 0.0):
+        """n_iters iterations as passes of 3 / 2 with an exchange after each; reductions on the
+        checked passes; returns the last checked pass's report summed over ranks."""
+        if tol > 0:
+            raise ValueError("GhostChain: tol = 0 only (fixed iteration counts)")
+        for s, checked in self.passes(n_iters, check_every):
+            if checked:
+                self.prob.iterate(s, check_every=s)      # reductions of its last iteration
+            else:
+                self.prob.step(s)                         # no reductions
+            self.exchange()
+        rep = self.prob.report()
+        if self.world > 1:
+            rep = all_reduce_report(rep, self.prob.frames.device, group=self.group)
+        return rep

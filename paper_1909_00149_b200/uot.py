@@ -226,6 +226,12 @@ class Problem:
         iterations per pass), 'k_wave2' / 'k_wave4' (register wavefront) or 'k_persist'."""
         return self.PATH_NAMES[int(lib().uot_kernel_path(self._ctx))]
 
+    def set_own_pairs(self, lo: int, hi: int):
+        """Chain prox on k_wave_prox: only pairs [lo, hi) are written and reduced; the others are
+        ghost copies of neighbouring shards' pairs, refreshed by the caller after each pass
+        (include/uot.h uot_set_own_pairs; dist.GhostChain)."""
+        check(lib().uot_set_own_pairs(self._ctx, int(lo), int(hi)), self._ctx)
+
     def set_temporal(self, enable: bool = True):
         """Fixed marginals: two iterations per HBM pass (k_iter2, default) or one (k_iter)."""
         check(lib().uot_set_temporal(self._ctx, int(bool(enable))), self._ctx)

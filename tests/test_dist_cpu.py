@@ -68,3 +68,59 @@ def test_gloo_boundary_exchange(world, T):
     mp.spawn(_worker, args=(world, _free_port(), T, out), nprocs=world, join=True)
     for r in range(world):
         assert out[r] == (True, True, True, True), (r, out[r])
+
+
+class _StubProb:
+    """The parts of uot.Problem that dist.GhostChain touches, on CPU tensors: the state of the
+    ghost range of a chain whose every value encodes (plane, chain, pair / frame)."""
+
+    def __init__(self, B, q0, q1, ny=2, nx=4):
+        P = q1 - q0
+        self.P = P
+        self.frames = torch.zeros(B, P + 1, ny, nx)
+        self.own = None
+        idx = torch.arange(q0, q1, dtype=torch.float32).view(1, P, 1, 1)
+        b = torch.arange(B, dtype=torch.float32).view(B, 1, 1, 1)
+        self.planes = {k: (1000 * (i + 1) + 100 * b + idx).expand(B, P, ny, nx).clone() for i, k in
+                       enumerate(("mx", "my", "r", "a"))}
+        fidx = torch.arange(q0, q1 + 1, dtype=torch.float32).view(1, P + 1, 1, 1)
+        self.planes["x"] = (9000 + 100 * b + fidx).expand(B, P + 1, ny, nx).clone()
+
+    def set_own_pairs(self, lo, hi):
+        self.own = (lo, hi)
+
+    def state(self):
+        return self.planes
+
+
+def _ghost_worker(rank, world, port, n_pairs, B, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1909_00149_b200.dist import GhostChain, ghost_range
+    p0, p1, q0, q1 = ghost_range(n_pairs, world, rank)
+    prob = _StubProb(B, q0, q1)
+    # ghosts start as garbage: the exchange must fill them with the neighbours' own values
+    for k, t in prob.planes.items():
+        lo, hi = p0 - q0, p1 - q0
+        t[:, :lo] = -1.0
+        t[:, (hi + 1 if k == "x" else hi):] = -1.0
+    gc = GhostChain(prob, n_pairs, rank, world)
+    gc.exchange()
+    ok = prob.own == ((p0 - q0, p1 - q0) if world > 1 else None)
+    exp = _StubProb(B, q0, q1).planes
+    for k in prob.planes:
+        ok = ok and torch.equal(prob.planes[k], exp[k])
+    out[rank] = ok
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_pairs,B", [(2, 19, 1), (3, 25, 2)])
+def test_gloo_ghost_pair_exchange(world, n_pairs, B):
+    """dist.GhostChain.exchange fills every shard's ghost pairs (3 per shared side) and ghost
+    frames with the neighbours' own values (world 2 / 3, gloo); own values are untouched."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_ghost_worker, args=(world, _free_port(), n_pairs, B, out), nprocs=world, join=True)
+    for r in range(world):
+        assert out[r] is True, r

@@ -189,18 +189,19 @@ def test_sharded_rpca_world2_bitwise(n, check, eps):
             assert np.array_equal(st[key], fs[key][p0:p1]), key
 
 
-@pytest.mark.parametrize("mode", ["fixed", "prox"])
-def test_bench_two_ranks_functional(mode):
+@pytest.mark.parametrize("mode,shard", [("fixed", "ghost"), ("prox", "ghost"), ("prox", "halo")])
+def test_bench_two_ranks_functional(mode, shard):
     """`bench.py --gpus 2` without a launcher re-launches itself as 2 ranks (torch.distributed.run);
     with --dist-backend gloo both share this GPU (functional check of the N > 1 bench path: frame
-    shards, boundary-frame exchange, global stop, report all-reduce; not a timing).  The job's
-    objective equals the one-rank run's."""
+    shards, boundary-frame exchange, global stop, report all-reduce; chain prox with ghost pairs
+    (dist.GhostChain) or per-iteration boundary duals (dist.ShardedChain); not a timing).  The
+    job's objective equals the one-rank run's."""
     import json
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     base = [sys.executable, os.path.join(root, "bench.py"), "--config", "C3", "--iters", "20", "--steps", "1",
-            "--warmup", "3", "--no-cpu", "--no-e2e", "--mode", mode]
+            "--warmup", "3", "--no-cpu", "--no-e2e", "--mode", mode, "--prox-shard", shard]
     env = dict(os.environ, UOT_TPERSIST="0", UOT_PERSIST="0")
     one = subprocess.run(base, capture_output=True, text=True, timeout=600, env=env)
     two = subprocess.run(base + ["--gpus", "2", "--dist-backend", "gloo"], capture_output=True, text=True,
@@ -212,3 +213,61 @@ def test_bench_two_ranks_functional(mode):
     assert l2["n_gpus"] == 2 and l2["iterations_per_step"] == 20
     # (the shards may select other pass kernels than the whole chain: fp32 rounding order only)
     assert l2["objective"] == pytest.approx(l1["objective"], rel=1e-5)
+
+
+# ----------------------------------------------------------------------------- ghost pairs (chain prox)
+def _ghost_worker(rank, world, port, passes, out):
+    import torch.distributed as dist
+    from paper_1909_00149_b200 import dist as udist
+    from paper_1909_00149_b200.uot import Problem
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.update({"UOT_PROX_WAVE": "2", "UOT_PROX_CL": "2"})
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    full = _frames()
+    p0, p1, q0, q1 = udist.ghost_range(T - 1, world, rank)
+    tau = _tau(True)
+    prob = Problem(torch.from_numpy(full[:, q0:q1 + 1]).cuda(), ALPHA, rho=10.0, tau1=tau, tau2=tau)
+    rep = udist.GhostChain(prob, T - 1, rank, world).run(passes, check_every=10)
+    st = {k: v.cpu().numpy() for k, v in prob.state().items()}
+    out[rank] = (p0, p1, q0, st, rep)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ghost_chain_world_bitwise(world):
+    """dist.GhostChain over `world` processes (gloo, one GPU): 3 ghost pairs per shared side,
+    k_wave_prox passes of 3 / 2 iterations (20 = 3 + 3 + 2 + 2 per check of 10), the boundary
+    pairs' state swapped after every pass -- every own pair and frame equals the unsharded
+    chain's (the same passes) bitwise; the report is the global one."""
+    n = 20
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    mp.spawn(_ghost_worker, args=(world, _free_port(), n, out), nprocs=world, join=True)
+    # the unsharded chain through the same driver (world 1: the same 3 / 2 passes, no exchange)
+    from paper_1909_00149_b200 import dist as udist
+    from paper_1909_00149_b200.uot import Problem
+    env = {"UOT_PROX_WAVE": "2", "UOT_PROX_CL": "2"}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        fp = _make(Problem, True, _tau(True))
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    full_rep = udist.GhostChain(fp, T - 1, 0, 1).run(n, check_every=10)
+    full_st = {k: v.cpu().numpy() for k, v in fp.state().items()}
+    for r in range(world):
+        p0, p1, q0, st, rep = out[r]
+        for key in ("mx", "my", "r", "a"):
+            assert np.array_equal(st[key][:, p0 - q0:p1 - q0], full_st[key][:, p0:p1]), (key, r)
+        last = p1 + (1 if p1 == T - 1 else 0)
+        assert np.array_equal(st["x"][:, p0 - q0:last - q0], full_st["x"][:, p0:last]), ("x", r)
+        assert rep["iterations"] == full_rep["iterations"] == n
+        for key in ("objective", "transport", "prox_term", "primal_res", "dual_res"):
+            assert rep[key] == pytest.approx(full_rep[key], rel=1e-10), key

@@ -137,3 +137,74 @@ def test_prox_wave_graph_capture(monkeypatch):
     ref, _ = oracle.iterate(fr, 1.0, 4.0, tau, tau, 32)
     errs = _norm_err(fr, prob.state(), ref)
     assert all(v <= 1e-3 for v in errs.values()), errs
+
+
+# ----------------------------------------------------------------------------- ghost pairs
+def _ghost_exchange(shards):
+    """What dist.GhostChain.exchange moves between neighbouring ranks, as device copies between the
+    shards' Problems (one GPU): own boundary pairs (M, r, a) and frames into the neighbours' ghosts."""
+    from paper_1909_00149_b200.dist import ghost_planes
+    for (A, ra), (Bp, rb) in zip(shards[:-1], shards[1:]):
+        S = 3
+        pa, xa = ghost_planes(A)
+        pb, xb = ghost_planes(Bp)
+        hi = ra[1] - ra[2]                      # A's own end, local
+        lo = rb[0] - rb[2]                      # B's own start, local (= S)
+        for ta, tb in zip(pa, pb):
+            tb[:, 0:S].copy_(ta[:, hi - S:hi])
+            ta[:, hi:hi + S].copy_(tb[:, lo:lo + S])
+        xb[:, 0:S].copy_(xa[:, hi - S:hi])
+        xa[:, hi:hi + S + 1].copy_(xb[:, lo:lo + S + 1])
+
+
+@pytest.mark.parametrize("world,B,T", [(2, 1, 20), (3, 2, 26)])
+def test_ghost_pair_shards_equal_unsharded(world, B, T, monkeypatch):
+    """A chain sharded by frame range with 3 ghost pairs per shared side (uot_set_own_pairs),
+    passes of 3 iterations, boundary pairs' state swapped after every pass (dist.GhostChain's
+    exchange, emulated by device copies): every own pair and frame equals the unsharded chain's
+    bitwise, and the shards' reports add up to the unsharded one."""
+    from paper_1909_00149_b200.dist import ghost_range
+    fr = inputs.gen_random(B, T, 20, 128, seed=T, kind="sparse")
+    tau = oracle.default_steps(128, 20, prox=True, n_frames=T, safety=0.95)[0]
+    alpha, rho, passes = 1.1, 4.0, 7
+    monkeypatch.setenv("UOT_PROX_WAVE", "2")
+    monkeypatch.setenv("UOT_PROX_CL", "2")
+    t = torch.from_numpy(fr).cuda()
+    full = Problem(t, alpha, rho=rho, tau1=tau, tau2=tau)
+    shards = []
+    for r in range(world):
+        p0, p1, q0, q1 = ghost_range(T - 1, world, r)
+        pr = Problem(t[:, q0:q1 + 1].contiguous(), alpha, rho=rho, tau1=tau, tau2=tau)
+        pr.set_own_pairs(p0 - q0, p1 - q0)
+        shards.append((pr, (p0, p1, q0, q1)))
+    for k in range(passes):
+        full.iterate(3, check_every=3)
+        for pr, _ in shards:
+            pr.iterate(3, check_every=3)
+        _ghost_exchange(shards)
+    fs = full.state()
+    reps = [pr.report() for pr, _ in shards]
+    for (pr, (p0, p1, q0, q1)) in shards:
+        st = pr.state()
+        for key in ("mx", "my", "r", "a"):
+            assert torch.equal(st[key][:, p0 - q0:p1 - q0], fs[key][:, p0:p1]), (key, p0, p1)
+        last = p1 + (1 if p1 == T - 1 else 0)
+        assert torch.equal(st["x"][:, p0 - q0:last - q0], fs["x"][:, p0:last]), ("x", p0, p1)
+    rf = full.report()
+    for key in ("objective", "transport", "growth", "prox_term", "upper_bound"):
+        assert sum(r[key] for r in reps) == pytest.approx(rf[key], rel=1e-12), key
+    for key in ("primal_res", "dual_res"):
+        assert math.sqrt(sum(r[key] ** 2 for r in reps)) == pytest.approx(rf[key], rel=1e-10), key
+    assert all(r["iterations"] == rf["iterations"] == 3 * passes for r in reps)
+
+
+def test_ghost_pairs_reject_single_iteration_runs(monkeypatch):
+    fr = inputs.gen_random(1, 14, 12, 64, seed=2, kind="sparse")
+    monkeypatch.setenv("UOT_PROX_WAVE", "2")
+    p = Problem(torch.from_numpy(fr).cuda(), 1.0, rho=2.0)
+    p.set_own_pairs(3, 10)
+    from paper_1909_00149_b200._lib import UotError
+    with pytest.raises(UotError):
+        p.iterate(1, check_every=0)        # a single iteration would be a k_iter pass
+    with pytest.raises(UotError):
+        p.set_own_pairs(5, 14)             # outside the context's 13 pairs
