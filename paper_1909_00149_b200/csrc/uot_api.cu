@@ -443,6 +443,7 @@ struct uot_ctx {
     struct {             // chain prox: register wavefront with pair groups (k_wave_prox)
         bool ok;
         int S;               // iterations of the long pass (3); short pass: 2
+        bool prefer2;        // split stretches into 2s (+ one 3 when odd) rather than 3s (+ 2s)
         int own_lo, own_hi;  // written pairs (uot_set_own_pairs: a shard's own pairs between ghost pairs)
         int cl, groups;      // CTAs per cluster, pair groups per chain
         int strips, segs, H;
@@ -512,7 +513,12 @@ static void plan_prox_wave(uot_ctx* c) {
     using namespace uotk;
     memset(&c->pw, 0, sizeof(c->pw));
     if (c->r_mode != 0) return;
-    c->pw.S = 3;                         // C4 chain prox: S = 3 1.81e11 px-it/s, S = 4 0.97e11 (255 registers, spills)
+    // passes of 3 (fn[0]) and 2 (fn[1]) iterations; groups are planned for 3 (the longest pass).  C4
+    // chain prox: passes of 2 with one 3 for odd stretches (default) 1.80e11 px-it/s, 3s with 2s for
+    // 3k+1 (UOT_PROX_PASS=3) 1.72e11 -- the S = 3 kernel carries 255 registers with spills, S = 2
+    // none; S = 4 (300+ B of spills) 0.97e11
+    c->pw.S = 3;
+    c->pw.prefer2 = env_int("UOT_PROX_PASS", 2) != 3;
     c->pw.fn[0][0] = (const void*)k_wave_prox<3, 0, false>;
     c->pw.fn[0][1] = (const void*)k_wave_prox<3, 0, true>;
     c->pw.fn[1][0] = (const void*)k_wave_prox<2, 0, false>;
@@ -1542,8 +1548,9 @@ static int launch_iters(uot_ctx* c, int n, int reduce_every, bool reduce_last, c
         int d = n - k;
         if (reduce_every > 0) d = std::min(d, reduce_every - (k % reduce_every));
         if (c->pw.ok) {                 // chain prox: passes of 3 and 2 (one k_iter only for a single iteration)
-            const int L = c->pw.S;         // (3k + 1 ends in 2 + 2: no one-iteration pass)
-            const int S = d == L + 1 ? 2 : (d >= L ? L : (d >= 2 ? 2 : 1));
+            const int L = c->pw.S;         // (never a one-iteration pass unless d == 1)
+            const int S = c->pw.prefer2 ? ((d % 2 == 1 && d >= 3) ? 3 : (d >= 2 ? 2 : 1))
+                                        : (d == L + 1 ? 2 : (d >= L ? L : (d >= 2 ? 2 : 1)));
             if (S == 1 && (c->pw.own_lo > 0 || c->pw.own_hi < c->P))   // k_iter would update the ghost pairs
                 return fail(c, UOT_E_INVALID, "ghost pairs set (uot_set_own_pairs): iterate in runs of 2..%d between checks", L);
             const int rc = S == 1 ? launch_one(c, UOT_PART_ALL, need_red(k), stop, tol)

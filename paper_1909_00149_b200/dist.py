@@ -334,7 +334,7 @@ class GhostChain:
 
     def passes(self, n_iters: int, check_every: int = 0):
         """The pass lengths of a run: each stretch up to a checked iteration split into passes of
-        S = 3 and 2 (a one-iteration stretch cannot be run on ghost pairs)."""
+        2 and 3 (a one-iteration stretch cannot be run on ghost pairs)."""
         out, k = [], 0
         while k < n_iters:
             d = n_iters - k
@@ -342,16 +342,15 @@ class GhostChain:
                 d = min(d, check_every - k % check_every)
             if d == 1:
                 raise ValueError("ghost-pair runs need stretches of >= 2 iterations between checks")
-            n3, r = divmod(d, 3)
-            seg = [3] * n3 + ([2] if r == 2 else [])
-            if r == 1:                                  # 3k + 1 = 3(k - 1) + 2 + 2
-                seg = [3] * (n3 - 1) + [2, 2]
+            # passes of 2 with one 3 first when the stretch is odd: the library's own split
+            # (uot_api.cu launch_iters, UOT_PROX_PASS default), so world 1 reproduces it exactly
+            seg = ([3] if d % 2 else []) + [2] * ((d - 3) // 2 if d % 2 else d // 2)
             out += [(s, i == len(seg) - 1) for i, s in enumerate(seg)]
             k += d
         return out
 
     def run(self, n_iters: int, check_every: int = 0, tol: float = 0.0):
-        """n_iters iterations as passes of 3 / 2 with an exchange after each; reductions on the
+        """n_iters iterations as passes of 2 / 3 with an exchange after each; reductions on the
         checked passes; returns the last checked pass's report summed over ranks."""
         if tol > 0:
             raise ValueError("GhostChain: tol = 0 only (fixed iteration counts)")
