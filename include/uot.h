@@ -230,6 +230,14 @@ int uot_set_temporal(uot_ctx* ctx, int enable);
  * with two-iteration passes / k_iter where a reduction falls inside four iterations. */
 int uot_kernel_path(const uot_ctx* ctx);
 
+/* Strip width of the register-wavefront passes (kernel paths 5 / 6 / 7 / 9; the five-iteration
+ * pass's layout): 128 = k_wave_pk / k_wave (one float4 column quad per lane), 64 = k_wave_n (one
+ * fp32x2 column pair per lane, twice the resident warps; chosen per grid where the narrower
+ * strips compute fewer halo pixels, e.g. 256-column rows -- DESIGN.md §6; UOT_WAVE_V = 2 / 4
+ * forces either), 0 when the context has no wavefront passes, -1 for a NULL context.  Iterates
+ * are equal either way (same arithmetic per pixel). */
+int uot_wave_cols(const uot_ctx* ctx);
+
 /* Ghost pairs of a chain-prox shard: only pairs [lo, hi) of each chain are written
  * and reduced by k_wave_prox passes; pairs outside are read-only copies of the neighbouring
  * shards' pairs (with their frames), which the caller refreshes after every pass -- S

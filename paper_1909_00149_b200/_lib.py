@@ -26,7 +26,7 @@ UOT_PART_ALL, UOT_PART_INTERIOR, UOT_PART_BOUNDARY = 0, 1, 2
 EXPORTED = ("uot_scratch_doubles", "uot_default_steps", "uot_create", "uot_reset", "uot_load_frames",
             "uot_iterate", "uot_iterate_part", "uot_get_report", "uot_prox_step", "uot_solve", "uot_objective", "uot_set_timing", "uot_get_timing",
             "uot_get_timing_paths",
-            "uot_state_slot", "uot_r_slot", "uot_set_temporal", "uot_kernel_path", "uot_set_own_pairs", "uot_launch_count",
+            "uot_state_slot", "uot_r_slot", "uot_set_temporal", "uot_kernel_path", "uot_wave_cols", "uot_set_own_pairs", "uot_launch_count",
             "uot_stop_external", "uot_stop_pack", "uot_stop_apply",
             "uot_destroy", "uot_last_error",
             "uot_df_scratch_doubles", "uot_df_create", "uot_df_reset", "uot_df_solve", "uot_df_set_timing",
@@ -161,6 +161,7 @@ def lib():
     L.uot_r_slot.argtypes = [ctypes.c_void_p]; L.uot_r_slot.restype = ctypes.c_int
     L.uot_set_temporal.argtypes = [ctypes.c_void_p, ctypes.c_int]; L.uot_set_temporal.restype = ctypes.c_int
     L.uot_kernel_path.argtypes = [ctypes.c_void_p]; L.uot_kernel_path.restype = ctypes.c_int
+    L.uot_wave_cols.argtypes = [ctypes.c_void_p]; L.uot_wave_cols.restype = ctypes.c_int
     L.uot_set_own_pairs.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
     L.uot_set_own_pairs.restype = ctypes.c_int
     L.uot_launch_count.argtypes = [ctypes.c_void_p]; L.uot_launch_count.restype = ctypes.c_int64

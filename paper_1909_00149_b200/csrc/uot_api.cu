@@ -23,6 +23,7 @@
 #include "uot_temporal.cuh"
 #include "uot_wave.cuh"
 #include "uot_wave_pk.cuh"
+#include "uot_wave_n.cuh"
 #include "uot_wave_prox.cuh"
 
 using namespace uotk;
@@ -65,6 +66,8 @@ struct TVar {
     size_t smem;
     bool ok, tma;
     bool wave;                                 // register wavefront k_wave (tx strips x ty segments of th rows)
+    int vn;                                    // wave: columns per lane (4: k_wave_pk / k_wave, 128-column strips;
+                                               // 2: k_wave_n, 64-column strips)
     const void* fn[2];
     CUtensorMap mx[2], my[2], a[2], r[2], f;   // [G][ny][nx] views, box 72 x rows
 };
@@ -95,7 +98,26 @@ static bool wvar_fill(TVar& v, bool pk) {
     return ok;
 }
 
+// narrow strips: k_wave_n (one fp32x2 column pair per lane, 64 columns per warp)
+template <int S, int RM>
+static bool wvar_fill_n(TVar& v) {
+    using namespace uotk;
+    v.S = S; v.wave = true; v.tma = false; v.threads = 32; v.smem = kWaveNSmem;
+    v.fn[0] = (const void*)k_wave_n<S, RM, false>;
+    v.fn[1] = (const void*)k_wave_n<S, RM, true>;
+    bool ok = true;
+    for (const void* f : v.fn)
+        ok = ok && cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem) == cudaSuccess;
+    return ok;
+}
+
 static bool wvar_select(TVar& v, int S, int rm, bool pk) {
+    if (v.vn == 2) {
+        if (S == 5) return rm == 1 ? wvar_fill_n<5, 1>(v) : (rm == 2 ? wvar_fill_n<5, 2>(v) : wvar_fill_n<5, 0>(v));
+        if (S == 4) return rm == 1 ? wvar_fill_n<4, 1>(v) : (rm == 2 ? wvar_fill_n<4, 2>(v) : wvar_fill_n<4, 0>(v));
+        if (S == 3) return rm == 1 ? wvar_fill_n<3, 1>(v) : (rm == 2 ? wvar_fill_n<3, 2>(v) : wvar_fill_n<3, 0>(v));
+        return rm == 1 ? wvar_fill_n<2, 1>(v) : (rm == 2 ? wvar_fill_n<2, 2>(v) : wvar_fill_n<2, 0>(v));
+    }
     if (S == 5) return rm == 1 ? wvar_fill<5, 1>(v, pk) : (rm == 2 ? wvar_fill<5, 2>(v, pk) : wvar_fill<5, 0>(v, pk));
     if (S == 4) return rm == 1 ? wvar_fill<4, 1>(v, pk) : (rm == 2 ? wvar_fill<4, 2>(v, pk) : wvar_fill<4, 0>(v, pk));
     if (S == 3) return rm == 1 ? wvar_fill<3, 1>(v, pk) : (rm == 2 ? wvar_fill<3, 2>(v, pk) : wvar_fill<3, 0>(v, pk));
@@ -447,6 +469,10 @@ struct uot_ctx {
         int own_lo, own_hi;  // written pairs (uot_set_own_pairs: a shard's own pairs between ghost pairs)
         int cl, groups;      // CTAs per cluster, pair groups per chain
         int strips, segs, H;
+        int strips2;         // strips of the two-iteration pass (its halo: fewer lanes at vn = 2)
+        int vn, warps;       // columns per lane (4: 128-column strips, 8 pairs per CTA; 2: 64-column
+                             // strips, 16 pairs per CTA) and warps per CTA
+        size_t smem[2];      // dynamic shared memory of the long / two-iteration pass
         const void* fn[2][2];  // [long / two-iteration pass][red]
     } pw;
     bool single_on;      // one-CTA k_single for single small pairs (UOT_SINGLE)
@@ -496,6 +522,20 @@ static int wave_height(long long G, int strips, int ny, int S, int resident = 0)
     return std::max(16, bestH);
 }
 
+// Relative cost of a wavefront pass with a given strip layout: whole waves x rows marched x the
+// pixel columns one SM advances per row step (resident warps x columns per warp) / the layout's
+// pixel throughput.  Compares the 128-column strips (k_wave_pk, 8 warps / SM at S >= 4) with the
+// 64-column ones (k_wave_n, 16).  Measured on C3 (63 x 256^2, S = 5): k_wave_n computes 0.86x
+// the pixel-levels of k_wave_pk (5 x 64 vs 3 x 128 columns, 37- vs 43-row segments) but takes
+// 1.13x the time (52.6 vs 46.4 us per pass: twice the cp.async / LDS / SHFL per pixel), so its
+// per-pixel throughput is 0.76 of k_wave_pk's (kWaveNEff); it wins only on rows where the quad
+// strips waste much more, e.g. 136 columns (2 x 128 vs 3 x 64).
+constexpr double kWaveNEff = 0.76;
+static double wave_cost(long long G, int strips, int ny, int H, int S, int resident, int cols, double eff) {
+    const long long wave = (long long)kSMs * resident;
+    const long long units = G * strips * (long long)((ny + H - 1) / H);
+    return (double)((units + wave - 1) / wave) * (H + 2 * S) * resident * cols / eff;
+}
 
 static int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
@@ -519,14 +559,38 @@ static void plan_prox_wave(uot_ctx* c) {
     // none; S = 4 (300+ B of spills) 0.97e11
     c->pw.S = 3;
     c->pw.prefer2 = env_int("UOT_PROX_PASS", 2) != 3;
-    c->pw.fn[0][0] = (const void*)k_wave_prox<3, 0, false>;
-    c->pw.fn[0][1] = (const void*)k_wave_prox<3, 0, true>;
-    c->pw.fn[1][0] = (const void*)k_wave_prox<2, 0, false>;
-    c->pw.fn[1][1] = (const void*)k_wave_prox<2, 0, true>;
-    const size_t sm[2] = {WpCfg<3>::smem, WpCfg<2>::smem};
+    // lane layout: 128-column strips with 8 pairs per CTA (default) or 64-column strips with 12 / 16
+    // (UOT_PROX_V=2, UOT_PROX_W=12 / 16: fewer registers per warp, more warps per SM).  Measured on C4
+    // chain prox (passes of 2): V4 x 8 1.79e11 px-it/s, V2 x 12 1.54e11, V2 x 16 (128-register cap,
+    // spills) 1.20e11 -- more resident warps do not pay for twice the per-pixel cp.async / LDS /
+    // st.async / SHFL traffic
+    c->pw.vn = env_int("UOT_PROX_V", 4) == 2 ? 2 : 4;
+    const int nw_env = env_int("UOT_PROX_W", 12);
+    if (c->pw.vn == 2 && nw_env == 16) {
+        c->pw.warps = 16;
+        c->pw.fn[0][0] = (const void*)k_wave_prox<3, 0, false, 2, 16>;
+        c->pw.fn[0][1] = (const void*)k_wave_prox<3, 0, true, 2, 16>;
+        c->pw.fn[1][0] = (const void*)k_wave_prox<2, 0, false, 2, 16>;
+        c->pw.fn[1][1] = (const void*)k_wave_prox<2, 0, true, 2, 16>;
+        c->pw.smem[0] = WpCfg<3, 2, 16>::smem; c->pw.smem[1] = WpCfg<2, 2, 16>::smem;
+    } else if (c->pw.vn == 2) {
+        c->pw.warps = 12;
+        c->pw.fn[0][0] = (const void*)k_wave_prox<3, 0, false, 2, 12>;
+        c->pw.fn[0][1] = (const void*)k_wave_prox<3, 0, true, 2, 12>;
+        c->pw.fn[1][0] = (const void*)k_wave_prox<2, 0, false, 2, 12>;
+        c->pw.fn[1][1] = (const void*)k_wave_prox<2, 0, true, 2, 12>;
+        c->pw.smem[0] = WpCfg<3, 2, 12>::smem; c->pw.smem[1] = WpCfg<2, 2, 12>::smem;
+    } else {
+        c->pw.warps = 8;
+        c->pw.fn[0][0] = (const void*)k_wave_prox<3, 0, false, 4>;
+        c->pw.fn[0][1] = (const void*)k_wave_prox<3, 0, true, 4>;
+        c->pw.fn[1][0] = (const void*)k_wave_prox<2, 0, false, 4>;
+        c->pw.fn[1][1] = (const void*)k_wave_prox<2, 0, true, 4>;
+        c->pw.smem[0] = WpCfg<3, 4>::smem; c->pw.smem[1] = WpCfg<2, 4>::smem;
+    }
     for (int k = 0; k < 2; ++k)
         for (int red = 0; red < 2; ++red)
-            if (cudaFuncSetAttribute(c->pw.fn[k][red], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm[k]) != cudaSuccess) {
+            if (cudaFuncSetAttribute(c->pw.fn[k][red], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->pw.smem[k]) != cudaSuccess) {
                 cudaGetLastError();
                 return;
             }
@@ -536,7 +600,7 @@ static void plan_prox_wave(uot_ctx* c) {
     const int clenv = env_int("UOT_PROX_CL", 0);
     for (int cl = 1; cl <= 8; cl *= 2) {
         if (clenv > 0 && cl != clenv) continue;
-        const int V = cl * kWpWarps - 2 * S;
+        const int V = cl * c->pw.warps - 2 * S;
         if (V <= 0) continue;
         const long long ctas = (long long)c->B * ((c->P + V - 1) / V) * cl;
         if (ctas < best) { best = ctas; best_cl = cl; }
@@ -547,14 +611,15 @@ static void plan_prox_wave(uot_ctx* c) {
     // pair slots per pair (halo pairs + idle slots): C4 320 / 255 = 1.25 runs the wave (1.54e11 vs
     // k_iter 1.29e11 px-it/s); C3 96 / 63 = 1.52 is slower than one pass per iteration (0.87e11 vs
     // 1.08e11), so above 1.34 chain prox stays on k_iter (UOT_PROX_WAVE=2 forces the wave)
-    if ((double)best * kWpWarps / ((double)c->B * c->P) > 1.34 && env_int("UOT_PROX_WAVE", 1) != 2) return;
+    if ((double)best * c->pw.warps / ((double)c->B * c->P) > 1.34 && env_int("UOT_PROX_WAVE", 1) != 2) return;
     c->pw.cl = best_cl;
-    c->pw.strips = wave_strips(c->nx, S);
+    c->pw.strips = wp_strips(c->nx, S, c->pw.vn);
+    c->pw.strips2 = wp_strips(c->nx, 2, c->pw.vn);
     if (!pw_regroup(c)) return;
     c->pw.ok = true;
     if (env_int("UOT_DEBUG", 0))
-        fprintf(stderr, "k_wave_prox plan: S %d cl %d groups %d strips %d segs %d H %d\n",
-                c->pw.S, c->pw.cl, c->pw.groups, c->pw.strips, c->pw.segs, c->pw.H);
+        fprintf(stderr, "k_wave_prox plan: S %d V %d cl %d groups %d strips %d segs %d H %d\n",
+                c->pw.S, c->pw.vn, c->pw.cl, c->pw.groups, c->pw.strips, c->pw.segs, c->pw.H);
 }
 
 // Pair groups over the own pairs [own_lo, own_hi) and the segment height (the wave model with the
@@ -563,12 +628,13 @@ static bool pw_regroup(uot_ctx* c) {
     using namespace uotk;
     const int S = c->pw.S, best_cl = c->pw.cl;
     const int own = c->pw.own_hi - c->pw.own_lo;
-    c->pw.groups = (own + best_cl * kWpWarps - 2 * S - 1) / (best_cl * kWpWarps - 2 * S);
+    const int NW = c->pw.warps;
+    c->pw.groups = (own + best_cl * NW - 2 * S - 1) / (best_cl * NW - 2 * S);
     // co-resident clusters (one 256-thread CTA per SM; cluster placement may strand SMs)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(best_cl * 64, 1);
-    cfg.blockDim = dim3(kWpWarps * 32);
-    cfg.dynamicSmemBytes = WpCfg<3>::smem;
+    cfg.blockDim = dim3(NW * 32);
+    cfg.dynamicSmemBytes = c->pw.smem[0];
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = best_cl; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
@@ -832,12 +898,25 @@ int uot_create(const uot_params* prm, const uot_buffers* buf, void* stream, uot_
                       (wenv_wave >= 0 ? wenv_wave != 0
                                       : (long long)c->G * strips * ((p.ny + wave_h - 1) / wave_h) >= (long long)kSMs * 8);
     static const int kVarS[4] = {2, 4, 3, 5};
+    const int wave_v = env_int("UOT_WAVE_V", 0);
+    const bool wave_pk = env_int("UOT_WAVE_PK", 1) != 0;
     for (int k = 0; k < 4; ++k) {
         TVar& v = c->tv[k];
         v.wave = wave;
         if (wave) {
-            v.tx = wave_strips(p.nx, kVarS[k]);
-            v.th = wave_h_env > 0 ? wave_h : wave_height(c->G, v.tx, p.ny, kVarS[k]);
+            const int S = kVarS[k], res4 = S >= 4 ? 8 : 10;
+            v.vn = 4;
+            v.tx = wave_strips(p.nx, S);
+            v.th = wave_h_env > 0 ? wave_h : wave_height(c->G, v.tx, p.ny, S, res4);
+            // 64-column strips (k_wave_n) where they save enough computed halo pixels to pay for
+            // their lower per-pixel throughput (wave_cost); UOT_WAVE_V = 2 / 4 forces
+            const int tx2 = waven_strips(p.nx, S);
+            const int th2 = wave_h_env > 0 ? wave_h : wave_height(c->G, tx2, p.ny, S, kWaveNMinB);
+            const bool narrow = wave_v == 2 ||
+                (wave_v == 0 && wave_pk &&
+                 wave_cost(c->G, tx2, p.ny, th2, S, kWaveNMinB, 64, kWaveNEff) <
+                     wave_cost(c->G, v.tx, p.ny, v.th, S, res4, 128, 1.0));
+            if (narrow) { v.vn = 2; v.tx = tx2; v.th = th2; }
         } else {
             v.tx = (p.nx + kTW - 1) / kTW;
         }
@@ -1401,8 +1480,9 @@ static int launch_pass(uot_ctx* c, int vi, bool red, const int* stop, double tol
 // clusters of pw.cl CTAs; iterations iter+1 .. iter+S, reductions (red) for iteration iter+S.
 static int launch_prox_pass(uot_ctx* c, int S, bool red, const int* stop, double tol) {
     const int in = c->slot, o = in ^ 1;
+    const int strips = S == 2 ? c->pw.strips2 : c->pw.strips;    // the pass's own halo (lanes per side)
     uotk::WaveProxArgs W{};
-    W.nx = c->nx; W.ny = c->ny; W.strips = c->pw.strips; W.segs = c->pw.segs; W.H = c->pw.H;
+    W.nx = c->nx; W.ny = c->ny; W.strips = strips; W.segs = c->pw.segs; W.H = c->pw.H;
     W.B = c->B; W.T = c->T; W.P = c->P; W.groups = c->pw.groups; W.cl = c->pw.cl; W.N = c->N;
     W.own_lo = c->pw.own_lo; W.own_hi = c->pw.own_hi;
     W.p = c->b.frames;
@@ -1429,21 +1509,21 @@ static int launch_prox_pass(uot_ctx* c, int S, bool red, const int* stop, double
     if (red && (c->pw.own_lo > 0 || c->pw.own_hi < c->P)) {
         // ghost pairs are not reduced: zero their records ([pair][strips * segs][kRec], contiguous
         // per pair), which the kernel leaves untouched
-        const size_t per = (size_t)c->pw.strips * c->pw.segs * kRec * sizeof(double);
+        const size_t per = (size_t)strips * c->pw.segs * kRec * sizeof(double);
         for (int b = 0; b < c->B; ++b) {
-            double* base = c->part + (size_t)b * c->P * c->pw.strips * c->pw.segs * kRec;
+            double* base = c->part + (size_t)b * c->P * strips * c->pw.segs * kRec;
             cudaError_t me = cudaSuccess;
             if (c->pw.own_lo > 0) me = cudaMemsetAsync(base, 0, per * c->pw.own_lo, c->s);
             if (me == cudaSuccess && c->pw.own_hi < c->P)
-                me = cudaMemsetAsync(base + (size_t)c->pw.own_hi * c->pw.strips * c->pw.segs * kRec, 0,
+                me = cudaMemsetAsync(base + (size_t)c->pw.own_hi * strips * c->pw.segs * kRec, 0,
                                      per * (c->P - c->pw.own_hi), c->s);
             if (me != cudaSuccess) return fail(c, UOT_E_CUDA, "ghost records: %s", cudaGetErrorString(me));
         }
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(c->B * c->pw.groups * c->pw.cl), (unsigned)(c->pw.strips * c->pw.segs));
-    cfg.blockDim = dim3(uotk::kWpWarps * 32);
-    cfg.dynamicSmemBytes = S == 3 ? uotk::WpCfg<3>::smem : uotk::WpCfg<2>::smem;
+    cfg.gridDim = dim3((unsigned)(c->B * c->pw.groups * c->pw.cl), (unsigned)(strips * c->pw.segs));
+    cfg.blockDim = dim3(c->pw.warps * 32);
+    cfg.dynamicSmemBytes = c->pw.smem[S == 2 ? 1 : 0];
     cfg.stream = c->s;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1464,7 +1544,7 @@ static int launch_prox_pass(uot_ctx* c, int S, bool red, const int* stop, double
     log_launch(c);
     if (red) {
         ReduceArgs R{};
-        R.partials = c->part; R.recs_per_pair = c->pw.strips * c->pw.segs; R.G = c->G;
+        R.partials = c->part; R.recs_per_pair = strips * c->pw.segs; R.G = c->G;
         R.pair_out = c->pair_it; R.glob = c->glob; R.counter = c->counter;
         R.stop = const_cast<int*>(stop); R.max_mask = 0u; R.is_iteration = 1; R.is_setup = 0;
         R.iteration = c->iter; R.tol = tol; R.tau1 = c->tau1;
@@ -1854,6 +1934,12 @@ int uot_get_timing_paths(uot_ctx* c, double* ms, int64_t* n) {
     c->ev_used = 0;
     c->ev_kind.clear();
     return UOT_OK;
+}
+
+int uot_wave_cols(const uot_ctx* c) {
+    if (!c) return -1;
+    const TVar& v = c->tv[3];                 // the five-iteration pass (all wave variants share the layout rule)
+    return (c->t2ok && v.ok && v.wave) ? 32 * v.vn : 0;
 }
 
 int uot_state_slot(const uot_ctx* c) { return c ? c->slot : -1; }

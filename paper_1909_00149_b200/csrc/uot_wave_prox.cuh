@@ -37,17 +37,83 @@
 
 namespace uotk {
 
-constexpr int kWpWarps = 8;               // warps (pairs) per CTA
+// Lane layouts: V = 4 columns per lane (one float4 quad, 128-column strips, 8 warps = 8 pairs per
+// CTA; the round-2 kernel) or V = 2 (one fp32x2 pair, 64-column strips, 16 warps per CTA: half
+// the registers per warp, twice the warps per SM for the latency-bound pass).
+// Same arithmetic per pixel either way (the packed ops of k_wave_pk).
+struct Duo { float2 l; };                 // columns (c, c+1) of one lane
+__device__ __forceinline__ Duo qadd(const Duo& a, const Duo& b) { return {pk_add(a.l, b.l)}; }
+__device__ __forceinline__ Duo qsub(const Duo& a, const Duo& b) { return {pk_sub(a.l, b.l)}; }
+__device__ __forceinline__ Duo qmul(const Duo& a, const Duo& b) { return {pk_mul(a.l, b.l)}; }
+__device__ __forceinline__ Duo qfma(float2 s, const Duo& b, const Duo& c) { return {pk_fma(s, b.l, c.l)}; }
+__device__ __forceinline__ Duo qfma(const Duo& a, const Duo& b, const Duo& c) { return {pk_fma(a.l, b.l, c.l)}; }
+__device__ __forceinline__ float qc(const Duo& q, int v) { return v == 0 ? q.l.x : q.l.y; }
+__device__ __forceinline__ Duo qdiff_right(const Duo& q, float right) { return {make_float2(q.l.x - q.l.y, q.l.y - right)}; }
+__device__ __forceinline__ Duo qdiff_left(const Duo& q, float left) { return {make_float2(q.l.x - left, q.l.y - q.l.x)}; }
+
+template <int V> struct WpLane;
+template <> struct WpLane<4> {
+    using T = Quad; using M = float4;
+    __device__ static T ld(const M& m) { return qd(m); }
+    __device__ static M st(const T& t) { return f4(t); }
+    __device__ static T splat(float v) { return qd(make_float4(v, v, v, v)); }
+    __device__ static float first(const T& t) { return t.l.x; }
+    __device__ static float last(const T& t) { return t.h.y; }
+    __device__ static void zero_last(M& m) { m.w = 0.f; }
+    __device__ static T relu(const T& t) {
+        return {make_float2(fmaxf(t.l.x, 0.f), fmaxf(t.l.y, 0.f)), make_float2(fmaxf(t.h.x, 0.f), fmaxf(t.h.y, 0.f))};
+    }
+    __device__ static T clampv(const T& t, float c) {
+        return {make_float2(fminf(fmaxf(t.l.x, -c), c), fminf(fmaxf(t.l.y, -c), c)),
+                make_float2(fminf(fmaxf(t.h.x, -c), c), fminf(fmaxf(t.h.y, -c), c))};
+    }
+    __device__ static T rsq(const T& t) {
+        return {make_float2(rsqrt_ftz(t.l.x), rsqrt_ftz(t.l.y)), make_float2(rsqrt_ftz(t.h.x), rsqrt_ftz(t.h.y))};
+    }
+    // -tau1 per column with the pinned column (the lane's last) scaled by 0 when `pin`
+    __device__ static T nt1x(float nt1, bool pin) { return {pk_dup(nt1), make_float2(nt1, pin ? 0.f : nt1)}; }
+    __device__ static void cp(float* s, const float* g, bool ok) { cp_async16(s, g, ok); }
+    __device__ static void st_if(float* g, const T& v, bool p) { st4_if(g, f4(v), p); }
+};
+template <> struct WpLane<2> {
+    using T = Duo; using M = float2;
+    __device__ static T ld(const M& m) { return {m}; }
+    __device__ static M st(const T& t) { return t.l; }
+    __device__ static T splat(float v) { return {make_float2(v, v)}; }
+    __device__ static float first(const T& t) { return t.l.x; }
+    __device__ static float last(const T& t) { return t.l.y; }
+    __device__ static void zero_last(M& m) { m.y = 0.f; }
+    __device__ static T relu(const T& t) { return {make_float2(fmaxf(t.l.x, 0.f), fmaxf(t.l.y, 0.f))}; }
+    __device__ static T clampv(const T& t, float c) { return {make_float2(fminf(fmaxf(t.l.x, -c), c), fminf(fmaxf(t.l.y, -c), c))}; }
+    __device__ static T rsq(const T& t) { return {make_float2(rsqrt_ftz(t.l.x), rsqrt_ftz(t.l.y))}; }
+    __device__ static T nt1x(float nt1, bool pin) { return {make_float2(nt1, pin ? 0.f : nt1)}; }
+    __device__ static void cp(float* s, const float* g, bool ok) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0) : "memory");
+    }
+    __device__ static void st_if(float* g, const T& v, bool p) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.global.v2.f32 [%0], {%1, %2};\n\t}"
+                     :: "l"(g), "f"(v.l.x), "f"(v.l.y), "r"((int)p));
+    }
+};
+constexpr int kWpWarps = 8;               // warps (pairs) per CTA of the V = 4 kernel
 constexpr int kWpStateRing = 3;           // rows of the state ring (M, r, a, x_t, x_{t+1}): current + 2 ahead
 constexpr int kWpPRing = 8;               // rows of the p ring (p_t, p_{t+1} at the level rows)
-template <int S> struct WpCfg {
+// halo lanes / written columns / strips of a V-column-per-lane strip (32 V columns)
+__host__ __device__ constexpr int wp_halo_lanes(int S, int V) { return (S + V - 1) / V; }
+__host__ __device__ constexpr int wp_out(int S, int V) { return 32 * V - 2 * V * wp_halo_lanes(S, V); }
+__host__ __device__ constexpr int wp_strips(int nx, int S, int V) {
+    return nx <= 32 * V ? 1 : (nx - 32 * V + wp_out(S, V) - 1) / wp_out(S, V) + 1;
+}
+template <int S, int V = 4, int NW = (V == 4 ? 8 : 16)> struct WpCfg {
+    static constexpr int W = NW;                                  // warps (pairs) per CTA
     static constexpr int P = kWpStateRing - 1;                    // rows in flight ahead
     static_assert(S + P + 1 <= kWpPRing, "p ring holds rows rho - S .. rho + P");
-    static constexpr size_t warp_floats = (size_t)(kWpStateRing * 6 + kWpPRing * 2) * 32 * 4;
+    static constexpr size_t warp_floats = (size_t)(kWpStateRing * 6 + kWpPRing * 2) * 32 * V;
     // receive buffers: levels 0 .. S-2 [2 bufs][2 sides][S-1][warp][lane], level S-1 [3 bufs][2 sides][warp][lane],
     // then one dummy slot per warp [warp][lane]
-    static constexpr size_t rb_floats = (size_t)(2 * 2 * (S - 1) + 3 * 2 + 1) * kWpWarps * 32 * 4;
-    static constexpr size_t smem = (warp_floats * kWpWarps + rb_floats) * sizeof(float) + kWpWarps * 2 * 8;
+    static constexpr size_t rb_floats = (size_t)(2 * 2 * (S - 1) + 3 * 2 + 1) * W * 32 * V;
+    static constexpr size_t smem = (warp_floats * W + rb_floats) * sizeof(float) + W * 2 * 8;
 };
 
 struct WaveProxArgs {
@@ -100,12 +166,26 @@ __device__ __forceinline__ void cluster_sync() {       // once per launch: relea
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int S, int RM, bool RED>
-__global__ void __launch_bounds__(kWpWarps * 32, 1) k_wave_prox(const WaveProxArgs A) {
+__device__ __forceinline__ void st_async2(unsigned addr, float2 v, unsigned bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];"
+                 :: "r"(addr), "f"(v.x), "f"(v.y), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_async_v(unsigned addr, float4 v, unsigned bar) { st_async4(addr, v, bar); }
+__device__ __forceinline__ void st_async_v(unsigned addr, float2 v, unsigned bar) { st_async2(addr, v, bar); }
+
+template <int S, int RM, bool RED, int V = 4, int NWT = (V == 4 ? 8 : 16)>
+__global__ void __launch_bounds__(NWT * 32, 1) k_wave_prox(const WaveProxArgs A) {
     static_assert(S >= 2 && S <= 3, "levels per pass (S = 4: 255 registers and spills; shared memory)");
-    using C = WpCfg<S>;
-    constexpr int HL = wave_halo_lanes(S), OUT = wave_out(S), P = C::P;
-    extern __shared__ __align__(16) float4 wpsm[];
+    using C = WpCfg<S, V, NWT>;
+    using L = WpLane<V>;
+    using T = typename L::T;
+    using Mv = typename L::M;
+    constexpr int NW = C::W;                                      // warps (pairs) per CTA
+    constexpr int HL = wp_halo_lanes(S, V), OUT = wp_out(S, V), P = C::P;
+    constexpr int SW = 32 * V;                                    // strip width (columns)
+    constexpr unsigned VB = (unsigned)sizeof(Mv);                 // bytes per lane and row
+    extern __shared__ __align__(16) float4 wpsm_raw[];
+    Mv* const wpsm = reinterpret_cast<Mv*>(wpsm_raw);
     pdl_wait();
     const bool stopped = A.stop != nullptr && *reinterpret_cast<const volatile int*>(A.stop);
     // every CTA of the cluster sees the same flag (set before this launch): uniform exit
@@ -118,76 +198,79 @@ __global__ void __launch_bounds__(kWpWarps * 32, 1) k_wave_prox(const WaveProxAr
     const int Pc = A.P;
     const int own = A.own_hi - A.own_lo;
     const int lo = A.own_lo + (int)((long long)g * own / A.groups), hi = A.own_lo + (int)((long long)(g + 1) * own / A.groups);
-    const int q = rank * kWpWarps + w;                            // slot in the group
+    const int q = rank * NW + w;                                  // slot in the group
     const int t = lo - S + q;                                     // pair of this warp
     const bool exists = t >= 0 && t < Pc && t < hi + S;
     const bool out_pair = t >= lo && t < hi;
-    const bool has_l = q > 0, has_r = q < CL * kWpWarps - 1;      // neighbour slots in the cluster
+    const bool has_l = q > 0, has_r = q < CL * NW - 1;            // neighbour slots in the cluster
     const int nx = A.nx, ny = A.ny;
-    const int gs = sx * OUT, gi = gs + 4 * lane;
+    const int gs = sx * OUT, gi = gs + V * lane;
     const bool lane_in = gi < nx;
-    const bool last_q = gi + 3 == nx - 1;
+    const bool last_q = gi + V - 1 == nx - 1;
     const bool left_edge = lane == 0 && sx == 0;
-    const bool writer = out_pair && lane_in && (lane >= HL || sx == 0) && (lane <= 31 - HL || gs + 128 >= nx);
+    const bool writer = out_pair && lane_in && (lane >= HL || sx == 0) && (lane <= 31 - HL || gs + SW >= nx);
     const int y0 = sy * A.H, y1 = min(y0 + A.H, ny);
     const int t0 = y0 - S, t1r = y1 - 1 + S;
     const size_t po = ((size_t)b * Pc + (size_t)(exists ? t : 0)) * (size_t)A.N;    // pair planes
     const size_t fo = ((size_t)b * A.T + (size_t)(exists ? t : 0)) * (size_t)A.N;   // frame t
     const float t1 = A.tau1, t2 = A.tau2, at1 = A.atau1, rsc = A.r_scale;
-    const float2 c1 = pk_dup(A.c1), c2 = pk_dup(A.c2), nc3 = pk_dup(-A.c3);
+    const float2 c1 = pk_dup(A.c1), c2 = pk_dup(A.c2);
+    const T nc3 = L::splat(-A.c3);
     const bool fix0 = A.fix_first && t == 0;                      // constant first frame
     const bool own_last = t == Pc - 1 && A.own_hi == Pc;          // also owns frame T-1 (writes, reductions)
-    const float2 nt1 = pk_dup(-t1), nt1h = make_float2(-t1, last_q ? 0.f : -t1);
+    const float2 nt1 = pk_dup(-t1);
+    const T nt1v = L::nt1x(-t1, last_q);                          // the pinned column nx-1 takes 0 (L3)
 
-    float4* sring = wpsm + (size_t)w * (C::warp_floats / 4) + lane;        // [slot][6][lane]
-    float4* pring = sring + kWpStateRing * 6 * 32;                          // [slot][2][lane]
-    float4* rbuf = wpsm + (size_t)kWpWarps * (C::warp_floats / 4);          // see WpCfg::rb_floats
-    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(rbuf + C::rb_floats / 4);   // [warp][buf]
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    const Quad zq = qd(z4);
+    Mv* sring = wpsm + (size_t)w * (C::warp_floats / V) + lane;           // [slot][6][lane]
+    Mv* pring = sring + kWpStateRing * 6 * 32;                             // [slot][2][lane]
+    Mv* rbuf = wpsm + (size_t)NW * (C::warp_floats / V);                   // see WpCfg::rb_floats
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(rbuf + C::rb_floats / V);   // [warp][buf]
+    Mv zm;
+    if constexpr (V == 4) zm = make_float4(0.f, 0.f, 0.f, 0.f); else zm = make_float2(0.f, 0.f);
+    const T zq = L::ld(zm);
     // neighbour slots: the same CTA (warp +- 1) or the adjacent CTA of the cluster; a neighbour
     // that is an empty slot (outside the chain or past the group's halo) sends nothing: its a is 0
     auto slot_exists = [&](int tt) { return tt >= 0 && tt < Pc && tt < hi + S; };
     const bool l_ex = has_l && slot_exists(t - 1), r_ex = has_r && slot_exists(t + 1);
-    const unsigned lw = w > 0 ? (unsigned)(w - 1) : (unsigned)(kWpWarps - 1);
-    const unsigned rw = w < kWpWarps - 1 ? (unsigned)(w + 1) : 0u;
+    const unsigned lw = w > 0 ? (unsigned)(w - 1) : (unsigned)(NW - 1);
+    const unsigned rw = w < NW - 1 ? (unsigned)(w + 1) : 0u;
     const unsigned lrank = w > 0 ? (unsigned)rank : (unsigned)(rank - 1);
-    const unsigned rrank = w < kWpWarps - 1 ? (unsigned)rank : (unsigned)(rank + 1);
+    const unsigned rrank = w < NW - 1 ? (unsigned)rank : (unsigned)(rank + 1);
     // byte offset of (step parity p2 = rel & 1, rel mod 3 = p3, side, level) for warp ww
     auto rboff = [&](int p2, int p3, int side, int lvl, unsigned ww) {
         const int k = lvl < S - 1 ? (p2 * 2 + side) * (S - 1) + lvl : 4 * (S - 1) + p3 * 2 + side;
-        return (unsigned)(((k * kWpWarps + (int)ww) * 32 + lane) * 16);
+        return (unsigned)(((k * NW + (int)ww) * 32 + lane) * VB);
     };
     const unsigned rb_base = smem_u32(rbuf), mb_base = smem_u32(mbar);
     const unsigned my_mb = mb_base + (unsigned)w * 16u;
-    const unsigned dummy = rb_base + (unsigned)((((4 * (S - 1) + 6) * kWpWarps + w) * 32 + lane) * 16);
+    const unsigned dummy = rb_base + (unsigned)((((4 * (S - 1) + 6) * NW + w) * 32 + lane) * VB);
     // pushes to the left neighbour land in its side 1 ("from the right"), to the right one in side 0;
     // a missing side's pushes go to the dummy slot and complete on this warp's own mbarrier
     const unsigned l_rb = l_ex ? map_rank(rb_base, lrank) : 0u, r_rb = r_ex ? map_rank(rb_base, rrank) : 0u;
     const unsigned l_mb = l_ex ? map_rank(mb_base + lw * 16u, lrank) : my_mb;
     const unsigned r_mb = r_ex ? map_rank(mb_base + rw * 16u, rrank) : my_mb;
-    const unsigned expect = 2u * S * 32u * 16u;                   // bytes per step and warp: both sides
+    const unsigned expect = 2u * S * 32u * VB;                    // bytes per step and warp: both sides
     const int nsteps = t1r - t0 + 1;                              // data of every step is exchanged
 
     auto issue = [&](int tr) {                                   // row tr -> state slot, p slot
         const bool ok = lane_in && tr >= 0 && tr < ny && tr <= t1r;
         const size_t ro = ok ? (size_t)tr * nx + gi : 0;
-        float4* s = sring + ((tr - t0) % kWpStateRing) * (6 * 32);
-        float4* pp = pring + (tr & (kWpPRing - 1)) * (2 * 32);
-        cp_async16(reinterpret_cast<float*>(s), A.mx_in + po + ro, ok);
-        cp_async16(reinterpret_cast<float*>(s + 32), A.my_in + po + ro, ok);
-        cp_async16(reinterpret_cast<float*>(s + 64), A.r_in + po + ro, ok);
-        cp_async16(reinterpret_cast<float*>(s + 96), A.a_in + po + ro, ok);
-        cp_async16(reinterpret_cast<float*>(s + 128), A.x_in + fo + ro, ok);
-        cp_async16(reinterpret_cast<float*>(s + 160), A.x_in + fo + A.N + ro, ok);
-        cp_async16(reinterpret_cast<float*>(pp), A.p + fo + ro, ok);
-        cp_async16(reinterpret_cast<float*>(pp + 32), A.p + fo + A.N + ro, ok);
+        Mv* s = sring + ((tr - t0) % kWpStateRing) * (6 * 32);
+        Mv* pp = pring + (tr & (kWpPRing - 1)) * (2 * 32);
+        L::cp(reinterpret_cast<float*>(s), A.mx_in + po + ro, ok);
+        L::cp(reinterpret_cast<float*>(s + 32), A.my_in + po + ro, ok);
+        L::cp(reinterpret_cast<float*>(s + 64), A.r_in + po + ro, ok);
+        L::cp(reinterpret_cast<float*>(s + 96), A.a_in + po + ro, ok);
+        L::cp(reinterpret_cast<float*>(s + 128), A.x_in + fo + ro, ok);
+        L::cp(reinterpret_cast<float*>(s + 160), A.x_in + fo + A.N + ro, ok);
+        L::cp(reinterpret_cast<float*>(pp), A.p + fo + ro, ok);
+        L::cp(reinterpret_cast<float*>(pp + 32), A.p + fo + A.N + ro, ok);
         cp_commit();
     };
 #pragma unroll
-    for (int k = 0; k < kWpStateRing * 6; ++k) sring[k * 32] = z4;
+    for (int k = 0; k < kWpStateRing * 6; ++k) sring[k * 32] = zm;
 #pragma unroll
-    for (int k = 0; k < kWpPRing * 2; ++k) pring[k * 32] = z4;
+    for (int k = 0; k < kWpPRing * 2; ++k) pring[k * 32] = zm;
     if (exists) {
 #pragma unroll
         for (int k = 0; k < P; ++k) issue(t0 + k);
@@ -197,7 +280,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 1) k_wave_prox(const WaveProxAr
         mbar_init(my_mb + 8, 1);
     }
     // receive slots start at zero (step t0's reads; a missing neighbour's side stays zero)
-    for (int k = 0; k < 4 * (S - 1) + 6; ++k) rbuf[((size_t)k * kWpWarps + w) * 32 + lane] = z4;
+    for (int k = 0; k < 4 * (S - 1) + 6; ++k) rbuf[((size_t)k * NW + w) * 32 + lane] = zm;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // phase 0 of both buffers: the data of steps t0, t0 + 1
     mbar_arm(my_mb, expect, lane == 0 && exists);
@@ -209,9 +292,9 @@ __global__ void __launch_bounds__(kWpWarps * 32, 1) k_wave_prox(const WaveProxAr
         return;
     }
 
-    struct Lv { Quad mx, my, r, a, nk, x0, x1; };
+    struct Lv { T mx, my, r, a, nk, x0, x1; };
     Lv SA[S], SB[S];
-    Quad upY[S + 1];
+    T upY[S + 1];
 #pragma unroll
     for (int j = 0; j < S; ++j) { SA[j] = {zq, zq, zq, zq, zq, zq, zq}; SB[j] = SA[j]; }
 #pragma unroll
@@ -225,14 +308,15 @@ __global__ void __launch_bounds__(kWpWarps * 32, 1) k_wave_prox(const WaveProxAr
         {
             issue(tr + P);
             cp_wait<P>();
-            const float4* s = sring + p3 * (6 * 32);            // (kWpStateRing == 3)
-            float4 Mx = s[0], My = s[32];
-            if (last_q) Mx.w = 0.f;                              // pinned flux components (L3)
-            if (tr == ny - 1) My = z4;
-            const float sh0 = __shfl_up_sync(kFull, Mx.w, 1);
-            const Quad qmy = qd(My), qr = qd(s[64]), x0 = qd(s[128]), x1 = qd(s[160]);
-            const Quad div0 = qadd(qdiff_left(qd(Mx), left_edge ? 0.f : sh0), qsub(qmy, upY[0]));
-            Cv[0].mx = qd(Mx); Cv[0].my = qmy; Cv[0].r = qr; Cv[0].a = qd(s[96]);
+            const Mv* s = sring + p3 * (6 * 32);                  // (kWpStateRing == 3)
+            Mv Mx = s[0], My = s[32];
+            if (last_q) L::zero_last(Mx);                         // pinned flux components (L3)
+            if (tr == ny - 1) My = zm;
+            const T qmx = L::ld(Mx);
+            const float sh0 = __shfl_up_sync(kFull, L::last(qmx), 1);
+            const T qmy = L::ld(My), qr = L::ld(s[64]), x0 = L::ld(s[128]), x1 = L::ld(s[160]);
+            const T div0 = qadd(qdiff_left(qmx, left_edge ? 0.f : sh0), qsub(qmy, upY[0]));
+            Cv[0].mx = qmx; Cv[0].my = qmy; Cv[0].r = qr; Cv[0].a = L::ld(s[96]);
             Cv[0].x0 = x0; Cv[0].x1 = x1;
             Cv[0].nk = qadd(qsub(qr, div0), qsub(x1, x0));       // -K^0 = (r - div M) + (x_{t+1} - x_t)
             upY[0] = qmy;
@@ -243,9 +327,9 @@ __global__ void __launch_bounds__(kWpWarps * 32, 1) k_wave_prox(const WaveProxAr
             mbar_arm(my_mb + ibuf * 8, expect, lane == 0 && rel + 1 <= nsteps - 1);
             __syncwarp();
         }
-        auto publish = [&](int lvl, const Quad& v) {
-            st_async4(l_ex ? l_rb + rboff(obuf, p3, 1, lvl, lw) : dummy, f4(v), l_mb + obuf * 8);
-            st_async4(r_ex ? r_rb + rboff(obuf, p3, 0, lvl, rw) : dummy, f4(v), r_mb + obuf * 8);
+        auto publish = [&](int lvl, const T& v) {
+            st_async_v(l_ex ? l_rb + rboff(obuf, p3, 1, lvl, lw) : dummy, L::st(v), l_mb + obuf * 8);
+            st_async_v(r_ex ? r_rb + rboff(obuf, p3, 0, lvl, rw) : dummy, L::st(v), r_mb + obuf * 8);
         };
         {
             publish(0, Cv[0].a);
@@ -254,52 +338,47 @@ __global__ void __launch_bounds__(kWpWarps * 32, 1) k_wave_prox(const WaveProxAr
                 const int rho = tr - j;
                 const Lv& p = Pv[j - 1];
                 // the neighbours' a^{j-1} at row rho (published at step tr - 1)
-                const Quad anl = qd(rbuf[rboff(ibuf, q3, 0, j - 1, w) / 16]);
-                const Quad anr = qd(rbuf[rboff(ibuf, q3, 1, j - 1, w) / 16]);
-                Quad n2, inv, nmx, nmy, rn;
+                const T anl = L::ld(rbuf[rboff(ibuf, q3, 0, j - 1, w) / VB]);
+                const T anr = L::ld(rbuf[rboff(ibuf, q3, 1, j - 1, w) / VB]);
+                T n2, inv, nmx, nmy, rn;
                 {
-                    Quad qx, qy;
-                    const Quad cA = Cv[j - 1].a;
+                    T qx, qy;
+                    const T cA = Cv[j - 1].a;
                     const float2 nt1y = pk_dup((rho == -1 || rho == ny - 1) ? 0.f : -t1);
-                    const float a5 = __shfl_down_sync(kFull, p.a.l.x, 1);
-                    const Quad gx = qdiff_right(p.a, a5), gy = qsub(p.a, cA);
-                    qx = {pk_fma(nt1, gx.l, p.mx.l), pk_fma(nt1h, gx.h, p.mx.h)};
+                    const float a5 = __shfl_down_sync(kFull, L::first(p.a), 1);
+                    const T gx = qdiff_right(p.a, a5), gy = qsub(p.a, cA);
+                    qx = qfma(nt1v, gx, p.mx);
                     qy = qfma(nt1y, gy, p.my);
                     n2 = qfma(qy, qy, qmul(qx, qx));
-                    inv = {make_float2(rsqrt_ftz(n2.l.x), rsqrt_ftz(n2.l.y)), make_float2(rsqrt_ftz(n2.h.x), rsqrt_ftz(n2.h.y))};
-                    Quad sf = qfma(nt1, inv, qd(make_float4(1.f, 1.f, 1.f, 1.f)));
-                    sf = {make_float2(fmaxf(sf.l.x, 0.f), fmaxf(sf.l.y, 0.f)), make_float2(fmaxf(sf.h.x, 0.f), fmaxf(sf.h.y, 0.f))};
+                    inv = L::rsq(n2);
+                    const T sf = L::relu(qfma(nt1, inv, L::splat(1.f)));
                     nmx = qmul(sf, qx); nmy = qmul(sf, qy);
-                    const Quad q5 = qfma(pk_dup(t1), p.a, p.r);
+                    const T q5 = qfma(pk_dup(t1), p.a, p.r);
                     if constexpr (RM == 0) {
-                        const Quad cl = {make_float2(fminf(fmaxf(q5.l.x, -at1), at1), fminf(fmaxf(q5.l.y, -at1), at1)),
-                                         make_float2(fminf(fmaxf(q5.h.x, -at1), at1), fminf(fmaxf(q5.h.y, -at1), at1))};
-                        rn = qsub(q5, cl);
+                        rn = qsub(q5, L::clampv(q5, at1));
                     } else if constexpr (RM == 1) {
-                        rn = qmul(q5, qd(make_float4(rsc, rsc, rsc, rsc)));
+                        rn = qmul(q5, L::splat(rsc));
                     } else {
                         rn = zq;
                     }
                 }
                 // line 4: x_t, x_{t+1} from a_{t-1}, a_t, a_{t+1} of level j-1
-                const float4* pr = pring + (rho & (kWpPRing - 1)) * (2 * 32);
-                const Quad p0 = qd(pr[0]), p1 = qd(pr[32]);
-                Quad x0n = qfma(c1, p0, qfma(c2, p.x0, qmul(qd(make_float4(nc3.x, nc3.x, nc3.x, nc3.x)), qsub(p.a, anl))));
-                x0n = {make_float2(fmaxf(x0n.l.x, 0.f), fmaxf(x0n.l.y, 0.f)), make_float2(fmaxf(x0n.h.x, 0.f), fmaxf(x0n.h.y, 0.f))};
+                const Mv* pr = pring + (rho & (kWpPRing - 1)) * (2 * 32);
+                const T p0 = L::ld(pr[0]), p1 = L::ld(pr[32]);
+                T x0n = L::relu(qfma(c1, p0, qfma(c2, p.x0, qmul(nc3, qsub(p.a, anl)))));
                 if (fix0) x0n = p.x0;
-                Quad x1n = qfma(c1, p1, qfma(c2, p.x1, qmul(qd(make_float4(nc3.x, nc3.x, nc3.x, nc3.x)), qsub(anr, p.a))));
-                x1n = {make_float2(fmaxf(x1n.l.x, 0.f), fmaxf(x1n.l.y, 0.f)), make_float2(fmaxf(x1n.h.x, 0.f), fmaxf(x1n.h.y, 0.f))};
-                const Quad fn = qsub(x1n, x0n);
+                const T x1n = L::relu(qfma(c1, p1, qfma(c2, p.x1, qmul(nc3, qsub(anr, p.a)))));
+                const T fn = qsub(x1n, x0n);
                 // lines 6-7: -K^j = (r^j - div M^j) + (x_{t+1} - x_t);  a^j = a^{j-1} + tau2 (2 K^j - K^{j-1})
-                const float shl = __shfl_up_sync(kFull, nmx.h.y, 1);
-                const Quad divn = qadd(qdiff_left(nmx, left_edge ? 0.f : shl), qsub(nmy, upY[j]));
-                const Quad nkn = qadd(qsub(rn, divn), fn);
-                const Quad an = qfma(pk_dup(t2), qfma(pk_dup(-2.f), nkn, p.nk), p.a);
+                const float shl = __shfl_up_sync(kFull, L::last(nmx), 1);
+                const T divn = qadd(qdiff_left(nmx, left_edge ? 0.f : shl), qsub(nmy, upY[j]));
+                const T nkn = qadd(qsub(rn, divn), fn);
+                const T an = qfma(pk_dup(t2), qfma(pk_dup(-2.f), nkn, p.nk), p.a);
                 if (RED && j == S) {
                     const float wr = (writer && rho >= y0 && rho < y1) ? 1.f : 0.f;
                     const float wl = own_last ? wr : 0.f;
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
+                    for (int v = 0; v < V; ++v) {
                         const float n2v = qc(n2, v), invv = qc(inv, v), rv = qc(rn, v), kv = qc(nkn, v);
                         const float nrm = fmaxf(fmaf(n2v, fminf(invv, 1e30f), -t1), 0.f);
                         const float dmx = qc(nmx, v) - qc(p.mx, v), dmy = qc(nmy, v) - qc(p.my, v), dr = rv - qc(p.r, v);
@@ -323,12 +402,12 @@ __global__ void __launch_bounds__(kWpWarps * 32, 1) k_wave_prox(const WaveProxAr
                 } else {
                     const bool wp = writer && rho >= y0 && rho < y1;
                     const size_t go = (size_t)rho * nx + gi;
-                    st4_if(A.mx_out + po + go, f4(nmx), wp);
-                    st4_if(A.my_out + po + go, f4(nmy), wp);
-                    st4_if(A.r_out + po + go, f4(rn), wp);
-                    st4_if(A.a_out + po + go, f4(an), wp);
-                    st4_if(A.x_out + fo + go, f4(x0n), wp);
-                    st4_if(A.x_out + fo + A.N + go, f4(x1n), wp && own_last);
+                    L::st_if(A.mx_out + po + go, nmx, wp);
+                    L::st_if(A.my_out + po + go, nmy, wp);
+                    L::st_if(A.r_out + po + go, rn, wp);
+                    L::st_if(A.a_out + po + go, an, wp);
+                    L::st_if(A.x_out + fo + go, x0n, wp);
+                    L::st_if(A.x_out + fo + A.N + go, x1n, wp && own_last);
                 }
             }
         }

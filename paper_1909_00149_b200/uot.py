@@ -226,6 +226,12 @@ class Problem:
         iterations per pass), 'k_wave2' / 'k_wave4' (register wavefront) or 'k_persist'."""
         return self.PATH_NAMES[int(lib().uot_kernel_path(self._ctx))]
 
+    @property
+    def wave_cols(self) -> int:
+        """Strip width of the register-wavefront passes: 128 (k_wave_pk), 64 (k_wave_n, narrow
+        strips) or 0 (no wavefront passes); include/uot.h uot_wave_cols."""
+        return int(lib().uot_wave_cols(self._ctx))
+
     def set_own_pairs(self, lo: int, hi: int):
         """Chain prox on k_wave_prox: only pairs [lo, hi) are written and reduced; the others are
         ghost copies of neighbouring shards' pairs, refreshed by the caller after each pass

@@ -588,27 +588,64 @@ def test_graph_capture_replays_iterations(env):
 
 
 # ------------------------------------------------------------------ k_wave edge shapes
-@pytest.mark.parametrize("shape", [(1, 2, 1, 8), (1, 2, 3, 4), (2, 3, 5, 116), (1, 2, 130, 228), (3, 2, 17, 240)],
+@pytest.mark.parametrize("shape", [(1, 2, 1, 8), (1, 2, 3, 4), (2, 3, 5, 116), (1, 2, 130, 228), (3, 2, 17, 240),
+                                   (1, 2, 9, 56), (1, 2, 21, 60), (2, 2, 7, 64), (1, 2, 19, 68), (1, 3, 33, 256)],
                          ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("costs", ["1.155,1.15,1.137,1.35", "9,9,9,0.1"], ids=["default", "S5"])
-@pytest.mark.parametrize("pk", [1, 0], ids=["packed", "scalar"])
+@pytest.mark.parametrize("pk", [1, 0, "narrow"], ids=["packed", "scalar", "narrow"])
 def test_wave_edge_shapes(shape, costs, pk):
     """The register wavefront on degenerate / ragged grids: one row, rows < S, one quad per
-    row, widths just under / over one 112- or 120-column strip, with 16-row segments and
-    reductions every 10 and 7 iterations; the packed fp32x2 kernel (k_wave_pk, default) and
-    the scalar k_wave."""
+    row, widths just under / over one 112- or 120-column strip (52 / 56 / 60 for the 64-column
+    strips), with 16-row segments and reductions every 10 and 7 iterations; the packed fp32x2
+    kernel (k_wave_pk), the scalar k_wave and the narrow-strip k_wave_n."""
     B, T, ny, nx = shape
     fr = inputs.gen_random(B, T, ny, nx, seed=3 + ny + nx, kind="uniform")
     tau = tau_for(ny, nx)
+    env = {"UOT_SINGLE": 0, "UOT_WAVE": 1, "UOT_TPERSIST": 0, "UOT_PERSIST": 0, "UOT_WAVE_H": 16, "UOT_PASS_COST": costs}
+    env.update({"UOT_WAVE_PK": 1, "UOT_WAVE_V": 2} if pk == "narrow" else {"UOT_WAVE_PK": pk, "UOT_WAVE_V": 4})
     for n, check in ((30, 10), (23, 7)):
-        prob, st, rep = gpu_run(fr, 1.2, n, tau, env={"UOT_SINGLE": 0, "UOT_WAVE": 1, "UOT_TPERSIST": 0, "UOT_PERSIST": 0,
-                                                     "UOT_WAVE_H": 16, "UOT_PASS_COST": costs, "UOT_WAVE_PK": pk},
-                                check_every=check)
+        prob, st, rep = gpu_run(fr, 1.2, n, tau, env=env, check_every=check)
         assert prob.kernel_path.startswith("k_wave")
+        assert prob.wave_cols == (64 if pk == "narrow" else 128)
         ref, rrep = oracle.iterate(fr, 1.2, math.inf, tau, tau, n)
         compare(fr, st, ref)
         assert rep["iterations"] == n and np.isfinite(rep["objective"])
         assert rep["objective"] == pytest.approx(rrep[:, 0].sum() + 1.2 * rrep[:, 1].sum(), rel=OBJ_RTOL, abs=1e-6)
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 150, 200), (1, 3, 77, 256), (1, 2, 40, 1024)], ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("costs", ["1.155,1.15,1.137,1.35", "9,9,9,0.1", "1.2,9,1.26,9", "9,0.1,9,9"],
+                         ids=["default", "S5", "S3", "S4"])
+def test_narrow_strips_equal_quad_strips(shape, costs):
+    """k_wave_n (64-column strips, one fp32x2 pair per lane) runs k_wave_pk's arithmetic per
+    pixel op for op: the iterates are EQUAL (bitwise up to the sign of zero) for every pass
+    length, with reductions every 10 iterations; the reductions agree to fp32 rounding."""
+    B, T, ny, nx = shape
+    fr = inputs.gen_random(B, T, ny, nx, seed=11 + nx, kind="sparse")
+    tau = tau_for(ny, nx)
+    base = {"UOT_SINGLE": 0, "UOT_WAVE": 1, "UOT_TPERSIST": 0, "UOT_PERSIST": 0, "UOT_PASS_COST": costs}
+    p4, st4, rep4 = gpu_run(fr, 0.8, 40, tau, env={**base, "UOT_WAVE_V": 4}, check_every=10)
+    p2, st2, rep2 = gpu_run(fr, 0.8, 40, tau, env={**base, "UOT_WAVE_V": 2}, check_every=10)
+    assert (p4.wave_cols, p2.wave_cols) == (128, 64)
+    for k in ("mx", "my", "r", "a"):
+        assert np.array_equal(st4[k], st2[k]), (k, np.abs(st4[k] - st2[k]).max())
+    for k in ("objective", "primal_res", "dual_res"):
+        assert rep2[k] == pytest.approx(rep4[k], rel=1e-5, abs=1e-9), k
+
+
+def test_wave_strip_width_model():
+    """The host's strip-width model (wave_cost with the measured per-pixel throughput of the
+    narrow strips, 0.76 of k_wave_pk's): C3's 256-column rows and C4's 1024-column rows keep the
+    128-column strips (5 x 64 computed columns vs 3 x 128 does not pay; 20 x 64 vs 9 x 128),
+    136-column rows take the narrow ones (3 x 64 vs 2 x 128); include/uot.h uot_wave_cols."""
+    p3 = Problem(torch.zeros((1, 64, 256, 256), device="cuda"), 0.3, tau1=0.1, tau2=0.1)
+    assert p3.wave_cols == 128
+    del p3
+    p4 = Problem(torch.zeros((1, 256, 1024, 1024), device="cuda"), 0.3, tau1=0.1, tau2=0.1)
+    assert p4.wave_cols == 128
+    del p4
+    p5 = Problem(torch.zeros((1, 128, 512, 136), device="cuda"), 0.3, tau1=0.1, tau2=0.1)
+    assert p5.wave_cols == 64
 
 
 # ------------------------------------------------------------------ randomized differential test
@@ -631,6 +668,7 @@ def test_random_pass_schedules_match_one_pass_kernel():
         env = {"UOT_PERSIST": 0}
         if path == "wave":
             env.update(UOT_WAVE=1, UOT_TPERSIST=0, UOT_WAVE_H=int(rng.choice([16, 32, 64, 128])),
+                       UOT_WAVE_V=int(rng.choice([0, 2, 4])),
                        UOT_PASS_COST=",".join(f"{c:.2f}" for c in rng.uniform(0.5, 2.0, 4)))
         elif path == "tiles":
             env.update(UOT_WAVE=0, UOT_TPERSIST=0)

@@ -57,11 +57,15 @@ CASES = [
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c[:4])) + "-" + "-".join(
     f"{k[4:]}{v}" for k, v in c[6].items()))
 @pytest.mark.parametrize("n,check", [(41, 10), (30, 7)])
-def test_prox_wave_matches_k_iter_and_oracle(case, n, check, monkeypatch):
+@pytest.mark.parametrize("layout", [{}, {"UOT_PROX_V": 2}, {"UOT_PROX_V": 2, "UOT_PROX_W": 16}],
+                         ids=["V4W8", "V2W12", "V2W16"])
+def test_prox_wave_matches_k_iter_and_oracle(case, n, check, layout, monkeypatch):
+    """Every lane layout of k_wave_prox: 128-column strips with 8 pairs per CTA (default),
+    64-column strips with 12 or 16."""
     B, T, ny, nx, alpha, rho, env = case
     fr = inputs.gen_random(B, T, ny, nx, seed=T * 13 + nx, kind="sparse")
     tau = oracle.default_steps(nx, ny, prox=True, n_frames=T, safety=0.95)[0]
-    pw, rw = _run(fr, alpha, rho, tau, n, {**WAVE, **env}, monkeypatch, check)
+    pw, rw = _run(fr, alpha, rho, tau, n, {**WAVE, **env, **layout}, monkeypatch, check)
     assert pw.kernel_path == "k_wave_prox"
     pi, ri = _run(fr, alpha, rho, tau, n, {**NO_WAVE, "UOT_PERSIST": 0}, monkeypatch, check)
     assert pi.kernel_path == "k_iter"
