@@ -4,6 +4,9 @@
 
   python scripts/ncu_summary.py launches <launches.csv> <out.md>
   python scripts/ncu_summary.py full <report.ncu-rep> <config> <alg_bytes_per_launch> <out.json> [kernel-substring]
+  python scripts/ncu_summary.py stalls <source-page.csv[.gz]> <config> <out.json>
+      (warp-stall sampling by reason and the hottest SASS lines, from `ncu -i R --page source
+       --csv --print-source sass`, merged into the config's entry)
 """
 import collections
 import csv
@@ -89,8 +92,43 @@ def full(rep, config, alg_bytes, out, pick=None):
     print(json.dumps(summ, indent=1))
 
 
+def stalls(path, config, out, top=12):
+    import gzip
+    raw = gzip.open(path, "rt").read() if path.endswith(".gz") else open(path).read()
+    lines = raw.splitlines()
+    start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
+    rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
+    hdr, rows = rows[0], rows[1:]
+    ix = {h: i for i, h in enumerate(hdr)}
+    cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+    tot = collections.Counter()
+    for r in rows:
+        for c in cols:
+            try:
+                tot[c] += float(r[ix[c]])
+            except ValueError:
+                pass
+    T = sum(tot.values()) or 1.0
+    key = "Warp Stall Sampling (All Samples)"
+    hot = sorted(rows, key=lambda r: -float(r[ix[key]] or 0))[:top]
+    summ = {"source_page": path, "samples": T,
+            "by_reason": {c: round(v / T, 3) for c, v in tot.most_common() if v},
+            "hottest": [{"sass": r[ix["Source"]].strip(), "samples": float(r[ix[key]] or 0),
+                         "reasons": {c: float(r[ix[c]]) for c in cols if r[ix[c]] not in ("0", "")}} for r in hot]}
+    allp = {}
+    try:
+        allp = json.load(open(out))
+    except Exception:
+        pass
+    allp.setdefault(config, {})["stalls"] = summ
+    json.dump(allp, open(out, "w"), indent=1)
+    print(json.dumps(summ, indent=1)[:3000])
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "stalls":
+        stalls(sys.argv[2], sys.argv[3], sys.argv[4])
     else:
         full(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5], sys.argv[6] if len(sys.argv) > 6 else None)
