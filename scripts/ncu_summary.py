@@ -4,7 +4,7 @@
 
   python scripts/ncu_summary.py launches <launches.csv> <out.md>
   python scripts/ncu_summary.py full <report.ncu-rep> <config> <alg_bytes_per_launch> <out.json> [kernel-substring]
-  python scripts/ncu_summary.py stalls <source-page.csv[.gz]> <config> <out.json>
+  python scripts/ncu_summary.py stalls <source-page.csv[.gz]> <config> <out.json> [kernel-substring]
       (warp-stall sampling by reason and the hottest SASS lines, from `ncu -i R --page source
        --csv --print-source sass`, merged into the config's entry)
 """
@@ -92,10 +92,16 @@ def full(rep, config, alg_bytes, out, pick=None):
     print(json.dumps(summ, indent=1))
 
 
-def stalls(path, config, out, top=12):
+def stalls(path, config, out, top=12, pick=None):
+    """The source page of the first kernel in the export (or the first whose name contains pick)."""
     import gzip
     raw = gzip.open(path, "rt").read() if path.endswith(".gz") else open(path).read()
     lines = raw.splitlines()
+    heads = [i for i, l in enumerate(lines) if l.startswith('"Kernel Name"')] + [len(lines)]
+    sec = 0
+    if pick is not None:
+        sec = next(k for k in range(len(heads) - 1) if pick in lines[heads[k]])
+    lines = lines[heads[sec]:heads[sec + 1]] if len(heads) > 1 else lines
     start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
     rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
     hdr, rows = rows[0], rows[1:]
@@ -111,7 +117,7 @@ def stalls(path, config, out, top=12):
     T = sum(tot.values()) or 1.0
     key = "Warp Stall Sampling (All Samples)"
     hot = sorted(rows, key=lambda r: -float(r[ix[key]] or 0))[:top]
-    summ = {"source_page": path, "samples": T,
+    summ = {"source_page": path, "kernel": lines[0].split(",", 1)[-1].strip().strip(',').strip('"'), "samples": T,
             "by_reason": {c: round(v / T, 3) for c, v in tot.most_common() if v},
             "hottest": [{"sass": r[ix["Source"]].strip(), "samples": float(r[ix[key]] or 0),
                          "reasons": {c: float(r[ix[c]]) for c in cols if r[ix[c]] not in ("0", "")}} for r in hot]}
@@ -129,6 +135,6 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     elif sys.argv[1] == "stalls":
-        stalls(sys.argv[2], sys.argv[3], sys.argv[4])
+        stalls(sys.argv[2], sys.argv[3], sys.argv[4], pick=sys.argv[5] if len(sys.argv) > 5 else None)
     else:
         full(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5], sys.argv[6] if len(sys.argv) > 6 else None)
