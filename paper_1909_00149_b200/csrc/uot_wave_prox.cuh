@@ -6,7 +6,8 @@
 // coupling across pairs is pointwise; across pixels it is the 5-point stencil of k_wave).
 //
 // Layout: the register wavefront of k_wave_pk (uot_wave_pk.cuh) runs one warp per pair --
-// a 128-column strip marching down H + 2S rows, level j updating row rho - j at step rho --
+// a strip of 32 V columns (V = 4 by default: 128 columns; V = 2: 64) marching down H + 2S rows,
+// level j updating row rho - j at step rho --
 // and the warps of consecutive pairs advance together.  Level j at step rho needs the
 // neighbour pairs' a^{j-1} at row rho - j, which the neighbours produced at step rho - 1:
 // each warp PUSHES its a^0 .. a^{S-1} of a step into both neighbours' receive buffers with
@@ -21,14 +22,15 @@
 // branch with convergence barriers): a warp without a neighbour on a side pushes that side's
 // bytes into a private dummy slot, completing them on its own mbarrier, and the receive slots
 // of a missing neighbour stay zero from the start (a = 0 there: chain end, L19).  The last
-// step's pushes are waited for too, so no push reaches a CTA that has exited.  Frames are recomputed by both pairs that use them: the warp of
+// step's pushes are waited for too, so no push reaches a CTA that has exited.  Frames are
+// recomputed by both pairs that use them: the warp of
 // pair t carries x_t and x_{t+1} per level (bit-identical to its neighbours' copies: same
 // inputs, same operations), so nothing is exchanged within a step.
 //
-// Pair groups: a cluster of CL CTAs x 8 warps holds CL*8 consecutive pairs of one chain (the
-// CTA-boundary neighbours sit in the adjacent CTA's shared memory).  After S levels a pair is
-// exact iff its S neighbours on both sides are in the group (the dependency cone), so a group
-// writes the middle CL*8 - 2S pairs; pairs outside the chain (t < 0, t >= P) are empty slots
+// Pair groups: a cluster of CL CTAs x NW warps (NW = 8 at V = 4; 12 or 16 at V = 2) holds CL*NW
+// consecutive pairs of one chain (the CTA-boundary neighbours sit in the adjacent CTA's shared
+// memory).  After S levels a pair is exact iff its S neighbours on both sides are in the group
+// (the dependency cone), so a group writes the middle CL*NW - 2S pairs; pairs outside the chain (t < 0, t >= P) are empty slots
 // whose a is the chain end's a_{-1} = a_{T-1} := 0 exactly (L19).  HBM traffic per pass and
 // pair-pixel: M, r, a, x_t, p_t read (x_{t+1}, p_{t+1} are the next pair's, L2 hits) and M, r,
 // a, x_t written: 44 B per S iterations, plus the 2S halo pairs of each group.
