@@ -115,7 +115,15 @@ template <int S, int V = 4, int NW = (V == 4 ? 8 : 16)> struct WpCfg {
     // receive buffers: levels 0 .. S-2 [2 bufs][2 sides][S-1][warp][lane], level S-1 [3 bufs][2 sides][warp][lane],
     // then one dummy slot per warp [warp][lane]
     static constexpr size_t rb_floats = (size_t)(2 * 2 * (S - 1) + 3 * 2 + 1) * W * 32 * V;
-    static constexpr size_t smem = (warp_floats * W + rb_floats) * sizeof(float) + W * 2 * 8;
+#ifndef UOT_PROX_UY
+#define UOT_PROX_UY 1
+#endif
+    // UOT_PROX_UY (default 1): each level's M_y of the previous row (div M's upper neighbour) in
+    // shared memory instead of registers -- frees 16 registers per thread at S = 3 (spills 60 / 136
+    // -> 48 / 80 B) and measured 1.831e11 vs 1.820e11 px-it/s on C4 chain prox (passes of 2), 1.731e11
+    // vs 1.713e11 (3-first), the same on two repeats (scripts/gpu_r02c_ab_uy.sh)
+    static constexpr size_t uy_floats = UOT_PROX_UY ? (size_t)(S + 1) * 32 * V : 0;
+    static constexpr size_t smem = (warp_floats * W + rb_floats + uy_floats * W) * sizeof(float) + W * 2 * 8;
 };
 
 struct WaveProxArgs {
@@ -296,11 +304,14 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_wave_prox(const WaveProxArgs A)
 
     struct Lv { T mx, my, r, a, nk, x0, x1; };
     Lv SA[S], SB[S];
-    T upY[S + 1];
+    T upY_r[UOT_PROX_UY ? 1 : S + 1];
+    Mv* const uyb = reinterpret_cast<Mv*>(mbar + NW * 2) + (size_t)w * (S + 1) * 32 + lane;
+    auto upy_get = [&](int j) -> T { if constexpr (UOT_PROX_UY != 0) return L::ld(uyb[j * 32]); else return upY_r[j]; };
+    auto upy_set = [&](int j, const T& v) { if constexpr (UOT_PROX_UY != 0) uyb[j * 32] = L::st(v); else upY_r[j] = v; };
 #pragma unroll
     for (int j = 0; j < S; ++j) { SA[j] = {zq, zq, zq, zq, zq, zq, zq}; SB[j] = SA[j]; }
 #pragma unroll
-    for (int j = 0; j <= S; ++j) upY[j] = zq;
+    for (int j = 0; j <= S; ++j) upy_set(j, zq);
     float s_tr = 0.f, s_gr = 0.f, s_k2 = 0.f, s_dz = 0.f, s_ub = 0.f, s_px = 0.f;
 
     auto step = [&](const int tr, Lv (&Pv)[S], Lv (&Cv)[S]) {
@@ -317,11 +328,11 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_wave_prox(const WaveProxArgs A)
             const T qmx = L::ld(Mx);
             const float sh0 = __shfl_up_sync(kFull, L::last(qmx), 1);
             const T qmy = L::ld(My), qr = L::ld(s[64]), x0 = L::ld(s[128]), x1 = L::ld(s[160]);
-            const T div0 = qadd(qdiff_left(qmx, left_edge ? 0.f : sh0), qsub(qmy, upY[0]));
+            const T div0 = qadd(qdiff_left(qmx, left_edge ? 0.f : sh0), qsub(qmy, upy_get(0)));
             Cv[0].mx = qmx; Cv[0].my = qmy; Cv[0].r = qr; Cv[0].a = L::ld(s[96]);
             Cv[0].x0 = x0; Cv[0].x1 = x1;
             Cv[0].nk = qadd(qsub(qr, div0), qsub(x1, x0));       // -K^0 = (r - div M) + (x_{t+1} - x_t)
-            upY[0] = qmy;
+            upy_set(0, qmy);
         }
         // the neighbours' pushes of step tr - 1 have landed; re-arm that buffer for step tr + 1
         if (rel > 0) {
@@ -373,7 +384,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_wave_prox(const WaveProxArgs A)
                 const T fn = qsub(x1n, x0n);
                 // lines 6-7: -K^j = (r^j - div M^j) + (x_{t+1} - x_t);  a^j = a^{j-1} + tau2 (2 K^j - K^{j-1})
                 const float shl = __shfl_up_sync(kFull, L::last(nmx), 1);
-                const T divn = qadd(qdiff_left(nmx, left_edge ? 0.f : shl), qsub(nmy, upY[j]));
+                const T divn = qadd(qdiff_left(nmx, left_edge ? 0.f : shl), qsub(nmy, upy_get(j)));
                 const T nkn = qadd(qsub(rn, divn), fn);
                 const T an = qfma(pk_dup(t2), qfma(pk_dup(-2.f), nkn, p.nk), p.a);
                 if (RED && j == S) {
@@ -396,7 +407,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_wave_prox(const WaveProxArgs A)
                         s_px = fmaf(wl, e1 * e1, s_px);
                     }
                 }
-                upY[j] = nmy;
+                upy_set(j, nmy);
                 if (j < S) {
                     Cv[j].mx = nmx; Cv[j].my = nmy; Cv[j].r = rn; Cv[j].a = an; Cv[j].nk = nkn;
                     Cv[j].x0 = x0n; Cv[j].x1 = x1n;
