@@ -108,3 +108,42 @@ def test_rpca_long_video_sharded_bitwise():
         _check_bitwise(full, sh, ranges, signed=False)
     finally:
         os.environ.pop("UOT_PERSIST", None)
+
+
+@pytest.mark.parametrize("ny,nx", [(8, 8), (128, 128)], ids=["8x8", "128x128"])
+def test_rpca_long_video_sharded_bitwise_frames(ny, nx):
+    """The sharded runs read M from the gathered plane, the unsharded one from L + D: at 128 x 128
+    (3 frame blocks x 512 pixel chunks of the line-10 apply, more CTAs than fit the GPU at once)
+    the two stay bitwise equal only if line 13 (D = M - T) waits for every block's reads of M
+    (k_rp_dupdate after the apply; writing D inside the apply raced with the other blocks)."""
+    import os
+    from test_rpca_shard_gpu import _check_bitwise, _emulated, _make
+    os.environ["UOT_PERSIST"] = "0"
+    try:
+        from paper_1909_00149_b200 import inputs
+        Y, phi, _, _ = inputs.gen_rpca(150, ny, nx, seed=23, K=2, observed=0.8)
+        full = _make(Y, phi)
+        full.solve(6, 0.0, 3)
+        sh, ranges, _ = _emulated(Y, phi, (0, 50, 100), 6, 3, 0.0)
+        _check_bitwise(full, sh, ranges, signed=False)
+    finally:
+        os.environ.pop("UOT_PERSIST", None)
+
+
+def test_rpca_long_video_large_frames_multiwave():
+    """T = 160 frames of 128 x 128: the line-10 apply runs 3 frame blocks x 512 pixel chunks, more
+    CTAs than fit the GPU at once, so the blocks of one pixel chunk run at different times.  Line 13
+    (D = M - T) must not overwrite D before every block has read M = L + D (k_rp_dupdate runs after
+    the apply); checked against the oracle's exact SVT with the subspace certificate holding."""
+    from paper_1909_00149_b200 import inputs
+    Y, phi, _, _ = inputs.gen_rpca(160, 128, 128, seed=12, K=3, observed=0.9)
+    prm = dict(PRM, gamma=2.0)
+    n = 50                     # (the one-step-per-iteration subspace tracks the SVT after the first tens)
+    prob, rep = _gpu(Y, phi, prm, n, check=10)
+    tau = prm["gamma"] / prm["rho"]
+    assert 0.0 <= rep["svt_min_ritz"] < tau * tau
+    st_o, res, nuc = _oracle(Y, phi, prm, n)
+    st_g = {k: v.double().cpu().numpy() for k, v in prob.state().items()}
+    _compare(Y, st_g, st_o)
+    obj = _oracle_objective(Y.astype(np.float64), phi, st_o, nuc[-1], prm)
+    assert rep["objective"] == pytest.approx(obj, rel=1e-4)
