@@ -130,12 +130,13 @@ def test_rpca_long_video_sharded_bitwise_frames(ny, nx):
         os.environ.pop("UOT_PERSIST", None)
 
 
-def test_rpca_long_video_large_frames_multiwave():
+def test_rpca_long_video_large_frames_multiwave(monkeypatch):
     """T = 160 frames of 128 x 128: the line-10 apply runs 3 frame blocks x 512 pixel chunks, more
     CTAs than fit the GPU at once, so the blocks of one pixel chunk run at different times.  Line 13
     (D = M - T) must not overwrite D before every block has read M = L + D (k_rp_dupdate runs after
     the apply); checked against the oracle's exact SVT with the subspace certificate holding."""
     from paper_1909_00149_b200 import inputs
+    monkeypatch.setenv("UOT_RPCA_K", "128")      # (the noisy 128 x 128 frames keep ~100 singular values above tau)
     Y, phi, _, _ = inputs.gen_rpca(160, 128, 128, seed=12, K=3, observed=0.9)
     prm = dict(PRM, gamma=2.0)
     n = 50                     # (the one-step-per-iteration subspace tracks the SVT after the first tens)
