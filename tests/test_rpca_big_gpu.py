@@ -30,9 +30,10 @@ def _gpu(Y, phi, prm, n, eps=0.0, check=None, shard=None):
     return prob, rep
 
 
-@pytest.mark.parametrize("T,ny,nx,masked", [(160, 8, 8, True), (200, 4, 16, False), (129, 6, 8, True)])
+@pytest.mark.parametrize("T,ny,nx,masked", [(160, 8, 8, True), (200, 4, 16, False), (129, 6, 8, True), (140, 5, 7, True)])
 def test_rpca_long_video_exact_subspace(T, ny, nx, masked):
-    """T > 128 (the one-CTA Jacobi limit), rank(M) <= N <= 64 = k: the subspace SVT is exact."""
+    """T > 128 (the one-CTA Jacobi limit), rank(M) <= N <= 64 = k: the subspace SVT is exact.
+    (5 x 7: N % 4 != 0 -- the unpipelined Gram, the lane-per-pixel apply and the scalar line 13.)"""
     from paper_1909_00149_b200 import inputs
     Y, phi, _, _ = inputs.gen_rpca(T, ny, nx, seed=T + nx, K=2, observed=0.8)
     if not masked:
